@@ -1,0 +1,1339 @@
+// mrlbm_oracle.cpp — CPU ORACLE for the adaptive MR-LBM time step.
+//
+// TEST INFRASTRUCTURE ONLY.  Nothing in the product (paper_2103_02903_b200/)
+// links, loads or calls this file; only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs do, as the checker.
+//
+// The reference (/root/reference/proj/core/include/mrlbm) ships the mesh and MR
+// primitives only; the step itself exists there as prose (SPEC.md, PAPER.md
+// Algorithm 1).  This file restates the step literally on top of the reference
+// headers, which it INCLUDES (never copies):
+//   CellSet / CellIndex  cell_set.hpp:17-394  (mesh sets, slot order)
+//   DomainBox, parent    cell.hpp:102-196
+//   project, predict     prediction.hpp:51-60, 143-173
+//   DenseMatrix          dense_matrix.hpp:42-113 (collision matvec order, inverse)
+// Semantics pinned in DESIGN.md §Decisions (SURVEY Appendix A ledger).
+//
+// PARITY STATUS: the reference ships no golden vectors for the step, so the
+// step is "parity unpinned" against upstream output; the primitives it uses
+// are the reference's own code, pinned by tests/test_oracle_prims.py.
+//
+// Build: oracle/Makefile  (g++ -std=c++20 -O2 -ffp-contract=off -include cmath
+//        -I/root/reference/proj/core/include -fopenmp)
+
+#include <mrlbm/cell.hpp>
+#include <mrlbm/cell_set.hpp>
+#include <mrlbm/dense_matrix.hpp>
+#include <mrlbm/prediction.hpp>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <functional>
+#include <mutex>
+#include <map>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <omp.h>
+
+#include "../include/mrlbm_gpu.h"
+
+namespace {
+
+using I64 = std::int64_t;
+using I128 = __int128;
+
+// exceptions must not cross an OpenMP region: capture the first, rethrow after
+struct OmpErr {
+    std::exception_ptr ep;
+    std::mutex mu;
+    template <class Fn>
+    void run(Fn&& fn)
+    {
+        try
+        {
+            fn();
+        }
+        catch (...)
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!ep)
+                ep = std::current_exception();
+        }
+    }
+    void rethrow()
+    {
+        if (ep)
+            std::rethrow_exception(ep);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Flattened reconstruction tables.
+// Pull formulation: memoised recursion rec(m, c) over an infinite uniform
+// level-l neighbourhood, each rec a linear form over level-l offsets with exact
+// dyadic coefficients (numerators over 8^depth in 1D, 64^depth in 2D).  The
+// one-hot prediction weights come from calling the reference predict<D>
+// (prediction.hpp:143-173), so the minus cross-term convention is the
+// reference's.
+// ---------------------------------------------------------------------------
+template <int D>
+struct TableBuilder {
+    // W[delta][o] numerators (denominator 8 for D=1, 64 for D=2)
+    std::array<std::array<I64, (D == 1 ? 3 : 9)>, (1 << D)> W{};
+    static constexpr int kDen = (D == 1 ? 8 : 64);
+    static constexpr int kShift = (D == 1 ? 3 : 6);
+
+    TableBuilder()
+    {
+        const auto cfg = mrlbm::PredictionConfig::make(1);
+        const int nst = (D == 1 ? 3 : 9);
+        for (int s = 0; s < (1 << D); ++s)
+        {
+            std::array<int, D> delta{};
+            for (int i = 0; i < D; ++i)
+                delta[i] = (s >> (D - 1 - i)) & 1;
+            for (int o = 0; o < nst; ++o)
+            {
+                std::array<I64, 3> hot{};
+                if (D == 1)
+                    hot[0] = o - 1;
+                else
+                {
+                    hot[0] = o / 3 - 1;
+                    hot[1] = o % 3 - 1;
+                }
+                auto at = [&](std::array<I64, 3> off) { return (off == hot) ? 1.0 : 0.0; };
+                const double w = mrlbm::predict<D>(at, delta, cfg);
+                const double num = w * kDen;
+                if (num != std::floor(num))
+                    throw std::domain_error("table: non-dyadic prediction weight");
+                W[s][o] = static_cast<I64>(num);
+            }
+        }
+    }
+
+    using Form = std::map<std::array<I64, D>, I128>; // level-l offset -> numerator
+
+    // rec at depth dd above level l (dd = m - l), relative cell c (level m coords,
+    // the leaf covers [0, 2^dd)^D).
+    const Form& rec(int dd, const std::array<I64, D>& c, std::map<std::pair<int, std::array<I64, D>>, Form>& memo)
+    {
+        auto key = std::make_pair(dd, c);
+        auto it = memo.find(key);
+        if (it != memo.end())
+            return it->second;
+        Form out;
+        if (dd == 0)
+        {
+            out[c] = 1; // numerator over 1
+        }
+        else
+        {
+            std::array<I64, D> p{};
+            int s = 0;
+            for (int i = 0; i < D; ++i)
+            {
+                p[i] = c[i] >> 1;
+                s = (s << 1) | static_cast<int>(c[i] - 2 * p[i]);
+            }
+            const int nst = (D == 1 ? 3 : 9);
+            for (int o = 0; o < nst; ++o)
+            {
+                const I64 w = W[s][o];
+                if (w == 0)
+                    continue;
+                std::array<I64, D> pc = p;
+                if (D == 1)
+                    pc[0] += o - 1;
+                else
+                {
+                    pc[0] += o / 3 - 1;
+                    pc[1] += o % 3 - 1;
+                }
+                const Form& sub = rec(dd - 1, pc, memo);
+                for (const auto& [k, v] : sub)
+                    out[k] += v * w; // numerators over kDen^dd
+            }
+        }
+        return memo.emplace(key, std::move(out)).first->second;
+    }
+
+    // side 0 = E = (B - eta) \ B, side 1 = A = B \ (B - eta)
+    std::vector<std::pair<std::array<int, D>, double>> build(int g, const int32_t* eta, int side)
+    {
+        const I64 n = I64{1} << g;
+        std::vector<std::array<I64, D>> cells;
+        auto inB = [&](const std::array<I64, D>& x)
+        {
+            for (int i = 0; i < D; ++i)
+                if (x[i] < 0 || x[i] >= n)
+                    return false;
+            return true;
+        };
+        // enumerate candidate finest cells in lexicographic order
+        std::array<I64, D> lo{}, hi{};
+        for (int i = 0; i < D; ++i)
+        {
+            lo[i] = -2;
+            hi[i] = n + 2;
+        }
+        std::array<I64, D> x = lo;
+        while (true)
+        {
+            std::array<I64, D> xe{};
+            for (int i = 0; i < D; ++i)
+                xe[i] = x[i] + eta[i];
+            const bool member = side == 0 ? (inB(xe) && !inB(x)) : (inB(x) && !inB(xe));
+            if (member)
+                cells.push_back(x);
+            int ax = D - 1;
+            while (ax >= 0)
+            {
+                if (++x[ax] < hi[ax])
+                    break;
+                x[ax] = lo[ax];
+                --ax;
+            }
+            if (ax < 0)
+                break;
+        }
+        std::map<std::pair<int, std::array<I64, D>>, Form> memo;
+        Form total;
+        for (const auto& c : cells)
+        {
+            const Form& f = rec(g, c, memo);
+            for (const auto& [k, v] : f)
+                total[k] += v;
+        }
+        std::vector<std::pair<std::array<int, D>, double>> out;
+        for (const auto& [k, v] : total)
+        {
+            if (v == 0)
+                continue;
+            // nearest double to the exact dyadic weight (Decision D.12)
+            const double w = std::ldexp(static_cast<double>(v), -kShift * g);
+            std::array<int, D> off{};
+            for (int i = 0; i < D; ++i)
+                off[i] = static_cast<int>(k[i]);
+            out.emplace_back(off, w);
+        }
+        return out; // std::map order == lexicographic offsets
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Equilibria (DESIGN.md Decisions D.18-D.21; PAPER.md:1143-1147,
+// 1345-1348).  m is the full moment vector (conserved moments unchanged by
+// collision); writes meq for every moment.
+// ---------------------------------------------------------------------------
+void equilibrium(const mrlbm_scheme_spec& sc, const double* m, double* meq)
+{
+    const double* P = sc.eq_params;
+    switch (sc.equilibrium)
+    {
+        case MRLBM_EQ_BURGERS_D1Q2:
+        {
+            const double u = m[0];
+            meq[0] = u;
+            meq[1] = 0.5 * u * u;
+            break;
+        }
+        case MRLBM_EQ_EULER_D1Q3X3:
+        {
+            const double gam = P[0];
+            const double lam2 = sc.lambda * sc.lambda;
+            const double rho = m[0], q = m[3], E = m[6];
+            const double u = q / rho;
+            const double p = (gam - 1.0) * (E - 0.5 * rho * u * u);
+            const double F[3] = {q, q * u + p, u * (E + p)};
+            const double U[3] = {rho, q, E};
+            for (int i = 0; i < 3; ++i)
+            {
+                meq[3 * i + 0] = U[i];
+                meq[3 * i + 1] = F[i];
+                meq[3 * i + 2] = lam2 * U[i];
+            }
+            break;
+        }
+        case MRLBM_EQ_ADVECTION_D2Q4:
+        {
+            const double u = m[0];
+            meq[0] = u;
+            meq[1] = P[0] * u;
+            meq[2] = P[1] * u;
+            meq[3] = 0.0;
+            break;
+        }
+        case MRLBM_EQ_EULER_D2Q4X4:
+        {
+            const double gam = P[0];
+            const double rho = m[0], qx = m[4], qy = m[8], E = m[12];
+            const double u = qx / rho;
+            const double v = qy / rho;
+            const double p = (gam - 1.0) * (E - 0.5 * rho * (u * u + v * v));
+            const double Fx[4] = {qx, qx * u + p, qx * v, u * (E + p)};
+            const double Fy[4] = {qy, qy * u, qy * v + p, v * (E + p)};
+            const double U[4] = {rho, qx, qy, E};
+            for (int i = 0; i < 4; ++i)
+            {
+                meq[4 * i + 0] = U[i];
+                meq[4 * i + 1] = Fx[i];
+                meq[4 * i + 2] = Fy[i];
+                meq[4 * i + 3] = 0.0;
+            }
+            break;
+        }
+        case MRLBM_EQ_NS_D2Q9:
+        {
+            const double cs2 = P[0];
+            const double rho = m[0], qx = m[1], qy = m[2];
+            meq[0] = rho;
+            meq[1] = qx;
+            meq[2] = qy;
+            if (P[1] == 0.0)
+            {
+                const double q2 = qx * qx + qy * qy;
+                meq[3] = 3.0 * (-2.0 * cs2 * rho + q2 / rho);
+                meq[6] = 9.0 * (cs2 * cs2 * rho - cs2 * q2 / rho);
+            }
+            else
+            { // literal printed form: |q|/rho, c_s^4 without rho
+                const double qn = std::sqrt(qx * qx + qy * qy);
+                meq[3] = 3.0 * (-2.0 * cs2 * rho + qn / rho);
+                meq[6] = 9.0 * (cs2 * cs2 - cs2 * qn / rho);
+            }
+            meq[4] = -3.0 * cs2 * qx;
+            meq[5] = -3.0 * cs2 * qy;
+            meq[7] = (qx * qx - qy * qy) / rho;
+            meq[8] = qx * qy / rho;
+            break;
+        }
+        default:
+            throw std::invalid_argument("unknown equilibrium");
+    }
+}
+
+template <int D>
+class Oracle {
+  public:
+    using Idx = mrlbm::Index<D>;
+    using Set = mrlbm::CellSet<D>;
+    using CIdx = mrlbm::CellIndex<D>;
+
+    struct Level {
+        Set leaves, internal; // S(Lambda) and internal complete-tree nodes at this level
+        CIdx li, ii;
+        std::vector<double> lf, itf; // AoS values: [slot * q + h]
+    };
+
+    mrlbm_scheme_spec sc{};
+    mrlbm_run_config rc{};
+    int J0 = 0, J1 = 0, q = 0;
+    mrlbm::DomainBox<D> box;
+    bool per[D]{};
+    mrlbm::PredictionConfig pcfg = mrlbm::PredictionConfig::make(1);
+    mrlbm::DenseMatrix M, Minv;
+    std::vector<Level> lev;                      // index m - J0
+    std::vector<std::vector<std::pair<Idx, std::vector<double>>>> staged;
+    bool committed = false;
+    int opp[MRLBM_MAX_Q]{};
+    // tables [gap][h][side] -> (offsets, weights)
+    std::vector<std::vector<std::array<std::vector<std::pair<std::array<int, D>, double>>, 2>>> tables;
+    std::int64_t fallback_last = 0;
+    std::int64_t leaf_updates = 0;
+    std::string err;
+
+    Oracle(const mrlbm_scheme_spec& s_, const mrlbm_run_config& r_) : sc(s_), rc(r_)
+    {
+        if (sc.d != D)
+            throw std::invalid_argument("dimension mismatch");
+        q = sc.q;
+        if (q < 1 || q > MRLBM_MAX_Q)
+            throw std::invalid_argument("q out of range");
+        J0 = rc.j_min;
+        J1 = rc.j_max;
+        if (J0 < 0 || J1 <= J0 || J1 - J0 + 1 > MRLBM_MAX_LEVELS)
+            throw std::invalid_argument("levels out of range");
+        if (rc.gamma != 1 || rc.graduation != 1)
+            throw std::invalid_argument("only gamma = graduation = 1 is supported");
+        box.j_min = J0;
+        for (int i = 0; i < D; ++i)
+            box.base_cells[i] = rc.base_cells[i];
+        for (int i = 0; i < D; ++i)
+        {
+            const bool a = rc.bc_kind[2 * i] == MRLBM_BC_PERIODIC;
+            const bool b = rc.bc_kind[2 * i + 1] == MRLBM_BC_PERIODIC;
+            if (a != b)
+                throw std::invalid_argument("periodic must be set on both faces of an axis");
+            per[i] = a;
+        }
+        M = mrlbm::DenseMatrix(q, q);
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j)
+                M(i, j) = sc.M[i * q + j];
+        // M^-1 from the reference Gauss-Jordan (dense_matrix.hpp:58-113); the
+        // descriptor's copy must agree bit for bit (the GPU uses the descriptor).
+        Minv = M.inverse();
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j)
+                if (std::memcmp(&Minv(i, j), &sc.Minv[i * q + j], sizeof(double)) != 0)
+                    throw std::invalid_argument("scheme Minv differs from DenseMatrix::inverse(M)");
+        for (int h = 0; h < q; ++h)
+        {
+            opp[h] = -1;
+            for (int k = 0; k < q; ++k)
+            {
+                bool ok = true;
+                for (int i = 0; i < D; ++i)
+                    ok = ok && sc.eta[k][i] == -sc.eta[h][i];
+                // vectorial schemes: the opposite velocity inside the same block
+                const int bs = q / sc.nblocks;
+                ok = ok && (k / bs == h / bs);
+                if (ok)
+                {
+                    opp[h] = k;
+                    break;
+                }
+            }
+        }
+        lev.resize(J1 - J0 + 1);
+        staged.resize(J1 - J0 + 1);
+        TableBuilder<D> tb;
+        tables.resize(J1 - J0 + 1);
+        for (int g = 0; g <= J1 - J0; ++g)
+        {
+            tables[g].resize(q);
+            for (int h = 0; h < q; ++h)
+                for (int side = 0; side < 2; ++side)
+                    tables[g][h][side] = tb.build(g, sc.eta[h], side);
+        }
+    }
+
+    // ---------------- geometry helpers ----------------
+    Idx extent(int m) const { return box.extent(m); }
+
+    // MR lookup rule outside the domain (Decision D.8): periodic wrap, else clamp.
+    Idx wrapclamp(int m, Idx c) const
+    {
+        const Idx n = extent(m);
+        for (int i = 0; i < D; ++i)
+        {
+            if (per[i])
+            {
+                c[i] %= n[i];
+                if (c[i] < 0)
+                    c[i] += n[i];
+            }
+            else if (c[i] < 0)
+                c[i] = 0;
+            else if (c[i] >= n[i])
+                c[i] = n[i] - 1;
+        }
+        return c;
+    }
+
+    bool inside_or_periodic(int m, const Idx& c) const
+    {
+        const Idx n = extent(m);
+        for (int i = 0; i < D; ++i)
+            if (!per[i] && (c[i] < 0 || c[i] >= n[i]))
+                return false;
+        return true;
+    }
+
+    // set algebra image of a same-level set that may stick out of the domain:
+    // clip non-periodic axes, wrap periodic ones (Decisions D.6, D.7)
+    Set wrapclip(int m, const Set& s) const
+    {
+        const Idx n = extent(m);
+        Set out;
+        std::array<int, D> a{};
+        for (int i = 0; i < D; ++i)
+            a[i] = per[i] ? -1 : 0;
+        while (true)
+        {
+            Idx shift{};
+            for (int i = 0; i < D; ++i)
+                shift[i] = static_cast<I64>(a[i]) * n[i];
+            out.merge(s.translated(shift).clipped(box, m));
+            int ax = D - 1;
+            while (ax >= 0)
+            {
+                if (per[ax] && a[ax] < 1)
+                {
+                    ++a[ax];
+                    break;
+                }
+                a[ax] = per[ax] ? -1 : 0;
+                --ax;
+            }
+            if (ax < 0)
+                break;
+        }
+        return out;
+    }
+
+    Set full_level(int m) const
+    {
+        Set s;
+        const Idx n = extent(m);
+        if constexpr (D == 1)
+        {
+            s.insert_run(Idx{0}, n[0]);
+        }
+        else
+        {
+            for (I64 x = 0; x < n[0]; ++x)
+                s.insert_run(Idx{x, 0}, n[1]);
+        }
+        return s;
+    }
+
+    // ---------------- value access on the current tree ----------------
+    const double* value_R(int m, const Idx& c) const
+    {
+        const Level& L = lev[m - J0];
+        if (auto s = L.li.slot(c))
+            return &L.lf[*s * q];
+        if (auto s = L.ii.slot(c))
+            return &L.itf[*s * q];
+        return nullptr;
+    }
+
+    // ---------------- loading ----------------
+    void load(int level, I64 n, const int32_t* idx, const double* f)
+    {
+        if (level < J0 || level > J1)
+            throw std::invalid_argument("load: level out of range");
+        auto& st = staged[level - J0];
+        st.clear();
+        st.reserve(n);
+        for (I64 i = 0; i < n; ++i)
+        {
+            Idx c{};
+            for (int a = 0; a < D; ++a)
+                c[a] = idx[i * D + a];
+            std::vector<double> v(q);
+            for (int h = 0; h < q; ++h)
+                v[h] = f[h * n + i];
+            st.emplace_back(c, std::move(v));
+        }
+    }
+
+    void commit()
+    {
+        // refined sets from the loaded leaves (closure upwards), then derive and verify
+        std::vector<Set> refined(J1 - J0);
+        std::vector<Set> leafsets(J1 - J0 + 1);
+        for (int m = J0; m <= J1; ++m)
+            for (const auto& [c, v] : staged[m - J0])
+            {
+                if (!mrlbm::DomainBox<D>(box).contains(m, c))
+                    throw std::invalid_argument("load: leaf outside the domain");
+                leafsets[m - J0].insert(c);
+            }
+        for (int m = J1; m > J0; --m)
+        {
+            Set up = leafsets[m - J0].coarsened();
+            if (m < J1)
+                up.merge(refined[m - J0].coarsened());
+            refined[m - 1 - J0].merge(up);
+        }
+        install_tree(refined);
+        // verify partition and place values
+        std::int64_t total = 0;
+        for (int m = J0; m <= J1; ++m)
+        {
+            Level& L = lev[m - J0];
+            const auto& st = staged[m - J0];
+            if (static_cast<std::size_t>(L.leaves.cell_count()) != st.size())
+                throw std::invalid_argument("load: leaves do not form a complete-leaf partition");
+            L.lf.assign(st.size() * q, 0.0);
+            for (const auto& [c, v] : st)
+            {
+                auto s = L.li.slot(c);
+                if (!s)
+                    throw std::invalid_argument("load: leaves do not form a complete-leaf partition");
+                std::copy(v.begin(), v.end(), L.lf.begin() + *s * q);
+            }
+            total += st.size();
+        }
+        (void)total;
+        for (auto& st : staged)
+            st.clear();
+        committed = true;
+    }
+
+    // install a tree given refined sets per level (index m - J0, m < J1)
+    void install_tree(const std::vector<Set>& refined)
+    {
+        for (int m = J0; m <= J1; ++m)
+        {
+            Level& L = lev[m - J0];
+            Set R = (m == J0) ? full_level(m) : refined[m - 1 - J0].refined();
+            if (m < J1)
+            {
+                L.internal = refined[m - J0];
+                L.leaves = set_difference(R, L.internal);
+            }
+            else
+            {
+                L.internal = Set();
+                L.leaves = R;
+            }
+            L.li = CIdx(L.leaves);
+            L.ii = CIdx(L.internal);
+            L.itf.assign(L.ii.size() * q, 0.0);
+        }
+    }
+
+    std::vector<Set> current_refined() const
+    {
+        std::vector<Set> r(J1 - J0);
+        for (int m = J0; m < J1; ++m)
+            r[m - J0] = lev[m - J0].internal;
+        return r;
+    }
+
+    // ---------------- the time step (Algorithm 1 body) ----
+    void project_internal()
+    {
+        // bottom-up projection P_down (prediction.hpp:51-60)
+        for (int m = J1 - 1; m >= J0; --m)
+        {
+            Level& L = lev[m - J0];
+            std::vector<Idx> cells;
+            L.internal.for_each_cell([&](const Idx& c) { cells.push_back(c); });
+            OmpErr oe;
+#pragma omp parallel for schedule(static)
+            for (std::size_t i = 0; i < cells.size(); ++i)
+                oe.run([&] {
+                const Idx& p = cells[i];
+                const auto ch = mrlbm::children(mrlbm::CellId<D>{m, p}, J1);
+                const double* cv[1 << D];
+                for (int s = 0; s < (1 << D); ++s)
+                {
+                    cv[s] = value_R(m + 1, ch[s].idx);
+                    if (!cv[s])
+                        throw std::logic_error("project: missing child");
+                }
+                const std::size_t slot = *L.ii.slot(p);
+                for (int h = 0; h < q; ++h)
+                {
+                    std::array<double, (1 << D)> v{};
+                    for (int s = 0; s < (1 << D); ++s)
+                        v[s] = cv[s][h];
+                    L.itf[slot * q + h] = mrlbm::project<D>(v);
+                }
+                });
+            oe.rethrow();
+        }
+    }
+
+    // gather the 3^D (or 5^D) same-level neighbourhood values with the MR rule
+    template <int W, class Get>
+    bool gather_box(int m, const Idx& center, std::vector<const double*>& out, Get&& get) const
+    {
+        constexpr int S = 2 * W + 1;
+        out.resize(D == 1 ? S : S * S);
+        for (int o = 0; o < (D == 1 ? S : S * S); ++o)
+        {
+            Idx c = center;
+            if (D == 1)
+                c[0] += o - W;
+            else
+            {
+                c[0] += o / S - W;
+                c[D - 1] += o % S - W;
+            }
+            out[o] = get(m, wrapclamp(m, c));
+            if (!out[o])
+                return false;
+        }
+        return true;
+    }
+
+    double predict_from(const std::vector<const double*>& st3, const std::array<int, D>& delta, int h) const
+    {
+        // reference predict with an accessor over the prefetched 3^D stencil
+        auto at = [&](std::array<I64, 3> off) -> double
+        {
+            int o = 0;
+            if (D == 1)
+                o = static_cast<int>(off[0]) + 1;
+            else
+                o = (static_cast<int>(off[0]) + 1) * 3 + static_cast<int>(off[1]) + 1;
+            return st3[o][h];
+        };
+        return mrlbm::predict<D>(at, delta, pcfg);
+    }
+
+    void step()
+    {
+        if (!committed)
+            throw std::logic_error("step before commit");
+        const int nl = J1 - J0 + 1;
+        // (1) projection of the old tree
+        project_internal();
+
+        // (2) details + group metric + T/H(b) flags
+        std::vector<Set> keep(J1 - J0), Rn(J1 - J0);
+        for (int m = J0; m < J1; ++m)
+        {
+            Level& L = lev[m - J0];
+            const int l = m + 1; // level of the sibling group
+            const double eps_l = std::ldexp(rc.epsilon, D * (l - J1));
+            const double eps_b = std::ldexp(eps_l, rc.mu + D);
+            std::vector<Idx> cells;
+            L.internal.for_each_cell([&](const Idx& c) { cells.push_back(c); });
+            std::vector<char> kflag(cells.size()), bflag(cells.size());
+            OmpErr oe;
+#pragma omp parallel
+            {
+                std::vector<const double*> st;
+#pragma omp for schedule(static)
+                for (std::size_t i = 0; i < cells.size(); ++i)
+                    oe.run([&] {
+                    const Idx& p = cells[i];
+                    auto get = [&](int mm, const Idx& c) { return value_R(mm, c); };
+                    if (!gather_box<1>(m, p, st, get))
+                        throw std::logic_error("details: unresolved prediction stencil (grading)");
+                    const auto ch = mrlbm::children(mrlbm::CellId<D>{m, p}, J1);
+                    double metric = 0.0;
+                    for (int s = 0; s < (1 << D); ++s)
+                    {
+                        std::array<int, D> delta{};
+                        for (int a = 0; a < D; ++a)
+                            delta[a] = (s >> (D - 1 - a)) & 1;
+                        const double* cv = value_R(l, ch[s].idx);
+                        for (int h = 0; h < q; ++h)
+                        {
+                            const double d = cv[h] - predict_from(st, delta, h);
+                            const double ad = std::fabs(d);
+                            if (ad > metric)
+                                metric = ad;
+                        }
+                    }
+                    kflag[i] = metric >= eps_l;
+                    bflag[i] = (l > J0 && l < J1) && metric >= eps_b;
+                    });
+            }
+            oe.rethrow();
+            for (std::size_t i = 0; i < cells.size(); ++i)
+            {
+                if (kflag[i])
+                    keep[m - J0].insert(cells[i]);
+                if (bflag[i])
+                {
+                    // H(b): refine the 2^D children of every cell of the group
+                    const auto ch = mrlbm::children(mrlbm::CellId<D>{m, cells[i]}, J1);
+                    for (const auto& c : ch)
+                        Rn[l - J0].insert(c.idx);
+                }
+            }
+        }
+        // T closure (Decision D.4): ancestors of kept groups are kept
+        for (int m = J1 - 1; m > J0; --m)
+            keep[m - 1 - J0].merge(keep[m - J0].coarsened());
+        for (int m = J0; m < J1; ++m)
+            Rn[m - J0].merge(keep[m - J0]);
+        // H(a): (l, k - eta^h) for every cell of R(T)
+        for (int l = J0 + 1; l <= J1; ++l)
+        {
+            const Set RT = keep[l - 1 - J0].refined();
+            for (int h = 0; h < q; ++h)
+            {
+                Idx shift{};
+                bool zero = true;
+                for (int i = 0; i < D; ++i)
+                {
+                    shift[i] = -sc.eta[h][i];
+                    zero = zero && shift[i] == 0;
+                }
+                if (zero)
+                    continue;
+                Rn[l - 1 - J0].merge(wrapclip(l, RT.translated(shift)).coarsened());
+            }
+        }
+        // grading G: one fine->coarse sweep (Decision D.7)
+        for (int m = J1 - 1; m > J0; --m)
+            Rn[m - 1 - J0].merge(wrapclip(m, Rn[m - J0].dilated(1)).coarsened());
+
+        // (3) transfer to the new tree (Decision D.24)
+        std::vector<Level> old = std::move(lev);
+        lev.assign(nl, Level{});
+        install_tree(Rn);
+        std::vector<Set> Rnew(nl);
+        std::vector<CIdx> Ridx(nl);
+        std::vector<std::vector<double>> Rval(nl);
+        for (int m = J0; m <= J1; ++m)
+        {
+            Rnew[m - J0] = set_union(lev[m - J0].leaves, lev[m - J0].internal);
+            Ridx[m - J0] = CIdx(Rnew[m - J0]);
+            Rval[m - J0].assign(Ridx[m - J0].size() * q, 0.0);
+            std::vector<Idx> cells;
+            Rnew[m - J0].for_each_cell([&](const Idx& c) { cells.push_back(c); });
+            const Level& O = old[m - J0];
+            OmpErr oe;
+#pragma omp parallel
+            {
+                std::vector<const double*> st;
+#pragma omp for schedule(static)
+                for (std::size_t i = 0; i < cells.size(); ++i)
+                    oe.run([&] {
+                    const Idx& c = cells[i];
+                    double* dst = &Rval[m - J0][i * q];
+                    const double* src = nullptr;
+                    if (auto s = O.li.slot(c))
+                        src = &O.lf[*s * q];
+                    else if (auto s2 = O.ii.slot(c))
+                        src = &O.itf[*s2 * q];
+                    if (src)
+                    {
+                        std::copy(src, src + q, dst);
+                        return;
+                    }
+                    if (m == J0)
+                        throw std::logic_error("transfer: coarsest cell missing");
+                    Idx p{};
+                    std::array<int, D> delta{};
+                    for (int a = 0; a < D; ++a)
+                    {
+                        p[a] = c[a] >> 1;
+                        delta[a] = static_cast<int>(c[a] - 2 * p[a]);
+                    }
+                    auto get = [&](int mm, const Idx& cc) -> const double*
+                    {
+                        auto s = Ridx[mm - J0].slot(cc);
+                        return s ? &Rval[mm - J0][*s * q] : nullptr;
+                    };
+                    if (!gather_box<1>(m - 1, p, st, get))
+                        throw std::logic_error("transfer: unresolved stencil");
+                    for (int h = 0; h < q; ++h)
+                        dst[h] = predict_from(st, delta, h);
+                    });
+            }
+            oe.rethrow();
+            // split into leaves / internal (internal re-projected below)
+            Level& L = lev[m - J0];
+            L.lf.assign(L.li.size() * q, 0.0);
+            L.leaves.for_each_cell(
+                [&](const Idx& c)
+                {
+                    const std::size_t a = *L.li.slot(c), b = *Ridx[m - J0].slot(c);
+                    std::copy(&Rval[m - J0][b * q], &Rval[m - J0][b * q] + q, &L.lf[a * q]);
+                });
+        }
+        old.clear();
+        // (4) internal values = projection of the new leaves (Decision D.25)
+        project_internal();
+
+        // (5) stream + collide on every new complete leaf
+        stream_collide();
+        leaf_updates += total_leaves();
+    }
+
+    std::int64_t total_leaves() const
+    {
+        std::int64_t n = 0;
+        for (const auto& L : lev)
+            n += L.li.size();
+        return n;
+    }
+
+    using Memo = std::unordered_map<std::uint64_t, std::vector<double>>;
+
+    std::uint64_t key(int m, const Idx& c) const
+    {
+        const Idx n = extent(m);
+        std::uint64_t lin = 0;
+        for (int i = 0; i < D; ++i)
+            lin = lin * static_cast<std::uint64_t>(n[i]) + static_cast<std::uint64_t>(c[i]);
+        return (static_cast<std::uint64_t>(m) << 56) | lin;
+    }
+
+    // zero-detail reconstruction f^^: R value if the cell is in
+    // the complete tree, else prediction from the coarser level.  c is inside.
+    const double* rec(int m, const Idx& c, Memo& memo) const
+    {
+        if (const double* v = value_R(m, c))
+            return v;
+        const std::uint64_t k = key(m, c);
+        auto it = memo.find(k);
+        if (it != memo.end())
+            return it->second.data();
+        if (m == J0)
+            throw std::logic_error("rec: coarsest cell missing");
+        Idx p{};
+        std::array<int, D> delta{};
+        for (int a = 0; a < D; ++a)
+        {
+            p[a] = c[a] >> 1;
+            delta[a] = static_cast<int>(c[a] - 2 * p[a]);
+        }
+        std::vector<const double*> st(D == 1 ? 3 : 9);
+        for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
+        {
+            Idx cc = p;
+            if (D == 1)
+                cc[0] += o - 1;
+            else
+            {
+                cc[0] += o / 3 - 1;
+                cc[1] += o % 3 - 1;
+            }
+            st[o] = rec(m - 1, wrapclamp(m - 1, cc), memo);
+        }
+        std::vector<double> v(q);
+        for (int h = 0; h < q; ++h)
+            v[h] = predict_from(st, delta, h);
+        return memo.emplace(k, std::move(v)).first->second.data();
+    }
+
+    // value of the complete leaf covering finest cell c (direct evaluation)
+    const double* covering_leaf(const Idx& cfine) const
+    {
+        for (int m = J1; m >= J0; --m)
+        {
+            Idx a{};
+            for (int i = 0; i < D; ++i)
+                a[i] = cfine[i] >> (J1 - m);
+            const Level& L = lev[m - J0];
+            if (auto s = L.li.slot(a))
+                return &L.lf[*s * q];
+        }
+        throw std::logic_error("covering leaf not found");
+    }
+
+    // finest-level E / A cells of leaf (l, k) for velocity eta, lexicographic
+    void rim_cells(int l, const Idx& k, const int32_t* eta, int side, std::vector<Idx>& out) const
+    {
+        out.clear();
+        const int g = J1 - l;
+        const I64 n = I64{1} << g;
+        Idx lo{}, hi{};
+        for (int i = 0; i < D; ++i)
+        {
+            lo[i] = k[i] * n - 1;
+            hi[i] = (k[i] + 1) * n + 1;
+        }
+        auto inB = [&](const Idx& x)
+        {
+            for (int i = 0; i < D; ++i)
+                if (x[i] < k[i] * n || x[i] >= (k[i] + 1) * n)
+                    return false;
+            return true;
+        };
+        Idx x = lo;
+        while (true)
+        {
+            Idx xe{};
+            for (int i = 0; i < D; ++i)
+                xe[i] = x[i] + eta[i];
+            const bool member = side == 0 ? (inB(xe) && !inB(x)) : (inB(x) && !inB(xe));
+            if (member)
+                out.push_back(x);
+            int ax = D - 1;
+            while (ax >= 0)
+            {
+                if (++x[ax] < hi[ax])
+                    break;
+                x[ax] = lo[ax];
+                --ax;
+            }
+            if (ax < 0)
+                break;
+        }
+    }
+
+    void stream_collide()
+    {
+        const Idx nfine = extent(J1);
+        std::int64_t nfb = 0;
+        for (int l = J0; l <= J1; ++l)
+        {
+            Level& L = lev[l - J0];
+            const int g = J1 - l;
+            const double scale = std::ldexp(1.0, D * (l - J1));
+            std::vector<Idx> cells;
+            L.leaves.for_each_cell([&](const Idx& c) { cells.push_back(c); });
+            std::vector<double> out(cells.size() * q);
+            std::vector<char> fb(cells.size(), 0);
+            OmpErr oe;
+#pragma omp parallel reduction(+ : nfb)
+            {
+                Memo memo;
+                std::vector<Idx> rim;
+                std::vector<double> f(q), mm(q), meq(q), mp(q), fs(q);
+#pragma omp for schedule(dynamic, 256)
+                for (std::size_t i = 0; i < cells.size(); ++i)
+                    oe.run([&] {
+                    const Idx& k = cells[i];
+                    const double* fstar = &L.lf[*L.li.slot(k) * q];
+                    // table validity (Decision D.13): 5^D box inside (or periodic)
+                    // and free of internal cells
+                    bool fallback = false;
+                    const int nb = (D == 1 ? 5 : 25);
+                    std::array<const double*, 25> bx{};
+                    for (int o = 0; o < nb && !fallback; ++o)
+                    {
+                        Idx c = k;
+                        if (D == 1)
+                            c[0] += o - 2;
+                        else
+                        {
+                            c[0] += o / 5 - 2;
+                            c[1] += o % 5 - 2;
+                        }
+                        if (!inside_or_periodic(l, c))
+                        {
+                            fallback = true;
+                            break;
+                        }
+                        c = wrapclamp(l, c);
+                        if (L.ii.slot(c))
+                        {
+                            fallback = true;
+                            break;
+                        }
+                        bx[o] = rec(l, c, memo);
+                    }
+                    fb[i] = fallback;
+                    nfb += fallback ? 1 : 0;
+                    for (int h = 0; h < q; ++h)
+                    {
+                        double sE = 0.0, sA = 0.0;
+                        if (!fallback)
+                        {
+                            for (int side = 0; side < 2; ++side)
+                            {
+                                double s = 0.0;
+                                for (const auto& [off, w] : tables[g][h][side])
+                                {
+                                    const int o = (D == 1) ? off[0] + 2 : (off[0] + 2) * 5 + off[1] + 2;
+                                    s += w * bx[o][h];
+                                }
+                                (side == 0 ? sE : sA) = s;
+                            }
+                        }
+                        else
+                        {
+                            rim_cells(l, k, sc.eta[h], 0, rim);
+                            for (const auto& x : rim)
+                                sE += rim_value(x, h, fstar, nfine, memo);
+                            rim_cells(l, k, sc.eta[h], 1, rim);
+                            for (const auto& x : rim)
+                                sA += rec(J1, x, memo)[h];
+                        }
+                        f[h] = fstar[h] + scale * (sE - sA);
+                    }
+                    // collide (Decision D.24)
+                    M.multiply(f.data(), mm.data());
+                    equilibrium(sc, mm.data(), meq.data());
+                    for (int h = 0; h < q; ++h)
+                        mp[h] = (1.0 - sc.s[h]) * mm[h] + sc.s[h] * meq[h];
+                    Minv.multiply(mp.data(), fs.data());
+                    if (rc.obstacle == 1)
+                        obstacle_blend(l, k, fs.data());
+                    for (int h = 0; h < q; ++h)
+                    {
+                        if (!std::isfinite(fs[h]))
+                            throw std::domain_error("non-finite population after collision");
+                        out[i * q + h] = fs[h];
+                    }
+                    });
+            }
+            oe.rethrow();
+            // write after all leaves of this level have read their stencils: but
+            // stencils also read other levels -> defer the swap until all levels done
+            pending.push_back(std::move(out));
+        }
+        for (int l = J0; l <= J1; ++l)
+            lev[l - J0].lf = std::move(pending[l - J0]);
+        pending.clear();
+        fallback_last = nfb;
+    }
+    std::vector<std::vector<double>> pending;
+
+    // E-rim value: reconstruction inside the domain, boundary rule outside
+    double rim_value(const Idx& x, int h, const double* fstar_leaf, const Idx& nfine, Memo& memo) const
+    {
+        int face = -1;
+        for (int i = 0; i < D && face < 0; ++i)
+        {
+            if (per[i])
+                continue;
+            if (x[i] < 0)
+                face = 2 * i;
+            else if (x[i] >= nfine[i])
+                face = 2 * i + 1;
+        }
+        if (face < 0)
+            return rec(J1, wrapclamp(J1, x), memo)[h];
+        const int kind = rc.bc_kind[face];
+        switch (kind)
+        {
+            case MRLBM_BC_COPY:
+                return covering_leaf(wrapclamp(J1, x))[h];
+            case MRLBM_BC_BOUNCE_BACK:
+                return fstar_leaf[opp_checked(h)];
+            case MRLBM_BC_ANTI_BOUNCE_BACK:
+                return -fstar_leaf[opp_checked(h)];
+            case MRLBM_BC_VELOCITY_BOUNCE_BACK:
+                return fstar_leaf[opp_checked(h)] + rc.bc_add[face][h];
+            default:
+                throw std::invalid_argument("bad boundary kind");
+        }
+    }
+
+    int opp_checked(int h) const
+    {
+        if (opp[h] < 0)
+            throw std::invalid_argument("bounce-back needs an opposite velocity");
+        return opp[h];
+    }
+
+    // config 5 obstacle: alpha by
+    // sub-sampling, f <- alpha feq0 + (1 - alpha) f
+    void obstacle_blend(int l, const Idx& k, double* fs) const
+    {
+        const int ns = rc.obstacle_subsamples;
+        const double dx = std::ldexp(1.0, -l);
+        const double r2 = rc.obstacle_radius * rc.obstacle_radius;
+        double x0[D], x1[D];
+        for (int i = 0; i < D; ++i)
+        {
+            x0[i] = rc.origin[i] + static_cast<double>(k[i]) * dx;
+            x1[i] = x0[i] + dx;
+        }
+        // bounding-box rejection (exact in dyadics)
+        for (int i = 0; i < D; ++i)
+            if (x1[i] < rc.obstacle_center[i] - rc.obstacle_radius || x0[i] > rc.obstacle_center[i] + rc.obstacle_radius)
+                return;
+        int cnt = 0;
+        for (int a = 0; a < ns; ++a)
+            for (int b = 0; b < (D == 1 ? 1 : ns); ++b)
+            {
+                const double sx = rc.origin[0] + (static_cast<double>(k[0]) + (a + 0.5) / ns) * dx;
+                double rr = (sx - rc.obstacle_center[0]) * (sx - rc.obstacle_center[0]);
+                if (D == 2)
+                {
+                    const double sy = rc.origin[1] + (static_cast<double>(k[D - 1]) + (b + 0.5) / ns) * dx;
+                    rr = rr + (sy - rc.obstacle_center[1]) * (sy - rc.obstacle_center[1]);
+                }
+                cnt += rr < r2;
+            }
+        if (cnt == 0)
+            return;
+        const double alpha = static_cast<double>(cnt) / (D == 1 ? ns : ns * ns);
+        for (int h = 0; h < q; ++h)
+            fs[h] = alpha * rc.obstacle_feq[h] + (1.0 - alpha) * fs[h];
+    }
+
+    std::int64_t level_count(int m) const { return lev[m - J0].li.size(); }
+
+    void read(int m, int32_t* idx, double* f) const
+    {
+        const Level& L = lev[m - J0];
+        const std::size_t n = L.li.size();
+        std::size_t i = 0;
+        L.leaves.for_each_cell(
+            [&](const Idx& c)
+            {
+                if (idx)
+                    for (int a = 0; a < D; ++a)
+                        idx[i * D + a] = static_cast<int32_t>(c[a]);
+                if (f)
+                    for (int h = 0; h < q; ++h)
+                        f[h * n + i] = L.lf[i * q + h];
+                ++i;
+            });
+    }
+
+    std::int64_t internal_count(int m) const { return lev[m - J0].ii.size(); }
+};
+
+struct Handle {
+    int d = 0;
+    std::unique_ptr<Oracle<1>> o1;
+    std::unique_ptr<Oracle<2>> o2;
+    std::string err;
+};
+
+template <class Fn>
+int guard(Handle* h, Fn&& fn)
+{
+    try
+    {
+        fn();
+        return MRLBM_OK;
+    }
+    catch (const std::invalid_argument& e)
+    {
+        h->err = e.what();
+        return MRLBM_ERR_CONFIG;
+    }
+    catch (const std::domain_error& e)
+    {
+        h->err = e.what();
+        return MRLBM_ERR_NUMERIC;
+    }
+    catch (const std::exception& e)
+    {
+        h->err = e.what();
+        return MRLBM_ERR_CAPACITY;
+    }
+}
+
+} // namespace
+
+extern "C" {
+
+int oracle_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, void** out)
+{
+    auto* h = new Handle();
+    h->d = sc->d;
+    const int st = guard(h,
+                         [&]
+                         {
+                             if (sc->d == 1)
+                                 h->o1 = std::make_unique<Oracle<1>>(*sc, *rc);
+                             else if (sc->d == 2)
+                                 h->o2 = std::make_unique<Oracle<2>>(*sc, *rc);
+                             else
+                                 throw std::invalid_argument("d must be 1 or 2");
+                         });
+    if (st != MRLBM_OK)
+    {
+        static thread_local std::string last;
+        last = h->err;
+        delete h;
+        *out = nullptr;
+        return st;
+    }
+    *out = h;
+    return MRLBM_OK;
+}
+
+#define ORACLE_DISPATCH(h, call)                                                                   \
+    guard(h, [&] {                                                                                 \
+        if (h->o1)                                                                                 \
+            h->o1->call;                                                                           \
+        else                                                                                       \
+            h->o2->call;                                                                           \
+    })
+
+int oracle_load_leaves(void* p, int level, int64_t n, const int32_t* idx, const double* f)
+{
+    auto* h = static_cast<Handle*>(p);
+    return ORACLE_DISPATCH(h, load(level, n, idx, f));
+}
+
+int oracle_commit(void* p)
+{
+    auto* h = static_cast<Handle*>(p);
+    return ORACLE_DISPATCH(h, commit());
+}
+
+int oracle_step(void* p, int nsteps)
+{
+    auto* h = static_cast<Handle*>(p);
+    for (int i = 0; i < nsteps; ++i)
+    {
+        const int st = ORACLE_DISPATCH(h, step());
+        if (st != MRLBM_OK)
+            return st;
+    }
+    return MRLBM_OK;
+}
+
+int oracle_level_count(void* p, int level, int64_t* n)
+{
+    auto* h = static_cast<Handle*>(p);
+    return guard(h, [&] { *n = h->o1 ? h->o1->level_count(level) : h->o2->level_count(level); });
+}
+
+int oracle_internal_count(void* p, int level, int64_t* n)
+{
+    auto* h = static_cast<Handle*>(p);
+    return guard(h, [&] { *n = h->o1 ? h->o1->internal_count(level) : h->o2->internal_count(level); });
+}
+
+int oracle_read_leaves(void* p, int level, int32_t* idx, double* f)
+{
+    auto* h = static_cast<Handle*>(p);
+    return ORACLE_DISPATCH(h, read(level, idx, f));
+}
+
+int64_t oracle_fallback_leaves(void* p)
+{
+    auto* h = static_cast<Handle*>(p);
+    return h->o1 ? h->o1->fallback_last : h->o2->fallback_last;
+}
+
+const char* oracle_last_error(void* p)
+{
+    return static_cast<Handle*>(p)->err.c_str();
+}
+
+void oracle_destroy(void* p)
+{
+    delete static_cast<Handle*>(p);
+}
+
+int oracle_set_threads(int n)
+{
+    omp_set_num_threads(n);
+    return omp_get_max_threads();
+}
+
+// table export (pull formulation) for cross-checking the product's tables
+int oracle_stream_table(int d, int gap, const int32_t eta[3], int side, int cap, int32_t* offsets, double* weights, int* n)
+{
+    try
+    {
+        if (d == 1)
+        {
+            TableBuilder<1> tb;
+            auto t = tb.build(gap, eta, side);
+            if (static_cast<int>(t.size()) > cap)
+                return MRLBM_ERR_CAPACITY;
+            for (std::size_t i = 0; i < t.size(); ++i)
+            {
+                offsets[i] = t[i].first[0];
+                weights[i] = t[i].second;
+            }
+            *n = static_cast<int>(t.size());
+        }
+        else
+        {
+            TableBuilder<2> tb;
+            auto t = tb.build(gap, eta, side);
+            if (static_cast<int>(t.size()) > cap)
+                return MRLBM_ERR_CAPACITY;
+            for (std::size_t i = 0; i < t.size(); ++i)
+            {
+                offsets[2 * i] = t[i].first[0];
+                offsets[2 * i + 1] = t[i].first[1];
+                weights[i] = t[i].second;
+            }
+            *n = static_cast<int>(t.size());
+        }
+        return MRLBM_OK;
+    }
+    catch (...)
+    {
+        return MRLBM_ERR_NUMERIC;
+    }
+}
+
+} // extern "C"

@@ -1,0 +1,164 @@
+"""ctypes wrapper of the CPU oracle (oracle/_lib/libmrlbm_oracle.so) and of the
+reference-primitive shim (oracle/_ref/libmrlbm_refprims.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+bench's cpu_baseline / --impl reference legs, never by the product package.
+"""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2103_02903_b200.abi import SchemeSpec, RunConfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_lib", "libmrlbm_oracle.so")
+REFPRIMS_SO = os.path.join(HERE, "_ref", "libmrlbm_refprims.so")
+REF_INCLUDE = "/root/reference/proj/core/include"
+
+
+def build():
+    """Compile the oracle and the reference shim (needs /root/reference)."""
+    if os.path.isdir(REF_INCLUDE):
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    if not os.path.exists(ORACLE_SO):
+        raise RuntimeError("oracle library missing and /root/reference not available to build it")
+
+
+_orc = None
+_ref = None
+
+
+def oracle_lib():
+    global _orc
+    if _orc is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        vp = C.c_void_p
+        P = C.POINTER
+        L.oracle_create.argtypes = [P(SchemeSpec), P(RunConfig), P(vp)]
+        L.oracle_load_leaves.argtypes = [vp, C.c_int, C.c_int64, vp, vp]
+        L.oracle_commit.argtypes = [vp]
+        L.oracle_step.argtypes = [vp, C.c_int]
+        L.oracle_level_count.argtypes = [vp, C.c_int, P(C.c_int64)]
+        L.oracle_internal_count.argtypes = [vp, C.c_int, P(C.c_int64)]
+        L.oracle_read_leaves.argtypes = [vp, C.c_int, vp, vp]
+        L.oracle_fallback_leaves.argtypes = [vp]
+        L.oracle_fallback_leaves.restype = C.c_int64
+        L.oracle_last_error.argtypes = [vp]
+        L.oracle_last_error.restype = C.c_char_p
+        L.oracle_destroy.argtypes = [vp]
+        L.oracle_destroy.restype = None
+        L.oracle_set_threads.argtypes = [C.c_int]
+        L.oracle_stream_table.argtypes = [C.c_int, C.c_int, P(C.c_int32), C.c_int, C.c_int, vp, vp, P(C.c_int)]
+        _orc = L
+    return _orc
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REFPRIMS_SO):
+            build()
+        L = C.CDLL(REFPRIMS_SO)
+        vp = C.c_void_p
+        L.ref_predict.restype = C.c_double
+        L.ref_predict.argtypes = [C.c_int, C.c_int, vp, vp]
+        L.ref_project.restype = C.c_double
+        L.ref_project.argtypes = [C.c_int, vp]
+        L.ref_derive_weights.argtypes = [C.c_int, vp, vp]
+        L.ref_prediction_coeffs.argtypes = [C.c_int, vp]
+        L.ref_inverse.argtypes = [C.c_int, vp, vp]
+        L.ref_multiply.argtypes = [C.c_int, vp, vp, vp]
+        L.ref_multiply.restype = None
+        L.ref_children2.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int, vp]
+        L.ref_parent2.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int, vp]
+        L.ref_cellindex_slots2.argtypes = [C.c_int, vp, vp]
+        _ref = L
+    return _ref
+
+
+def set_threads(n):
+    return oracle_lib().oracle_set_threads(int(n))
+
+
+class Oracle:
+    """Same call sequence as paper_2103_02903_b200.Solver, on the CPU."""
+
+    def __init__(self, scheme, cfg):
+        self.L = oracle_lib()
+        self.d, self.q = scheme.d, scheme.q
+        h = C.c_void_p()
+        st = self.L.oracle_create(C.byref(scheme), C.byref(cfg), C.byref(h))
+        if st != 0:
+            raise ValueError(f"oracle_create failed with status {st}")
+        self.h = h
+
+    def _check(self, st):
+        if st != 0:
+            msg = self.L.oracle_last_error(self.h).decode()
+            if st == 2:
+                raise ValueError(msg)
+            if st == 3:
+                raise FloatingPointError(msg)
+            raise RuntimeError(f"oracle status {st}: {msg}")
+
+    def load_leaves(self, level, idx, f):
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        self._check(self.L.oracle_load_leaves(self.h, int(level), idx.shape[0], idx.ctypes.data_as(C.c_void_p),
+                                              f.ctypes.data_as(C.c_void_p)))
+
+    def commit(self):
+        self._check(self.L.oracle_commit(self.h))
+
+    def step(self, n=1):
+        self._check(self.L.oracle_step(self.h, int(n)))
+
+    def level_count(self, level):
+        n = C.c_int64(0)
+        self._check(self.L.oracle_level_count(self.h, int(level), C.byref(n)))
+        return n.value
+
+    def internal_count(self, level):
+        n = C.c_int64(0)
+        self._check(self.L.oracle_internal_count(self.h, int(level), C.byref(n)))
+        return n.value
+
+    def fallback_leaves(self):
+        return int(self.L.oracle_fallback_leaves(self.h))
+
+    def read_leaves(self, level):
+        n = self.level_count(level)
+        idx = np.zeros((n, self.d), dtype=np.int32)
+        f = np.zeros((self.q, n), dtype=np.float64)
+        if n:
+            self._check(self.L.oracle_read_leaves(self.h, int(level), idx.ctypes.data_as(C.c_void_p),
+                                                  f.ctypes.data_as(C.c_void_p)))
+        return idx, f
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.oracle_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stream_table(d, gap, eta, side):
+    cap = 64
+    off = np.zeros((cap, d), dtype=np.int32)
+    w = np.zeros(cap, dtype=np.float64)
+    n = C.c_int(0)
+    e = (C.c_int32 * 3)(*([int(v) for v in eta] + [0] * (3 - len(eta))))
+    st = oracle_lib().oracle_stream_table(d, gap, e, side, cap, off.ctypes.data_as(C.c_void_p),
+                                          w.ctypes.data_as(C.c_void_p), C.byref(n))
+    if st != 0:
+        raise ValueError(f"oracle_stream_table failed with status {st}")
+    return off[: n.value].copy(), w[: n.value].copy()

@@ -1,0 +1,1906 @@
+// mrlbm_step.cu — B200 (sm_100a) implementation of one adaptive MR-LBM time step
+// (Algorithm 1 body) behind the C-ABI in include/mrlbm_gpu.h.
+//
+// Data layout in HBM, per level m:
+//   map[v][m]   int32 dense over the level box: slot of the cell or -1
+//   cells[v][m] int32 slot -> linear cell index (row-major, last axis fastest)
+//               slots: leaves [0,nL) | internal [nL,nL+nI) | virtual [.., +nV),
+//               each range in lexicographic order == reference CellIndex order
+//               (cell_set.hpp:333-354)
+//   F0/F1[m]    fp64 SoA, one contiguous array per population, stride = level cells
+//   kind/rn/keep uint8 dense scratch flags (rebuilt every step)
+// Two tree versions v alternate (old -> new); F0 holds the state f*, F1 is the
+// transfer / reconstruction buffer.
+//
+// Arithmetic mirrors the reference operation order exactly (no FMA: --fmad=false):
+//   project  prediction.hpp:51-60     predict dense_matrix.hpp:42-54 (matvec)
+//   predict  prediction.hpp:143-173   (center + s0 qx + s1 qy - s0 s1 qxy)
+// so meshes and fields are bit-identical to the CPU oracle.
+#include "mrlbm_internal.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <climits>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace mrlbm_b200 {
+
+constexpr int kL = MRLBM_MAX_LEVELS;
+constexpr int kQ = MRLBM_MAX_Q;
+
+enum : uint8_t { K_LEAF = 1, K_INT = 2, K_VIRT = 4, K_FB = 8 };
+
+struct Geo {
+    int d, q, J0, J1, nlev, per0, per1;
+    int nx[kL], ny[kL];
+    long long cap[kL];
+};
+
+struct Tree {
+    int32_t* map[kL];
+    int32_t* cells[kL];
+    int* cnt; // [nlev][4] = nL, nI, nV, -
+};
+
+struct Fld {
+    double* f[kL];
+};
+
+struct Flags {
+    uint8_t* kind[kL];
+    uint8_t* rn[kL];
+    uint8_t* keep[kL];
+};
+
+struct SchemeDev {
+    int q, nblocks, bs, eq, mu, obstacle, obs_ns;
+    double lambda, eps;
+    int eta[kQ][2];
+    int opp[kQ];
+    double M[kQ * kQ], Minv[kQ * kQ], s[kQ], eqp[8];
+    int bc_kind[4];
+    double bc_add[4][kQ];
+    double origin[2], obs_c[2], obs_r, obs_feq[kQ];
+};
+
+struct Aux {
+    int* err;          // [0] unresolved stencil, [1] non-finite, [2] inconsistency
+    int* fb_count;     // fallback leaves of the current step
+    int2* fb_list;     // (level, lin)
+    long long fb_cap;
+    long long* updates; // accumulated leaf updates
+    const int2* tidx;   // [(g * q + h) * 2 + side] -> (start, count)
+    const int2* toff;
+    const double* tw;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ int mr_coord(int c, int n, int per)
+{
+    if (per)
+    {
+        c %= n;
+        return c < 0 ? c + n : c;
+    }
+    return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+template <int D>
+__device__ __forceinline__ void lin2xy(int lin, int ny, int& x, int& y)
+{
+    if (D == 1)
+    {
+        x = lin;
+        y = 0;
+    }
+    else
+    {
+        x = lin / ny;
+        y = lin - x * ny;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ int xy2lin(int x, int y, int ny)
+{
+    return D == 1 ? x : x * ny + y;
+}
+
+// stencil lookup with the MR boundary rule (clamp / wrap), Decision D.8
+template <int D>
+__device__ __forceinline__ int mr_lin(const Geo& g, int m, int x, int y)
+{
+    const int li = m - g.J0;
+    const int xx = mr_coord(x, g.nx[li], g.per0);
+    if (D == 1)
+        return xx;
+    const int yy = mr_coord(y, g.ny[li], g.per1);
+    return xx * g.ny[li] + yy;
+}
+
+// reference predict<D> operation order (prediction.hpp:64-75, 143-159), gamma = 1
+// st: 3 (1D) or 9 (2D, index (ox+1)*3 + (oy+1)) stencil values
+template <int D>
+__device__ __forceinline__ double mr_predict(const double* st, int dx, int dy)
+{
+    const double c1 = -0.125;
+    const double center = st[D == 1 ? 1 : 4];
+    if (D == 1)
+    {
+        const double s0 = dx == 0 ? 1.0 : -1.0;
+        const double q1 = __dadd_rn(0.0, __dmul_rn(c1, __dsub_rn(st[2], st[0])));
+        return __dadd_rn(center, __dmul_rn(s0, q1));
+    }
+    else
+    {
+        const double s0 = dx == 0 ? 1.0 : -1.0;
+        const double s1 = dy == 0 ? 1.0 : -1.0;
+        const double qx = __dadd_rn(0.0, __dmul_rn(c1, __dsub_rn(st[7], st[1])));
+        const double qy = __dadd_rn(0.0, __dmul_rn(c1, __dsub_rn(st[5], st[3])));
+        const double inner = __dadd_rn(__dsub_rn(__dsub_rn(st[8], st[2]), st[6]), st[0]);
+        const double qxy = __dadd_rn(0.0, __dmul_rn(__dmul_rn(c1, c1), inner));
+        const double a = __dadd_rn(__dadd_rn(center, __dmul_rn(s0, qx)), __dmul_rn(s1, qy));
+        return __dsub_rn(a, __dmul_rn(__dmul_rn(s0, s1), qxy));
+    }
+}
+
+__device__ __forceinline__ void flag_err(int* err, int which)
+{
+    atomicAdd(&err[which], 1);
+}
+
+#define GRID_STRIDE(i, begin, end)                                                                  \
+    for (long long i = (long long)(begin) + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)(end); \
+         i += (long long)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- K1 / K6 project
+// internal value = (sum of the 2^D children in children order) / 2^D   (prediction.hpp:51-60)
+template <int D>
+__global__ void k_project(Geo g, Tree t, Fld F, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
+    const int ny = g.ny[li], ny1 = g.ny[li + 1];
+    const long long cap = g.cap[li], cap1 = g.cap[li + 1];
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        int px, py;
+        lin2xy<D>(t.cells[m - g.J0][s], ny, px, py);
+        int cs[1 << D];
+        bool ok = true;
+        for (int c = 0; c < (1 << D); ++c)
+        {
+            const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+            const int sl = t.map[li + 1][xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)];
+            cs[c] = sl;
+            ok = ok && sl >= 0;
+        }
+        if (!ok)
+        {
+            flag_err(aux.err, 0);
+            continue;
+        }
+        for (int h = 0; h < g.q; ++h)
+        {
+            const double* src = F.f[li + 1] + (long long)h * cap1;
+            double acc = 0.0;
+            for (int c = 0; c < (1 << D); ++c)
+                acc = __dadd_rn(acc, src[cs[c]]);
+            F.f[li][(long long)h * cap + s] = __ddiv_rn(acc, (double)(1 << D));
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K2 details
+// d = f - predict; metric = max over siblings and populations
+// (PAPER.md:656); keep iff metric >= eps_l (Eq. 10), blow-up
+// refinement iff metric >= 2^{mu+D} eps_l
+template <int D>
+__global__ void k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int l = m + 1;
+    const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
+    const int ny = g.ny[li], ny1 = g.ny[li + 1];
+    const long long cap = g.cap[li], cap1 = g.cap[li + 1];
+    const double eps_l = ldexp(sc->eps, D * (l - g.J1));
+    const double eps_b = ldexp(eps_l, sc->mu + D);
+    const bool can_b = (l > g.J0) && (l < g.J1);
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        const int plin = t.cells[li][s];
+        int px, py;
+        lin2xy<D>(plin, ny, px, py);
+        constexpr int NS = D == 1 ? 3 : 9;
+        int st[NS];
+        bool ok = true;
+        for (int o = 0; o < NS; ++o)
+        {
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            const int sl = t.map[li][mr_lin<D>(g, m, px + ox, py + oy)];
+            st[o] = sl;
+            ok = ok && sl >= 0 && sl < nL + nI;
+        }
+        int cs[1 << D];
+        for (int c = 0; c < (1 << D); ++c)
+        {
+            const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+            cs[c] = t.map[li + 1][xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)];
+            ok = ok && cs[c] >= 0;
+        }
+        if (!ok)
+        {
+            flag_err(aux.err, 0);
+            continue;
+        }
+        double metric = 0.0;
+        for (int h = 0; h < g.q; ++h)
+        {
+            const double* fm = F.f[li] + (long long)h * cap;
+            const double* f1 = F.f[li + 1] + (long long)h * cap1;
+            double sv[NS];
+            for (int o = 0; o < NS; ++o)
+                sv[o] = fm[st[o]];
+            for (int c = 0; c < (1 << D); ++c)
+            {
+                const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+                const double d = __dsub_rn(f1[cs[c]], mr_predict<D>(sv, dx, dy));
+                const double ad = fabs(d);
+                if (ad > metric)
+                    metric = ad;
+            }
+        }
+        if (metric >= eps_l)
+            fl.keep[li][plin] = 1;
+        if (can_b && metric >= eps_b)
+        {
+            // H(b): refine the 2^D children of every cell of the group
+            for (int c = 0; c < (1 << D); ++c)
+            {
+                const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+                fl.rn[li + 1][xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)] = 1;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K3 flags
+// T closure: ancestors of kept groups are kept (Decision D.4)
+template <int D>
+__global__ void k_closure(Geo g, Tree t, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
+    const int ny = g.ny[li], nyp = g.ny[li - 1];
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        const int plin = t.cells[li][s];
+        if (!fl.keep[li][plin])
+            continue;
+        int px, py;
+        lin2xy<D>(plin, ny, px, py);
+        fl.keep[li - 1][xy2lin<D>(px >> 1, py >> 1, nyp)] = 1;
+    }
+}
+
+// rn |= keep;  H(a): (l, k - eta^h) for k in R(T) at level l = m + 1
+template <int D>
+__global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, int m)
+{
+    const int li = m - g.J0;
+    const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
+    const int ny = g.ny[li];
+    const int nx1 = g.nx[li + 1], ny1 = g.ny[li + 1];
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        const int plin = t.cells[li][s];
+        if (!fl.keep[li][plin])
+            continue;
+        fl.rn[li][plin] = 1;
+        int px, py;
+        lin2xy<D>(plin, ny, px, py);
+        for (int c = 0; c < (1 << D); ++c)
+        {
+            const int cx = 2 * px + (D == 1 ? c : (c >> 1)), cy = D == 1 ? 0 : 2 * py + (c & 1);
+            for (int h = 0; h < sc->q; ++h)
+            {
+                const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
+                if (ex == 0 && ey == 0)
+                    continue;
+                int x = cx - ex, y = cy - ey;
+                if (!g.per0 && (x < 0 || x >= nx1))
+                    continue;
+                if (D == 2 && !g.per1 && (y < 0 || y >= ny1))
+                    continue;
+                x = mr_coord(x, nx1, 1);
+                if (D == 2)
+                    y = mr_coord(y, ny1, 1);
+                fl.rn[li][xy2lin<D>(x >> 1, y >> 1, ny)] = 1;
+            }
+        }
+    }
+}
+
+// grading G: for p refined at level m, its 3^D box must be in R_m, i.e. the
+// parents of the box at level m-1 are refined (one fine->coarse sweep, Decision D.7)
+template <int D>
+__global__ void k_grade(Geo g, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li], nyp = g.ny[li - 1];
+    const long long n = (long long)nx * ny;
+    GRID_STRIDE(i, 0, n)
+    {
+        if (!fl.rn[li][i])
+            continue;
+        int px, py;
+        lin2xy<D>((int)i, ny, px, py);
+        for (int ox = -1; ox <= 1; ++ox)
+            for (int oy = (D == 1 ? 0 : -1); oy <= (D == 1 ? 0 : 1); ++oy)
+            {
+                int x = px + ox, y = py + oy;
+                if (!g.per0 && (x < 0 || x >= nx))
+                    continue;
+                if (D == 2 && !g.per1 && (y < 0 || y >= ny))
+                    continue;
+                x = mr_coord(x, nx, 1);
+                if (D == 2)
+                    y = mr_coord(y, ny, 1);
+                fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, nyp)] = 1;
+            }
+    }
+}
+
+// ---------------------------------------------------------------- K4 kinds, fallback, ghosts, compaction
+template <int D>
+__global__ void k_kinds(Geo g, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int ny = g.ny[li], nyp = li > 0 ? g.ny[li - 1] : 1;
+    const long long n = (long long)g.nx[li] * ny;
+    GRID_STRIDE(i, 0, n)
+    {
+        int x, y;
+        lin2xy<D>((int)i, ny, x, y);
+        const bool inR = (m == g.J0) || fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, nyp)];
+        const bool ref = (m < g.J1) && fl.rn[li][i];
+        fl.kind[li][i] = inR ? (ref ? K_INT : K_LEAF) : 0;
+    }
+}
+
+// table validity (Decision D.13): the 5^D box of a leaf is inside (or periodic)
+// and holds no internal cell; else the leaf streams by the recursive path
+template <int D>
+__global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li];
+    const long long n = (long long)nx * ny;
+    GRID_STRIDE(i, 0, n)
+    {
+        if (fl.kind[li][i] != K_LEAF)
+            continue;
+        int x, y;
+        lin2xy<D>((int)i, ny, x, y);
+        bool fb = false;
+        for (int ox = -2; ox <= 2 && !fb; ++ox)
+            for (int oy = (D == 1 ? 0 : -2); oy <= (D == 1 ? 0 : 2) && !fb; ++oy)
+            {
+                int xx = x + ox, yy = y + oy;
+                if (!g.per0 && (xx < 0 || xx >= nx))
+                {
+                    fb = true;
+                    break;
+                }
+                if (D == 2 && !g.per1 && (yy < 0 || yy >= ny))
+                {
+                    fb = true;
+                    break;
+                }
+                xx = mr_coord(xx, nx, 1);
+                if (D == 2)
+                    yy = mr_coord(yy, ny, 1);
+                if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
+                    fb = true;
+            }
+        if (fb)
+        {
+            fl.kind[li][i] = K_LEAF | K_FB;
+            if (m < g.J1)
+            {
+                const int k = atomicAdd(aux.fb_count, 1);
+                if (k < aux.fb_cap)
+                    aux.fb_list[k] = make_int2(m, (int)i);
+                else
+                    flag_err(aux.err, 2);
+            }
+            else
+                atomicAdd(aux.fb_count + 1, 1); // gap-0 fallback leaves need no band
+        }
+    }
+}
+
+// mark the reconstruction band (2 cells outside / inside the leaf boundary) at
+// every finer level as virtual (materialised zero-detail reconstruction)
+template <int D>
+__global__ void k_band(Geo g, Flags fl, Aux aux)
+{
+    const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
+    for (int it = blockIdx.x; it < nfb; it += gridDim.x)
+    {
+        const int2 e = aux.fb_list[it];
+        const int l = e.x;
+        int kx, ky;
+        lin2xy<D>(e.y, g.ny[l - g.J0], kx, ky);
+        for (int m = l + 1; m <= g.J1; ++m)
+        {
+            const int li = m - g.J0;
+            const int nx = g.nx[li], ny = g.ny[li];
+            const int side = 1 << (m - l);
+            const int bx0 = kx * side, by0 = ky * side;
+            const int S = side + 4;
+            long long total;
+            if (D == 1)
+                total = side <= 4 ? S : 8;
+            else
+                total = side <= 4 ? (long long)S * S : (long long)S * S - (long long)(side - 4) * (side - 4);
+            for (long long t = threadIdx.x; t < total; t += blockDim.x)
+            {
+                int x, y = 0;
+                if (D == 1)
+                {
+                    if (side <= 4)
+                        x = bx0 - 2 + (int)t;
+                    else
+                        x = t < 4 ? bx0 - 2 + (int)t : bx0 + side - 2 + (int)(t - 4);
+                }
+                else if (side <= 4)
+                {
+                    x = bx0 - 2 + (int)(t / S);
+                    y = by0 - 2 + (int)(t % S);
+                }
+                else
+                {
+                    const long long top = 4LL * S;
+                    if (t < top)
+                    {
+                        x = bx0 - 2 + (int)(t / S);
+                        y = by0 - 2 + (int)(t % S);
+                    }
+                    else if (t < top + (long long)(side - 4) * 8)
+                    {
+                        const long long u = t - top;
+                        x = bx0 + 2 + (int)(u / 8);
+                        const int c = (int)(u % 8);
+                        y = c < 4 ? by0 - 2 + c : by0 + side - 2 + (c - 4);
+                    }
+                    else
+                    {
+                        const long long u = t - top - (long long)(side - 4) * 8;
+                        x = bx0 + side - 2 + (int)(u / S);
+                        y = by0 - 2 + (int)(u % S);
+                    }
+                }
+                if (!g.per0 && (x < 0 || x >= nx))
+                    continue;
+                if (D == 2 && !g.per1 && (y < 0 || y >= ny))
+                    continue;
+                x = mr_coord(x, nx, 1);
+                if (D == 2)
+                    y = mr_coord(y, ny, 1);
+                const int lin = xy2lin<D>(x, y, ny);
+                if ((fl.kind[li][lin] & (K_LEAF | K_INT)) == 0)
+                    fl.kind[li][lin] = K_VIRT;
+            }
+        }
+    }
+}
+
+// ghost layer: cells not in R within Chebyshev distance 2 of an R cell
+template <int D>
+__global__ void k_ghost(Geo g, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li];
+    const long long n = (long long)nx * ny;
+    GRID_STRIDE(i, 0, n)
+    {
+        if (fl.kind[li][i] != 0)
+            continue;
+        int x, y;
+        lin2xy<D>((int)i, ny, x, y);
+        bool near = false;
+        for (int ox = -2; ox <= 2 && !near; ++ox)
+            for (int oy = (D == 1 ? 0 : -2); oy <= (D == 1 ? 0 : 2); ++oy)
+            {
+                int xx = x + ox, yy = y + oy;
+                if (!g.per0 && (xx < 0 || xx >= nx))
+                    continue;
+                if (D == 2 && !g.per1 && (yy < 0 || yy >= ny))
+                    continue;
+                xx = mr_coord(xx, nx, 1);
+                if (D == 2)
+                    yy = mr_coord(yy, ny, 1);
+                if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & (K_LEAF | K_INT))
+                {
+                    near = true;
+                    break;
+                }
+            }
+        if (near)
+            fl.kind[li][i] = K_VIRT;
+    }
+}
+
+// compaction: per-tile counts -> tile scan -> ballot/prefix scatter (lexicographic)
+constexpr int kTileThreads = 256;
+constexpr int kCellsPerThread = 16;
+constexpr int kTile = kTileThreads * kCellsPerThread;
+
+__device__ __forceinline__ int cat_of(uint8_t k)
+{
+    return (k & K_LEAF) ? 0 : (k & K_INT) ? 1 : (k & K_VIRT) ? 2 : 3;
+}
+
+__global__ void k_tile_count(const uint8_t* kind, long long n, int* tile_counts)
+{
+    __shared__ int red[3][kTileThreads / 32];
+    const long long tile = blockIdx.x;
+    const long long base = tile * kTile + (long long)threadIdx.x * kCellsPerThread;
+    int c[3] = {0, 0, 0};
+    for (int j = 0; j < kCellsPerThread; ++j)
+    {
+        const long long i = base + j;
+        if (i < n)
+        {
+            const int ct = cat_of(kind[i]);
+            if (ct < 3)
+                ++c[ct];
+        }
+    }
+    for (int k = 0; k < 3; ++k)
+    {
+        int v = c[k];
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0)
+            red[k][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3)
+    {
+        int v = 0;
+        for (int w = 0; w < kTileThreads / 32; ++w)
+            v += red[threadIdx.x][w];
+        tile_counts[tile * 3 + threadIdx.x] = v;
+    }
+}
+
+// single block: exclusive scan of the tile counts per category; totals -> cnt
+__global__ void k_tile_scan(int* tile_counts, int ntiles, int* cnt)
+{
+    __shared__ int part[3][1024];
+    const int T = blockDim.x;
+    const int per = (ntiles + T - 1) / T;
+    const int b = threadIdx.x * per, e = min(ntiles, b + per);
+    int loc[3] = {0, 0, 0};
+    for (int t = b; t < e; ++t)
+        for (int k = 0; k < 3; ++k)
+            loc[k] += tile_counts[t * 3 + k];
+    for (int k = 0; k < 3; ++k)
+        part[k][threadIdx.x] = loc[k];
+    __syncthreads();
+    if (threadIdx.x < 3)
+    {
+        int run = 0;
+        for (int i = 0; i < T; ++i)
+        {
+            const int v = part[threadIdx.x][i];
+            part[threadIdx.x][i] = run;
+            run += v;
+        }
+        cnt[threadIdx.x] = run;
+    }
+    __syncthreads();
+    int run[3] = {part[0][threadIdx.x], part[1][threadIdx.x], part[2][threadIdx.x]};
+    for (int t = b; t < e; ++t)
+        for (int k = 0; k < 3; ++k)
+        {
+            const int v = tile_counts[t * 3 + k];
+            tile_counts[t * 3 + k] = run[k];
+            run[k] += v;
+        }
+}
+
+__global__ void k_tile_scatter(const uint8_t* kind, long long n, const int* tile_offsets, const int* cnt,
+                               int32_t* map, int32_t* cells)
+{
+    __shared__ int wsum[3][kTileThreads / 32];
+    const long long tile = blockIdx.x;
+    const long long base = tile * kTile + (long long)threadIdx.x * kCellsPerThread;
+    uint8_t kv[kCellsPerThread];
+    int c[3] = {0, 0, 0};
+    for (int j = 0; j < kCellsPerThread; ++j)
+    {
+        const long long i = base + j;
+        kv[j] = i < n ? kind[i] : 0;
+        const int ct = cat_of(kv[j]);
+        if (ct < 3)
+            ++c[ct];
+    }
+    // block exclusive scan of per-thread counts (warp shuffles + warp totals)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int pre[3];
+    for (int k = 0; k < 3; ++k)
+    {
+        int v = c[k];
+        for (int o = 1; o < 32; o <<= 1)
+        {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
+        }
+        pre[k] = v - c[k];
+        if (lane == 31)
+            wsum[k][wid] = v;
+    }
+    __syncthreads();
+    const int catbase[3] = {0, cnt[0], cnt[0] + cnt[1]};
+    int pos[3];
+    for (int k = 0; k < 3; ++k)
+    {
+        int wpre = 0;
+        for (int w = 0; w < wid; ++w)
+            wpre += wsum[k][w];
+        pos[k] = catbase[k] + tile_offsets[tile * 3 + k] + wpre + pre[k];
+    }
+    for (int j = 0; j < kCellsPerThread; ++j)
+    {
+        const long long i = base + j;
+        if (i >= n)
+            break;
+        const int ct = cat_of(kv[j]);
+        if (ct < 3)
+        {
+            const int sl = pos[ct]++;
+            map[i] = sl;
+            cells[sl] = (int)i;
+        }
+        else
+            map[i] = -1;
+    }
+}
+
+// ---------------------------------------------------------------- K5 transfer, virtual values
+// new R cell: old value if it was in the old complete tree (copy / projected),
+// else prediction from the new level m-1 values (Decision D.24)
+template <int D>
+__global__ void k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int nL = tn.cnt[li * 4 + 0], nI = tn.cnt[li * 4 + 1];
+    const int onR = to.cnt[li * 4 + 0] + to.cnt[li * 4 + 1];
+    const int ny = g.ny[li];
+    const long long cap = g.cap[li];
+    GRID_STRIDE(s, 0, nL + nI)
+    {
+        const int lin = tn.cells[li][s];
+        const int os = to.map[li][lin];
+        if (os >= 0 && os < onR)
+        {
+            for (int h = 0; h < g.q; ++h)
+                F1.f[li][(long long)h * cap + s] = F0.f[li][(long long)h * cap + os];
+            continue;
+        }
+        if (m == g.J0)
+        {
+            flag_err(aux.err, 2);
+            continue;
+        }
+        int x, y;
+        lin2xy<D>(lin, ny, x, y);
+        const int px = x >> 1, py = y >> 1, dx = x & 1, dy = y & 1;
+        constexpr int NS = D == 1 ? 3 : 9;
+        int st[NS];
+        const int pnR = tn.cnt[(li - 1) * 4 + 0] + tn.cnt[(li - 1) * 4 + 1];
+        bool ok = true;
+        for (int o = 0; o < NS; ++o)
+        {
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            st[o] = tn.map[li - 1][mr_lin<D>(g, m - 1, px + ox, py + oy)];
+            ok = ok && st[o] >= 0 && st[o] < pnR;
+        }
+        if (!ok)
+        {
+            flag_err(aux.err, 0);
+            continue;
+        }
+        const long long capp = g.cap[li - 1];
+        for (int h = 0; h < g.q; ++h)
+        {
+            double sv[NS];
+            for (int o = 0; o < NS; ++o)
+                sv[o] = F1.f[li - 1][(long long)h * capp + st[o]];
+            F1.f[li][(long long)h * cap + s] = mr_predict<D>(sv, dx, dy);
+        }
+    }
+}
+
+// virtual cells (ghosts + reconstruction bands): zero-detail prediction from level m-1
+template <int D>
+__global__ void k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int nR = tn.cnt[li * 4 + 0] + tn.cnt[li * 4 + 1], nV = tn.cnt[li * 4 + 2];
+    const int ny = g.ny[li];
+    const long long cap = g.cap[li], capp = g.cap[li - 1];
+    GRID_STRIDE(s, nR, nR + nV)
+    {
+        const int lin = tn.cells[li][s];
+        int x, y;
+        lin2xy<D>(lin, ny, x, y);
+        const int px = x >> 1, py = y >> 1, dx = x & 1, dy = y & 1;
+        constexpr int NS = D == 1 ? 3 : 9;
+        int st[NS];
+        bool ok = true;
+        for (int o = 0; o < NS; ++o)
+        {
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            st[o] = tn.map[li - 1][mr_lin<D>(g, m - 1, px + ox, py + oy)];
+            ok = ok && st[o] >= 0;
+        }
+        if (!ok)
+        {
+            flag_err(aux.err, 0);
+            continue;
+        }
+        for (int h = 0; h < g.q; ++h)
+        {
+            double sv[NS];
+            for (int o = 0; o < NS; ++o)
+                sv[o] = F1.f[li - 1][(long long)h * capp + st[o]];
+            F1.f[li][(long long)h * cap + s] = mr_predict<D>(sv, dx, dy);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K7/K8 stream + collide
+__device__ void equilibrium(const SchemeDev& sc, const double* m, double* meq)
+{
+    const double* P = sc.eqp;
+    switch (sc.eq)
+    {
+        case MRLBM_EQ_BURGERS_D1Q2:
+        {
+            const double u = m[0];
+            meq[0] = u;
+            meq[1] = __dmul_rn(__dmul_rn(0.5, u), u);
+            break;
+        }
+        case MRLBM_EQ_EULER_D1Q3X3:
+        {
+            const double gam = P[0];
+            const double lam2 = __dmul_rn(sc.lambda, sc.lambda);
+            const double rho = m[0], q = m[3], E = m[6];
+            const double u = __ddiv_rn(q, rho);
+            const double p = __dmul_rn(__dsub_rn(gam, 1.0), __dsub_rn(E, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rho), u), u)));
+            const double F[3] = {q, __dadd_rn(__dmul_rn(q, u), p), __dmul_rn(u, __dadd_rn(E, p))};
+            const double U[3] = {rho, q, E};
+            for (int i = 0; i < 3; ++i)
+            {
+                meq[3 * i + 0] = U[i];
+                meq[3 * i + 1] = F[i];
+                meq[3 * i + 2] = __dmul_rn(lam2, U[i]);
+            }
+            break;
+        }
+        case MRLBM_EQ_ADVECTION_D2Q4:
+        {
+            const double u = m[0];
+            meq[0] = u;
+            meq[1] = __dmul_rn(P[0], u);
+            meq[2] = __dmul_rn(P[1], u);
+            meq[3] = 0.0;
+            break;
+        }
+        case MRLBM_EQ_EULER_D2Q4X4:
+        {
+            const double gam = P[0];
+            const double rho = m[0], qx = m[4], qy = m[8], E = m[12];
+            const double u = __ddiv_rn(qx, rho);
+            const double v = __ddiv_rn(qy, rho);
+            const double ke = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
+            const double p = __dmul_rn(__dsub_rn(gam, 1.0), __dsub_rn(E, __dmul_rn(__dmul_rn(0.5, rho), ke)));
+            const double Fx[4] = {qx, __dadd_rn(__dmul_rn(qx, u), p), __dmul_rn(qx, v), __dmul_rn(u, __dadd_rn(E, p))};
+            const double Fy[4] = {qy, __dmul_rn(qy, u), __dadd_rn(__dmul_rn(qy, v), p), __dmul_rn(v, __dadd_rn(E, p))};
+            const double U[4] = {rho, qx, qy, E};
+            for (int i = 0; i < 4; ++i)
+            {
+                meq[4 * i + 0] = U[i];
+                meq[4 * i + 1] = Fx[i];
+                meq[4 * i + 2] = Fy[i];
+                meq[4 * i + 3] = 0.0;
+            }
+            break;
+        }
+        case MRLBM_EQ_NS_D2Q9:
+        {
+            const double cs2 = P[0];
+            const double rho = m[0], qx = m[1], qy = m[2];
+            meq[0] = rho;
+            meq[1] = qx;
+            meq[2] = qy;
+            if (P[1] == 0.0)
+            {
+                const double q2 = __dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy));
+                meq[3] = __dmul_rn(3.0, __dadd_rn(__dmul_rn(__dmul_rn(-2.0, cs2), rho), __ddiv_rn(q2, rho)));
+                meq[6] = __dmul_rn(9.0, __dsub_rn(__dmul_rn(__dmul_rn(cs2, cs2), rho), __ddiv_rn(__dmul_rn(cs2, q2), rho)));
+            }
+            else
+            {
+                const double qn = __dsqrt_rn(__dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)));
+                meq[3] = __dmul_rn(3.0, __dadd_rn(__dmul_rn(__dmul_rn(-2.0, cs2), rho), __ddiv_rn(qn, rho)));
+                meq[6] = __dmul_rn(9.0, __dsub_rn(__dmul_rn(cs2, cs2), __ddiv_rn(__dmul_rn(cs2, qn), rho)));
+            }
+            meq[4] = __dmul_rn(__dmul_rn(-3.0, cs2), qx);
+            meq[5] = __dmul_rn(__dmul_rn(-3.0, cs2), qy);
+            meq[7] = __ddiv_rn(__dsub_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)), rho);
+            meq[8] = __ddiv_rn(__dmul_rn(qx, qy), rho);
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+// value of the finest cell (x, y) for the fallback E/A sums: inside -> the
+// materialised reconstruction (leaf or virtual slot at J1); outside -> boundary
+// rule by direct evaluation
+template <int D, int Q>
+__device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev& sc, int x,
+                                            int y, int h, const double* fstar, Aux& aux)
+{
+    const int lj = g.J1 - g.J0;
+    const int nx = g.nx[lj], ny = g.ny[lj];
+    int face = -1;
+    if (!g.per0 && (x < 0 || x >= nx))
+        face = x < 0 ? 0 : 1;
+    else if (D == 2 && !g.per1 && (y < 0 || y >= ny))
+        face = y < 0 ? 2 : 3;
+    if (face < 0)
+    {
+        const int lin = mr_lin<D>(g, g.J1, x, y);
+        const int sl = tn.map[lj][lin];
+        if (sl < 0)
+        {
+            flag_err(aux.err, 0);
+            return 0.0;
+        }
+        return F1.f[lj][(long long)h * g.cap[lj] + sl];
+    }
+    const int kind = sc.bc_kind[face];
+    if (kind == MRLBM_BC_COPY)
+    {
+        // leaf covering the clamped finest cell
+        const int cx = mr_coord(x, nx, 0), cy = D == 2 ? mr_coord(y, ny, 0) : 0;
+        for (int m = g.J1; m >= g.J0; --m)
+        {
+            const int li = m - g.J0;
+            const int sh = g.J1 - m;
+            const int sl = tn.map[li][xy2lin<D>(cx >> sh, cy >> sh, g.ny[li])];
+            if (sl >= 0 && sl < tn.cnt[li * 4 + 0])
+                return F1.f[li][(long long)h * g.cap[li] + sl];
+        }
+        flag_err(aux.err, 0);
+        return 0.0;
+    }
+    const int hb = sc.opp[h];
+    if (hb < 0)
+    {
+        flag_err(aux.err, 2);
+        return 0.0;
+    }
+    if (kind == MRLBM_BC_BOUNCE_BACK)
+        return fstar[hb];
+    if (kind == MRLBM_BC_ANTI_BOUNCE_BACK)
+        return -fstar[hb];
+    return __dadd_rn(fstar[hb], sc.bc_add[face][h]);
+}
+
+template <int D>
+__device__ __forceinline__ bool in_box(int x, int y, int bx0, int bx1, int by0, int by1)
+{
+    return x >= bx0 && x < bx1 && (D == 1 || (y >= by0 && y < by1));
+}
+
+// sum over the E (side 0) / A (side 1) finest cells in lexicographic order.
+// E and A lie in the one-cell rim inside / outside the leaf's finest box B, so
+// only rows x in {bx0-1, bx0, bx1-1, bx1} are scanned in full; the rows between
+// contribute their end columns {by0-1, by0, by1-1, by1} only.
+template <int D, int Q>
+__device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev& sc, int h, int side, int bx0,
+                          int bx1, int by0, int by1, const double* fstar, Aux& aux)
+{
+    const int ex = sc.eta[h][0], ey = D == 1 ? 0 : sc.eta[h][1];
+    double s = 0.0;
+    if (ex == 0 && ey == 0)
+        return s;
+    auto visit = [&](int x, int y)
+    {
+        const bool inb = in_box<D>(x, y, bx0, bx1, by0, by1);
+        const bool ine = in_box<D>(x + ex, y + ey, bx0, bx1, by0, by1);
+        if (side == 0 ? (ine && !inb) : (inb && !ine))
+            s = __dadd_rn(s, rim_value<D, Q>(g, tn, F1, sc, x, y, h, fstar, aux));
+    };
+    const int rows[4] = {bx0 - 1, bx0, bx1 - 1, bx1};
+    int prev_row = INT_MIN;
+    for (int r = 0; r < 4; ++r)
+    {
+        const int x = rows[r];
+        if (x == prev_row)
+            continue;
+        // interior rows strictly between the previous edge row and this one
+        if (D == 2 && prev_row != INT_MIN)
+        {
+            const int ys[4] = {by0 - 1, by0, by1 - 1, by1};
+            for (int xi = prev_row + 1; xi < x; ++xi)
+            {
+                int prev = INT_MIN;
+                for (int k = 0; k < 4; ++k)
+                {
+                    if (ys[k] == prev)
+                        continue;
+                    prev = ys[k];
+                    visit(xi, ys[k]);
+                }
+            }
+        }
+        prev_row = x;
+        if (D == 1)
+            visit(x, 0);
+        else
+            for (int y = by0 - 1; y <= by1; ++y)
+                visit(x, y);
+    }
+    return s;
+}
+
+template <int D, int Q>
+__global__ void __launch_bounds__(128) k_stream_collide(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* scg, int m,
+                                                        Aux aux)
+{
+    __shared__ SchemeDev sc;
+    {
+        const int* src = reinterpret_cast<const int*>(scg);
+        int* dst = reinterpret_cast<int*>(&sc);
+        for (int i = threadIdx.x; i < (int)(sizeof(SchemeDev) / sizeof(int)); i += blockDim.x)
+            dst[i] = src[i];
+    }
+    __syncthreads();
+    const int li = m - g.J0;
+    const int nL = tn.cnt[li * 4 + 0];
+    const int nx = g.nx[li], ny = g.ny[li];
+    const long long cap = g.cap[li];
+    const int gap = g.J1 - m;
+    const double scale = ldexp(1.0, D * (m - g.J1));
+    const int bs = sc.bs;
+    GRID_STRIDE(s, 0, nL)
+    {
+        const int lin = tn.cells[li][s];
+        int x, y;
+        lin2xy<D>(lin, ny, x, y);
+        const bool fb = (fl.kind[li][lin] & K_FB) != 0;
+        double fs[Q], f[Q];
+        for (int h = 0; h < Q; ++h)
+            fs[h] = F1.f[li][(long long)h * cap + s];
+        if (!fb)
+        {
+            for (int h = 0; h < Q; ++h)
+            {
+                double sum[2];
+                for (int side = 0; side < 2; ++side)
+                {
+                    const int2 ti = aux.tidx[(gap * Q + h) * 2 + side];
+                    double acc = 0.0;
+                    for (int e = ti.x; e < ti.x + ti.y; ++e)
+                    {
+                        const int2 o = aux.toff[e];
+                        int xx = x + o.x, yy = y + o.y;
+                        if (g.per0)
+                            xx = mr_coord(xx, nx, 1);
+                        if (D == 2 && g.per1)
+                            yy = mr_coord(yy, ny, 1);
+                        const int sl = tn.map[li][xy2lin<D>(xx, yy, ny)];
+                        if (sl < 0)
+                        {
+                            flag_err(aux.err, 0);
+                            continue;
+                        }
+                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[e], F1.f[li][(long long)h * cap + sl]));
+                    }
+                    sum[side] = acc;
+                }
+                f[h] = __dadd_rn(fs[h], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+            }
+        }
+        else
+        {
+            const int side_n = 1 << gap;
+            const int bx0 = x * side_n, bx1 = bx0 + side_n;
+            const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
+            for (int h = 0; h < Q; ++h)
+            {
+                const double sE = rim_sum<D, Q>(g, tn, F1, sc, h, 0, bx0, bx1, by0, by1, fs, aux);
+                const double sA = rim_sum<D, Q>(g, tn, F1, sc, h, 1, bx0, bx1, by0, by1, fs, aux);
+                f[h] = __dadd_rn(fs[h], __dmul_rn(scale, __dsub_rn(sE, sA)));
+            }
+        }
+        // collide: m = M f; m' = (1-s) m + s meq; f* = M^-1 m'
+        double mo[Q], meq[Q];
+        for (int i = 0; i < Q; ++i)
+        {
+            const int b0 = (i / bs) * bs;
+            double acc = 0.0;
+            for (int j = b0; j < b0 + bs; ++j)
+                acc = __dadd_rn(acc, __dmul_rn(sc.M[i * Q + j], f[j]));
+            mo[i] = acc;
+        }
+        equilibrium(sc, mo, meq);
+        for (int i = 0; i < Q; ++i)
+            mo[i] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, sc.s[i]), mo[i]), __dmul_rn(sc.s[i], meq[i]));
+        bool bad = false;
+        for (int i = 0; i < Q; ++i)
+        {
+            const int b0 = (i / bs) * bs;
+            double acc = 0.0;
+            for (int j = b0; j < b0 + bs; ++j)
+                acc = __dadd_rn(acc, __dmul_rn(sc.Minv[i * Q + j], mo[j]));
+            f[i] = acc;
+        }
+        if (sc.obstacle == 1 && D == 2)
+        {
+            // config 5 volume-fraction blend
+            const double dx = ldexp(1.0, -m);
+            const double x0 = __dadd_rn(sc.origin[0], __dmul_rn((double)x, dx));
+            const double y0 = __dadd_rn(sc.origin[1], __dmul_rn((double)y, dx));
+            const double x1 = __dadd_rn(x0, dx), y1 = __dadd_rn(y0, dx);
+            const bool cand = !(x1 < __dsub_rn(sc.obs_c[0], sc.obs_r) || x0 > __dadd_rn(sc.obs_c[0], sc.obs_r) ||
+                                y1 < __dsub_rn(sc.obs_c[1], sc.obs_r) || y0 > __dadd_rn(sc.obs_c[1], sc.obs_r));
+            if (cand)
+            {
+                const int ns = sc.obs_ns;
+                const double r2 = __dmul_rn(sc.obs_r, sc.obs_r);
+                int cnt = 0;
+                for (int a = 0; a < ns; ++a)
+                {
+                    const double sx = __dadd_rn(sc.origin[0], __dmul_rn(__dadd_rn((double)x, __ddiv_rn((double)a + 0.5, (double)ns)), dx));
+                    const double ddx = __dsub_rn(sx, sc.obs_c[0]);
+                    const double rx = __dmul_rn(ddx, ddx);
+                    for (int b = 0; b < ns; ++b)
+                    {
+                        const double sy = __dadd_rn(sc.origin[1], __dmul_rn(__dadd_rn((double)y, __ddiv_rn((double)b + 0.5, (double)ns)), dx));
+                        const double ddy = __dsub_rn(sy, sc.obs_c[1]);
+                        cnt += __dadd_rn(rx, __dmul_rn(ddy, ddy)) < r2;
+                    }
+                }
+                if (cnt > 0)
+                {
+                    const double alpha = __ddiv_rn((double)cnt, (double)(ns * ns));
+                    for (int h = 0; h < Q; ++h)
+                        f[h] = __dadd_rn(__dmul_rn(alpha, sc.obs_feq[h]), __dmul_rn(__dsub_rn(1.0, alpha), f[h]));
+                }
+            }
+        }
+        for (int h = 0; h < Q; ++h)
+        {
+            bad = bad || !isfinite(f[h]);
+            F0.f[li][(long long)h * cap + s] = f[h];
+        }
+        if (bad)
+            flag_err(aux.err, 1);
+    }
+}
+
+__global__ void k_count_updates(const int* cnt, int nlev, long long* acc)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+    {
+        long long s = 0;
+        for (int i = 0; i < nlev; ++i)
+            s += cnt[i * 4];
+        *acc += s;
+    }
+}
+
+// loading: mark loaded leaves and their ancestors; scatter values after compaction
+template <int D>
+__global__ void k_load_mark(Geo g, Flags fl, const int* lins, int n, int m)
+{
+    const int li = m - g.J0;
+    const int ny = g.ny[li];
+    GRID_STRIDE(i, 0, n)
+    {
+        const int lin = lins[i];
+        fl.keep[li][lin] = 1; // loaded-leaf marker
+        if (m > g.J0)
+        {
+            int x, y;
+            lin2xy<D>(lin, ny, x, y);
+            fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, g.ny[li - 1])] = 1;
+        }
+    }
+}
+
+template <int D>
+__global__ void k_closure_dense(Geo g, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int ny = g.ny[li];
+    const long long n = (long long)g.nx[li] * ny;
+    GRID_STRIDE(i, 0, n)
+    {
+        if (!fl.rn[li][i])
+            continue;
+        int x, y;
+        lin2xy<D>((int)i, ny, x, y);
+        fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, g.ny[li - 1])] = 1;
+    }
+}
+
+__global__ void k_load_scatter(const int* lins, const double* fin, int n, int q, const int32_t* map, const uint8_t* kind,
+                               double* F, long long cap, int* err)
+{
+    GRID_STRIDE(i, 0, n)
+    {
+        const int lin = lins[i];
+        const int sl = map[lin];
+        if (sl < 0 || kind[lin] != K_LEAF)
+        {
+            atomicAdd(&err[2], 1);
+            continue;
+        }
+        for (int h = 0; h < q; ++h)
+            F[(long long)h * cap + sl] = fin[(long long)h * n + i];
+    }
+}
+
+} // namespace mrlbm_b200
+
+using namespace mrlbm_b200;
+
+// ====================================================================== host context
+struct mrlbm_ctx {
+    mrlbm_scheme_spec sc{};
+    mrlbm_run_config rc{};
+    int D = 0, q = 0, J0 = 0, J1 = 0, nlev = 0;
+    Geo geo{};
+    cudaStream_t stream = nullptr;
+    int32_t* map[2][kL]{};
+    int32_t* cells[2][kL]{};
+    int* cnt[2]{};
+    uint8_t* kind[kL]{};
+    uint8_t* rn[kL]{};
+    uint8_t* keep[kL]{};
+    double* F[2][kL]{};
+    int* tiles[kL]{};
+    long long ntiles[kL]{};
+    SchemeDev* sch = nullptr;
+    int* err = nullptr;
+    int* fbc = nullptr;
+    int2* fbl = nullptr;
+    long long fbcap = 0;
+    long long* upd = nullptr;
+    int2* tidx = nullptr;
+    int2* toff = nullptr;
+    double* tw = nullptr;
+    int cur = 0;
+    bool committed = false;
+    bool profiling = false;
+    bool use_graph = true;
+    cudaGraphExec_t graph[2]{};
+    std::vector<std::vector<int32_t>> st_lin;
+    std::vector<std::vector<double>> st_f;
+    cudaEvent_t ev[16]{};
+    double phase_ms[MRLBM_PHASE_COUNT]{};
+    std::string err_msg;
+    int grid_cap = 148 * 8;
+};
+
+namespace {
+
+int set_err(mrlbm_ctx* c, int code, const std::string& msg)
+{
+    if (c)
+        c->err_msg = msg;
+    return code;
+}
+
+#define CU(call)                                                                                                       \
+    do                                                                                                                 \
+    {                                                                                                                  \
+        cudaError_t e_ = (call);                                                                                       \
+        if (e_ != cudaSuccess)                                                                                         \
+            return set_err(ctx, MRLBM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+Tree tree_of(mrlbm_ctx* c, int v)
+{
+    Tree t{};
+    for (int i = 0; i < c->nlev; ++i)
+    {
+        t.map[i] = c->map[v][i];
+        t.cells[i] = c->cells[v][i];
+    }
+    t.cnt = c->cnt[v];
+    return t;
+}
+
+Fld fld_of(mrlbm_ctx* c, int v)
+{
+    Fld f{};
+    for (int i = 0; i < c->nlev; ++i)
+        f.f[i] = c->F[v][i];
+    return f;
+}
+
+Flags flags_of(mrlbm_ctx* c)
+{
+    Flags f{};
+    for (int i = 0; i < c->nlev; ++i)
+    {
+        f.kind[i] = c->kind[i];
+        f.rn[i] = c->rn[i];
+        f.keep[i] = c->keep[i];
+    }
+    return f;
+}
+
+Aux aux_of(mrlbm_ctx* c)
+{
+    Aux a{};
+    a.err = c->err;
+    a.fb_count = c->fbc;
+    a.fb_list = c->fbl;
+    a.fb_cap = c->fbcap;
+    a.updates = c->upd;
+    a.tidx = c->tidx;
+    a.toff = c->toff;
+    a.tw = c->tw;
+    return a;
+}
+
+int grid_for(mrlbm_ctx* c, long long n, int threads = 256)
+{
+    long long b = (n + threads - 1) / threads;
+    if (b < 1)
+        b = 1;
+    if (b > c->grid_cap)
+        b = c->grid_cap;
+    return static_cast<int>(b);
+}
+
+template <int D>
+void launch_compaction(mrlbm_ctx* c, int v, int m)
+{
+    const int li = m - c->J0;
+    const long long n = c->geo.cap[li];
+    const int nt = static_cast<int>(c->ntiles[li]);
+    k_tile_count<<<nt, kTileThreads, 0, c->stream>>>(c->kind[li], n, c->tiles[li]);
+    k_tile_scan<<<1, 1024, 0, c->stream>>>(c->tiles[li], nt, c->cnt[v] + li * 4);
+    k_tile_scatter<<<nt, kTileThreads, 0, c->stream>>>(c->kind[li], n, c->tiles[li], c->cnt[v] + li * 4, c->map[v][li],
+                                                       c->cells[v][li]);
+}
+
+void phase_mark(mrlbm_ctx* c, int k)
+{
+    if (c->profiling)
+        cudaEventRecord(c->ev[k], c->stream);
+}
+
+template <int D, int Q>
+void enqueue_step(mrlbm_ctx* c)
+{
+    const int o = c->cur, n = 1 - c->cur;
+    const Geo& g = c->geo;
+    Tree to = tree_of(c, o), tn = tree_of(c, n);
+    Fld F0 = fld_of(c, 0), F1 = fld_of(c, 1);
+    Flags fl = flags_of(c);
+    Aux aux = aux_of(c);
+    cudaStream_t s = c->stream;
+    const int T = 256;
+    for (int li = 0; li < c->nlev; ++li)
+    {
+        cudaMemsetAsync(c->keep[li], 0, g.cap[li], s);
+        cudaMemsetAsync(c->rn[li], 0, g.cap[li], s);
+    }
+    cudaMemsetAsync(c->fbc, 0, 2 * sizeof(int), s);
+    phase_mark(c, 0);
+    // K1 projection of the old tree (bottom-up)
+    for (int m = c->J1 - 1; m >= c->J0; --m)
+        k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux);
+    phase_mark(c, 1);
+    // K2 details + flags
+    for (int m = c->J0; m < c->J1; ++m)
+        k_details<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux);
+    phase_mark(c, 2);
+    // K3 closure, enlargement, grading
+    for (int m = c->J1 - 1; m > c->J0; --m)
+        k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);
+    for (int m = c->J0; m < c->J1; ++m)
+        k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m);
+    for (int m = c->J1 - 1; m > c->J0; --m)
+        k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+    phase_mark(c, 3);
+    // K4 kinds, fallback flags, reconstruction bands, ghosts, compaction
+    for (int m = c->J0; m <= c->J1; ++m)
+        k_kinds<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+    for (int m = c->J0; m <= c->J1; ++m)
+        k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux);
+    k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);
+    for (int m = c->J0; m <= c->J1; ++m)
+        k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+    for (int m = c->J0; m <= c->J1; ++m)
+        launch_compaction<D>(c, n, m);
+    phase_mark(c, 4);
+    // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
+    for (int m = c->J0; m <= c->J1; ++m)
+        k_transfer<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux);
+    for (int m = c->J1 - 1; m >= c->J0; --m)
+        k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);
+    for (int m = c->J0 + 1; m <= c->J1; ++m)
+        k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);
+    phase_mark(c, 5);
+    // K7/K8 stream + collide (+ obstacle) on every new leaf
+    for (int m = c->J0; m <= c->J1; ++m)
+        k_stream_collide<D, Q><<<grid_for(c, g.cap[m - c->J0], 128), 128, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux);
+    k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);
+    phase_mark(c, 6);
+}
+
+using StepFn = void (*)(mrlbm_ctx*);
+
+StepFn step_fn(int d, int q)
+{
+    if (d == 1 && q == 2)
+        return enqueue_step<1, 2>;
+    if (d == 1 && q == 9)
+        return enqueue_step<1, 9>;
+    if (d == 2 && q == 4)
+        return enqueue_step<2, 4>;
+    if (d == 2 && q == 9)
+        return enqueue_step<2, 9>;
+    if (d == 2 && q == 16)
+        return enqueue_step<2, 16>;
+    return nullptr;
+}
+
+int check_device_errors(mrlbm_ctx* ctx)
+{
+    int e[4] = {0, 0, 0, 0};
+    CU(cudaMemcpyAsync(e, ctx->err, sizeof(e), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (e[0] || e[2])
+        return set_err(ctx, MRLBM_ERR_CAPACITY,
+                       "mesh invariant violated: unresolved stencils=" + std::to_string(e[0]) +
+                           " inconsistencies=" + std::to_string(e[2]));
+    if (e[1])
+        return set_err(ctx, MRLBM_ERR_NUMERIC, "non-finite populations after collision: " + std::to_string(e[1]));
+    return MRLBM_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_ctx** out)
+{
+    *out = nullptr;
+    mrlbm_ctx* ctx = nullptr;
+    if (!sc || !rc)
+        return MRLBM_ERR_CONFIG;
+    if (sc->d < 1 || sc->d > 2 || !step_fn(sc->d, sc->q))
+        return MRLBM_ERR_CONFIG;
+    if (rc->j_min < 0 || rc->j_max <= rc->j_min || rc->j_max - rc->j_min + 1 > kL)
+        return MRLBM_ERR_CONFIG;
+    if (rc->gamma != 1 || rc->graduation != 1 || sc->nblocks < 1 || sc->q % sc->nblocks)
+        return MRLBM_ERR_CONFIG;
+    for (int i = 0; i < sc->d; ++i)
+        if ((rc->bc_kind[2 * i] == MRLBM_BC_PERIODIC) != (rc->bc_kind[2 * i + 1] == MRLBM_BC_PERIODIC))
+            return MRLBM_ERR_CONFIG;
+    ctx = new mrlbm_ctx();
+    ctx->sc = *sc;
+    ctx->rc = *rc;
+    ctx->D = sc->d;
+    ctx->q = sc->q;
+    ctx->J0 = rc->j_min;
+    ctx->J1 = rc->j_max;
+    ctx->nlev = ctx->J1 - ctx->J0 + 1;
+    Geo& g = ctx->geo;
+    g.d = ctx->D;
+    g.q = ctx->q;
+    g.J0 = ctx->J0;
+    g.J1 = ctx->J1;
+    g.nlev = ctx->nlev;
+    g.per0 = rc->bc_kind[0] == MRLBM_BC_PERIODIC;
+    g.per1 = ctx->D == 2 && rc->bc_kind[2] == MRLBM_BC_PERIODIC;
+    for (int li = 0; li < ctx->nlev; ++li)
+    {
+        const long long nx = rc->base_cells[0] << li;
+        const long long ny = ctx->D == 2 ? (rc->base_cells[1] << li) : 1;
+        if (nx * ny >= (1LL << 31))
+        {
+            delete ctx;
+            return MRLBM_ERR_CONFIG;
+        }
+        g.nx[li] = static_cast<int>(nx);
+        g.ny[li] = static_cast<int>(ny);
+        g.cap[li] = nx * ny;
+    }
+    int dev = 0;
+    cudaError_t ce = cudaGetDevice(&dev);
+    if (ce != cudaSuccess)
+    {
+        *out = nullptr;
+        delete ctx;
+        return MRLBM_ERR_CUDA;
+    }
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev);
+    ctx->grid_cap = prop.multiProcessorCount * 8;
+    int st = [&]() -> int
+    {
+        CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        for (int v = 0; v < 2; ++v)
+        {
+            CU(cudaMalloc(&ctx->cnt[v], sizeof(int) * 4 * kL));
+            CU(cudaMemset(ctx->cnt[v], 0, sizeof(int) * 4 * kL));
+        }
+        long long total_cells = 0;
+        for (int li = 0; li < ctx->nlev; ++li)
+        {
+            const long long n = g.cap[li];
+            total_cells += n;
+            for (int v = 0; v < 2; ++v)
+            {
+                CU(cudaMalloc(&ctx->map[v][li], sizeof(int32_t) * n));
+                CU(cudaMalloc(&ctx->cells[v][li], sizeof(int32_t) * n));
+                CU(cudaMemset(ctx->map[v][li], 0xff, sizeof(int32_t) * n));
+                CU(cudaMalloc(&ctx->F[v][li], sizeof(double) * n * ctx->q));
+                CU(cudaMemset(ctx->F[v][li], 0, sizeof(double) * n * ctx->q));
+            }
+            CU(cudaMalloc(&ctx->kind[li], n));
+            CU(cudaMalloc(&ctx->rn[li], n));
+            CU(cudaMalloc(&ctx->keep[li], n));
+            ctx->ntiles[li] = (n + kTile - 1) / kTile;
+            CU(cudaMalloc(&ctx->tiles[li], sizeof(int) * 3 * ctx->ntiles[li]));
+        }
+        ctx->fbcap = total_cells;
+        CU(cudaMalloc(&ctx->fbl, sizeof(int2) * ctx->fbcap));
+        CU(cudaMalloc(&ctx->fbc, sizeof(int) * 2));
+        CU(cudaMalloc(&ctx->err, sizeof(int) * 4));
+        CU(cudaMemset(ctx->err, 0, sizeof(int) * 4));
+        CU(cudaMalloc(&ctx->upd, sizeof(long long)));
+        CU(cudaMemset(ctx->upd, 0, sizeof(long long)));
+        // scheme constants
+        SchemeDev h{};
+        h.q = sc->q;
+        h.nblocks = sc->nblocks;
+        h.bs = sc->q / sc->nblocks;
+        h.eq = sc->equilibrium;
+        h.mu = rc->mu;
+        h.lambda = sc->lambda;
+        h.eps = rc->epsilon;
+        h.obstacle = rc->obstacle;
+        h.obs_ns = rc->obstacle_subsamples;
+        for (int i = 0; i < sc->q; ++i)
+        {
+            h.eta[i][0] = sc->eta[i][0];
+            h.eta[i][1] = sc->eta[i][1];
+            h.s[i] = sc->s[i];
+            h.obs_feq[i] = rc->obstacle_feq[i];
+            h.opp[i] = -1;
+            const int bs = h.bs;
+            for (int k = 0; k < sc->q; ++k)
+                if (k / bs == i / bs && sc->eta[k][0] == -sc->eta[i][0] && (sc->d == 1 || sc->eta[k][1] == -sc->eta[i][1]))
+                {
+                    h.opp[i] = k;
+                    break;
+                }
+            for (int j = 0; j < sc->q; ++j)
+            {
+                h.M[i * sc->q + j] = sc->M[i * sc->q + j];
+                h.Minv[i * sc->q + j] = sc->Minv[i * sc->q + j];
+            }
+        }
+        for (int k = 0; k < 8; ++k)
+            h.eqp[k] = sc->eq_params[k];
+        for (int f = 0; f < 4; ++f)
+        {
+            h.bc_kind[f] = rc->bc_kind[f];
+            for (int i = 0; i < sc->q; ++i)
+                h.bc_add[f][i] = rc->bc_add[f][i];
+        }
+        h.origin[0] = rc->origin[0];
+        h.origin[1] = rc->origin[1];
+        h.obs_c[0] = rc->obstacle_center[0];
+        h.obs_c[1] = rc->obstacle_center[1];
+        h.obs_r = rc->obstacle_radius;
+        CU(cudaMalloc(&ctx->sch, sizeof(SchemeDev)));
+        CU(cudaMemcpy(ctx->sch, &h, sizeof(SchemeDev), cudaMemcpyHostToDevice));
+        // flattened tables for every gap / population / side
+        std::vector<int2> idx, off;
+        std::vector<double> w;
+        for (int gp = 0; gp < ctx->nlev; ++gp)
+            for (int hh = 0; hh < sc->q; ++hh)
+                for (int side = 0; side < 2; ++side)
+                {
+                    std::vector<TableEntry> t;
+                    const int rcode = build_stream_table(sc->d, gp, sc->eta[hh], side, t);
+                    if (rcode != MRLBM_OK)
+                        return set_err(ctx, rcode, "flattened table construction failed");
+                    idx.push_back(make_int2(static_cast<int>(off.size()), static_cast<int>(t.size())));
+                    for (const auto& e : t)
+                    {
+                        off.push_back(make_int2(e.off[0], e.off[1]));
+                        w.push_back(e.w);
+                    }
+                }
+        if (off.empty())
+        {
+            off.push_back(make_int2(0, 0));
+            w.push_back(0.0);
+        }
+        CU(cudaMalloc(&ctx->tidx, sizeof(int2) * idx.size()));
+        CU(cudaMalloc(&ctx->toff, sizeof(int2) * off.size()));
+        CU(cudaMalloc(&ctx->tw, sizeof(double) * w.size()));
+        CU(cudaMemcpy(ctx->tidx, idx.data(), sizeof(int2) * idx.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->toff, off.data(), sizeof(int2) * off.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ctx->tw, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+        for (auto& e : ctx->ev)
+            CU(cudaEventCreate(&e));
+        return MRLBM_OK;
+    }();
+    if (st != MRLBM_OK)
+    {
+        const std::string msg = ctx->err_msg;
+        mrlbm_destroy(ctx);
+        fprintf(stderr, "mrlbm_create: %s\n", msg.c_str());
+        return st;
+    }
+    ctx->st_lin.resize(ctx->nlev);
+    ctx->st_f.resize(ctx->nlev);
+    *out = ctx;
+    return MRLBM_OK;
+}
+
+int mrlbm_load_leaves(mrlbm_ctx* ctx, int level, int64_t n, const int32_t* idx, const double* f)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    if (level < ctx->J0 || level > ctx->J1 || n < 0)
+        return set_err(ctx, MRLBM_ERR_CONFIG, "load: level out of range");
+    const int li = level - ctx->J0;
+    auto& L = ctx->st_lin[li];
+    auto& V = ctx->st_f[li];
+    L.resize(n);
+    V.assign(f, f + n * ctx->q);
+    for (int64_t i = 0; i < n; ++i)
+    {
+        const int x = idx[i * ctx->D];
+        const int y = ctx->D == 2 ? idx[i * ctx->D + 1] : 0;
+        if (x < 0 || x >= ctx->geo.nx[li] || y < 0 || y >= ctx->geo.ny[li])
+            return set_err(ctx, MRLBM_ERR_CONFIG, "load: leaf outside the domain");
+        L[i] = ctx->D == 2 ? x * ctx->geo.ny[li] + y : x;
+    }
+    ctx->committed = false;
+    return MRLBM_OK;
+}
+
+int mrlbm_commit(mrlbm_ctx* ctx)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    const Geo& g = ctx->geo;
+    Flags fl = flags_of(ctx);
+    const int v = ctx->cur;
+    for (int li = 0; li < ctx->nlev; ++li)
+    {
+        CU(cudaMemsetAsync(ctx->keep[li], 0, g.cap[li], ctx->stream));
+        CU(cudaMemsetAsync(ctx->rn[li], 0, g.cap[li], ctx->stream));
+    }
+    CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
+    std::vector<int*> dl(ctx->nlev, nullptr);
+    std::vector<double*> dfv(ctx->nlev, nullptr);
+    auto cleanup = [&]()
+    {
+        for (auto p : dl)
+            if (p)
+                cudaFree(p);
+        for (auto p : dfv)
+            if (p)
+                cudaFree(p);
+    };
+    int st = [&]() -> int
+    {
+        for (int li = 0; li < ctx->nlev; ++li)
+        {
+            const long long n = ctx->st_lin[li].size();
+            if (!n)
+                continue;
+            CU(cudaMalloc(&dl[li], sizeof(int) * n));
+            CU(cudaMalloc(&dfv[li], sizeof(double) * n * ctx->q));
+            CU(cudaMemcpyAsync(dl[li], ctx->st_lin[li].data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+            CU(cudaMemcpyAsync(dfv[li], ctx->st_f[li].data(), sizeof(double) * n * ctx->q, cudaMemcpyHostToDevice,
+                               ctx->stream));
+            if (ctx->D == 1)
+                k_load_mark<1><<<grid_for(ctx, n), 256, 0, ctx->stream>>>(g, fl, dl[li], (int)n, ctx->J0 + li);
+            else
+                k_load_mark<2><<<grid_for(ctx, n), 256, 0, ctx->stream>>>(g, fl, dl[li], (int)n, ctx->J0 + li);
+        }
+        for (int m = ctx->J1 - 1; m > ctx->J0; --m)
+        {
+            if (ctx->D == 1)
+                k_closure_dense<1><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
+            else
+                k_closure_dense<2><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
+        }
+        for (int m = ctx->J0; m <= ctx->J1; ++m)
+        {
+            if (ctx->D == 1)
+            {
+                k_kinds<1><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
+                launch_compaction<1>(ctx, v, m);
+            }
+            else
+            {
+                k_kinds<2><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
+                launch_compaction<2>(ctx, v, m);
+            }
+        }
+        for (int li = 0; li < ctx->nlev; ++li)
+        {
+            const long long n = ctx->st_lin[li].size();
+            if (!n)
+                continue;
+            k_load_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(dl[li], dfv[li], (int)n, ctx->q, ctx->map[v][li],
+                                                                     ctx->kind[li], ctx->F[0][li], g.cap[li], ctx->err);
+        }
+        CU(cudaGetLastError());
+        int counts[4 * kL];
+        CU(cudaMemcpyAsync(counts, ctx->cnt[v], sizeof(int) * 4 * kL, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        for (int li = 0; li < ctx->nlev; ++li)
+            if (counts[li * 4] != static_cast<int>(ctx->st_lin[li].size()))
+                return set_err(ctx, MRLBM_ERR_CONFIG, "load: leaves do not form a complete-leaf partition (level " +
+                                                          std::to_string(ctx->J0 + li) + ")");
+        return check_device_errors(ctx);
+    }();
+    cleanup();
+    if (st != MRLBM_OK)
+        return st;
+    for (auto& s : ctx->st_lin)
+        std::vector<int32_t>().swap(s);
+    for (auto& s : ctx->st_f)
+        std::vector<double>().swap(s);
+    for (auto& gph : ctx->graph)
+        if (gph)
+        {
+            cudaGraphExecDestroy(gph);
+            gph = nullptr;
+        }
+    ctx->committed = true;
+    return MRLBM_OK;
+}
+
+int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    if (!ctx->committed)
+        return set_err(ctx, MRLBM_ERR_STATE, "step before commit");
+    StepFn fn = step_fn(ctx->D, ctx->q);
+    CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
+    CU(cudaEventRecord(ctx->ev[14], ctx->stream));
+    double phase[MRLBM_PHASE_COUNT] = {0};
+    for (int it = 0; it < nsteps; ++it)
+    {
+        if (ctx->use_graph && !ctx->profiling)
+        {
+            cudaGraphExec_t& ge = ctx->graph[ctx->cur];
+            if (!ge)
+            {
+                cudaGraph_t gr;
+                CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+                fn(ctx);
+                CU(cudaStreamEndCapture(ctx->stream, &gr));
+                CU(cudaGraphInstantiate(&ge, gr, 0));
+                cudaGraphDestroy(gr);
+            }
+            CU(cudaGraphLaunch(ge, ctx->stream));
+        }
+        else
+        {
+            fn(ctx);
+            CU(cudaGetLastError());
+            if (ctx->profiling)
+            {
+                CU(cudaEventSynchronize(ctx->ev[6]));
+                const int map_phase[6] = {MRLBM_PHASE_PROJECT, MRLBM_PHASE_DETAILS, MRLBM_PHASE_FLAGS,
+                                          MRLBM_PHASE_COMPACT, MRLBM_PHASE_TRANSFER, MRLBM_PHASE_STREAM};
+                for (int k = 0; k < 6; ++k)
+                {
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]);
+                    phase[map_phase[k]] += ms;
+                }
+            }
+        }
+        ctx->cur = 1 - ctx->cur;
+    }
+    CU(cudaEventRecord(ctx->ev[15], ctx->stream));
+    const int st = check_device_errors(ctx);
+    if (stats)
+    {
+        std::memset(stats, 0, sizeof(*stats));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[14], ctx->ev[15]);
+        stats->ms_total = ms;
+        for (int k = 0; k < MRLBM_PHASE_COUNT; ++k)
+            stats->ms_phase[k] = phase[k];
+        int counts[4 * kL];
+        int fb[2];
+        long long upd = 0;
+        CU(cudaMemcpy(counts, ctx->cnt[ctx->cur], sizeof(counts), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(fb, ctx->fbc, sizeof(fb), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(&upd, ctx->upd, sizeof(upd), cudaMemcpyDeviceToHost));
+        stats->levels = ctx->nlev;
+        long long nS = 0, nI = 0, nG = 0;
+        for (int li = 0; li < ctx->nlev; ++li)
+        {
+            stats->leaves[li] = counts[li * 4];
+            stats->internal[li] = counts[li * 4 + 1];
+            stats->virtual_cells[li] = counts[li * 4 + 2];
+            nS += counts[li * 4];
+            nI += counts[li * 4 + 1];
+            nG += counts[li * 4 + 2];
+        }
+        stats->fallback_leaves = fb[0] + fb[1];
+        stats->leaf_updates = upd;
+        // SURVEY 8d compulsory fp64 model with N_old ~ N_new (last step's counts)
+        stats->bytes_model = 8LL * ctx->q * (2 * nS + 3 * nI + 5 * nS + nI + 2 * nG);
+    }
+    return st;
+}
+
+int mrlbm_level_count(mrlbm_ctx* ctx, int level, int64_t* n)
+{
+    if (!ctx || level < ctx->J0 || level > ctx->J1)
+        return MRLBM_ERR_CONFIG;
+    int c = 0;
+    CU(cudaMemcpyAsync(&c, ctx->cnt[ctx->cur] + (level - ctx->J0) * 4, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *n = c;
+    return MRLBM_OK;
+}
+
+int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
+{
+    if (!ctx || level < ctx->J0 || level > ctx->J1)
+        return MRLBM_ERR_CONFIG;
+    const int li = level - ctx->J0;
+    int64_t n = 0;
+    int st = mrlbm_level_count(ctx, level, &n);
+    if (st != MRLBM_OK)
+        return st;
+    if (n == 0)
+        return MRLBM_OK;
+    if (idx)
+    {
+        std::vector<int32_t> lins(n);
+        CU(cudaMemcpyAsync(lins.data(), ctx->cells[ctx->cur][li], sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        const int ny = ctx->geo.ny[li];
+        for (int64_t i = 0; i < n; ++i)
+        {
+            if (ctx->D == 1)
+                idx[i] = lins[i];
+            else
+            {
+                idx[2 * i] = lins[i] / ny;
+                idx[2 * i + 1] = lins[i] % ny;
+            }
+        }
+    }
+    if (f)
+    {
+        for (int h = 0; h < ctx->q; ++h)
+            CU(cudaMemcpyAsync(f + h * n, ctx->F[0][li] + h * ctx->geo.cap[li], sizeof(double) * n,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return MRLBM_OK;
+}
+
+int mrlbm_set_profiling(mrlbm_ctx* ctx, int on)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    ctx->profiling = on != 0;
+    return MRLBM_OK;
+}
+
+int mrlbm_set_graph(mrlbm_ctx* ctx, int on)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    ctx->use_graph = on != 0;
+    return MRLBM_OK;
+}
+
+void* mrlbm_stream_handle(mrlbm_ctx* ctx)
+{
+    return ctx ? static_cast<void*>(ctx->stream) : nullptr;
+}
+
+int mrlbm_synchronize(mrlbm_ctx* ctx)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MRLBM_OK;
+}
+
+const char* mrlbm_last_error(const mrlbm_ctx* ctx)
+{
+    return ctx ? ctx->err_msg.c_str() : "null context";
+}
+
+void mrlbm_destroy(mrlbm_ctx* ctx)
+{
+    if (!ctx)
+        return;
+    if (ctx->stream)
+        cudaStreamSynchronize(ctx->stream);
+    for (auto& gph : ctx->graph)
+        if (gph)
+            cudaGraphExecDestroy(gph);
+    for (int v = 0; v < 2; ++v)
+    {
+        cudaFree(ctx->cnt[v]);
+        for (int li = 0; li < kL; ++li)
+        {
+            cudaFree(ctx->map[v][li]);
+            cudaFree(ctx->cells[v][li]);
+            cudaFree(ctx->F[v][li]);
+        }
+    }
+    for (int li = 0; li < kL; ++li)
+    {
+        cudaFree(ctx->kind[li]);
+        cudaFree(ctx->rn[li]);
+        cudaFree(ctx->keep[li]);
+        cudaFree(ctx->tiles[li]);
+    }
+    cudaFree(ctx->sch);
+    cudaFree(ctx->err);
+    cudaFree(ctx->fbc);
+    cudaFree(ctx->fbl);
+    cudaFree(ctx->upd);
+    cudaFree(ctx->tidx);
+    cudaFree(ctx->toff);
+    cudaFree(ctx->tw);
+    for (auto& e : ctx->ev)
+        if (e)
+            cudaEventDestroy(e);
+    if (ctx->stream)
+        cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+} // extern "C"

@@ -1,0 +1,99 @@
+"""Host-side mirror of the reference's solver interface for the hot path.
+
+`Solver` wraps one C-ABI context (one GPU stream, all levels resident in HBM):
+load a complete-leaf FieldSet in CellIndex order, run Algorithm-1 steps
+(adapt -> stream -> collide), read leaves back.  Errors raise like the
+reference's exceptions (ValueError ~ std::invalid_argument, FloatingPointError
+~ std::domain_error, RuntimeError otherwise).
+"""
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .abi import StepStats, PHASES, ERR_CONFIG, ERR_NUMERIC
+
+
+class MRLBMError(RuntimeError):
+    pass
+
+
+def _raise(status, msg):
+    if status == ERR_CONFIG:
+        raise ValueError(msg)
+    if status == ERR_NUMERIC:
+        raise FloatingPointError(msg)
+    raise MRLBMError(f"status {status}: {msg}")
+
+
+class Solver:
+    def __init__(self, scheme, cfg):
+        self.L = _lib.lib()
+        self.scheme, self.cfg = scheme, cfg
+        self.d, self.q = scheme.d, scheme.q
+        h = C.c_void_p()
+        st = self.L.mrlbm_create(C.byref(scheme), C.byref(cfg), C.byref(h))
+        if st != 0:
+            _raise(st, "mrlbm_create failed (invalid configuration or no CUDA device)")
+        self.h = h
+
+    def _check(self, st):
+        if st != 0:
+            _raise(st, self.L.mrlbm_last_error(self.h).decode())
+
+    def load_leaves(self, level, idx, f):
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        n = idx.shape[0]
+        assert f.shape == (self.q, n)
+        self._check(self.L.mrlbm_load_leaves(self.h, int(level), n, idx.ctypes.data_as(C.c_void_p),
+                                             f.ctypes.data_as(C.c_void_p)))
+
+    def commit(self):
+        self._check(self.L.mrlbm_commit(self.h))
+
+    def step(self, n=1):
+        stats = StepStats()
+        self._check(self.L.mrlbm_step(self.h, int(n), C.byref(stats)))
+        return stats
+
+    def level_count(self, level):
+        n = C.c_int64(0)
+        self._check(self.L.mrlbm_level_count(self.h, int(level), C.byref(n)))
+        return n.value
+
+    def read_leaves(self, level):
+        n = self.level_count(level)
+        idx = np.zeros((n, self.d), dtype=np.int32)
+        f = np.zeros((self.q, n), dtype=np.float64)
+        if n:
+            self._check(self.L.mrlbm_read_leaves(self.h, int(level), idx.ctypes.data_as(C.c_void_p),
+                                                 f.ctypes.data_as(C.c_void_p)))
+        return idx, f
+
+    def set_profiling(self, on=True):
+        self._check(self.L.mrlbm_set_profiling(self.h, int(bool(on))))
+
+    def set_graph(self, on=True):
+        self._check(self.L.mrlbm_set_graph(self.h, int(bool(on))))
+
+    def stream_handle(self):
+        return self.L.mrlbm_stream_handle(self.h)
+
+    def synchronize(self):
+        self._check(self.L.mrlbm_synchronize(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.mrlbm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def phase_dict(stats):
+        return {p: stats.ms_phase[i] for i, p in enumerate(PHASES)}

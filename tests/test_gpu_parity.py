@@ -1,0 +1,37 @@
+"""GPU parity: the CUDA step vs the CPU oracle, step by step, through the C-ABI.
+
+Integer state (leaf sets per level) must be identical; fields within 1e-12
+relative per step (north_star) -- in practice they are bit-identical because
+both sides use the reference operation order without FMA.
+"""
+import numpy as np
+import pytest
+
+from parity_util import make_pair, compare
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (config, J_bar, epsilon override, steps)
+    (1, 7, -1.0, 40),
+    (2, 8, -1.0, 40),
+    (3, 6, -1.0, 30),
+    (3, 5, 0.0, 20),     # uniform-mesh mode (epsilon = 0)
+    (4, 6, -1.0, 20),
+    (5, 6, -1.0, 20),
+]
+
+
+@pytest.mark.parametrize("cid,J,eps,steps", CASES)
+def test_step_parity(cid, J, eps, steps):
+    sc, rc, gpu, ora = make_pair(cid, J, eps)
+    worst = 0.0
+    for k in range(steps):
+        gpu.step(1)
+        ora.step(1)
+        rel, bitwise, total = compare(gpu, ora, rc, f"config {cid} step {k}")
+        assert rel <= 1e-12, f"config {cid} step {k}: rel diff {rel}"
+        worst = max(worst, rel)
+    gpu.close()
+    ora.close()
+    print(f"config {cid} J={J} eps={eps}: {steps} steps, worst rel {worst:.3e}")
