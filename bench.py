@@ -1,0 +1,309 @@
+#!/usr/bin/env python3
+"""Benchmark of the adaptive MR-LBM time step (BASELINE.json metric: leaf-cell
+updates/s for the full step incl. adaptation; HBM GB/s vs peak).
+
+Workload (config.workload): BASELINE configs[4], D2Q9 Navier-Stokes past a
+cylinder, levels 2..12 (finest 8192 x 4096), epsilon = 1e-4, from its seeded
+initial datum.  A "step" is one Algorithm-1 iteration (adapt -> transfer ->
+stream -> collide -> obstacle) over the whole adaptive mesh.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
+
+--impl reference times the CPU restatement of the reference path (the oracle;
+the reference ships no step of its own) on the host cores.
+Multi-GPU: the path does not shard in this tier (replicas only);
+every rank runs an independent replica, value = total updates / max time.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_ID = 5
+METRIC = "MR-LBM leaf-cell updates/s (full step incl. adaptation)"
+UNIT = "leaf-updates/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9]
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows)
+        smax = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+def snapshot(s, rc):
+    out = {}
+    for lv in range(rc.j_min, rc.j_max + 1):
+        out[lv] = s.read_leaves(lv)
+    return out
+
+
+def run_cpu_sample(steps=2, jmax=9, threads=None):
+    """CPU oracle (the reference path restated on the reference headers) on a
+    bounded sample: config 5 at J_bar = jmax from its initial datum."""
+    from oracle import pyoracle
+    from paper_2103_02903_b200 import build_config, finest_cells, initial_finest
+    cores = threads or os.cpu_count() or 1
+    pyoracle.set_threads(cores)
+    sc, rc = build_config(CONFIG_ID, jmax)
+    o = pyoracle.Oracle(sc, rc)
+    o.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
+    o.commit()
+    upd, secs = 0, 0.0
+    for _ in range(steps):
+        t = time.perf_counter()
+        o.step(1)
+        secs += time.perf_counter() - t
+        upd += sum(o.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1))
+    o.close()
+    return {"value": upd / secs, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"config 5 (D2Q9 cylinder) at J_bar={jmax} ({(8 << (jmax - 2)) * (4 << (jmax - 2))} finest cells), "
+                      f"{steps} oracle steps from the initial datum, {cores} threads, {secs:.2f} s"}
+
+
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    # each step: one oracle step of the bounded sample (config 5 at J_bar = 9)
+    from oracle import pyoracle
+    from paper_2103_02903_b200 import build_config, finest_cells, initial_finest
+    cores = os.cpu_count() or 1
+    pyoracle.set_threads(cores)
+    jmax = 9
+    sc, rc = build_config(CONFIG_ID, jmax)
+    o = pyoracle.Oracle(sc, rc)
+    o.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
+    o.commit()
+    for _ in range(args.warmup):
+        o.step(1)
+    upd, secs = 0, 0.0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        o.step(1)
+        secs += time.perf_counter() - t
+        upd += sum(o.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1))
+    v = upd / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (config 5 initial datum, seeded perturbation)",
+        "config": {"workload": f"config 5 D2Q9 cylinder, levels 2..{jmax} (bounded CPU sample of levels 2..12)",
+                   "epsilon": rc.epsilon},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"config 5 at J_bar={jmax}, {args.steps} timed oracle steps after {args.warmup} warm-up"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def bench_product(args):
+    import numpy as np
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
+    from paper_2103_02903_b200.abi import PHASES
+
+    sc, rc = build_config(CONFIG_ID, args.jmax)
+    idx0, f0 = finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc)
+    s = Solver(sc, rc)
+    s.load_leaves(rc.j_max, idx0, f0)
+    s.commit()
+    stream = torch.cuda.ExternalStream(s.stream_handle(), device=dev)
+    # warm-up (also evolves the state into the measured regime)
+    st = s.step(args.warmup)
+    # state snapshot for the e2e leg (same K steps, through host buffers)
+    snap = snapshot(s, rc)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed region: K steps, L2 flushed between steps (outside the events)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    u0 = st.leaf_updates
+    barrier()
+    launches = 0
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+            evs[k][0].record(stream)
+            st = s.step(1)
+            evs[k][1].record(stream)
+            launches += st.kernel_launches
+    barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    updates = st.leaf_updates - u0
+    clocks = clk.summary()
+    tmax = torch.tensor([ms], device=dev, dtype=torch.float64)
+    utot = torch.tensor([float(updates)], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(utot, op=torch.distributed.ReduceOp.SUM)
+    ms_max = float(tmax.item())
+    value = float(utot.item()) / (ms_max / 1e3)
+    state_bytes = 8 * sc.q * sum(int(st.leaves[i]) for i in range(st.levels))
+
+    # ---- phase breakdown (profiling pass: eager launches + events per phase), continues the run
+    s.set_profiling(True)
+    sp = s.step(max(1, min(args.steps, 3)))
+    s.set_profiling(False)
+    nprof = max(1, min(args.steps, 3))
+    phase_ms = {p: sp.ms_phase[i] / nprof for i, p in enumerate(PHASES)}
+    dom = max(phase_ms, key=phase_ms.get)
+    peak, peak_kind = load_peaks()
+    stream_bytes = sp.bytes_stream
+    achieved = stream_bytes / (phase_ms["stream"] / 1e3) / 1e9 if phase_ms["stream"] > 0 else 0.0
+    step_ms_prof = sum(phase_ms.values())
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_stream_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("bytes_per_step")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the C-ABI with host buffers: load snapshot -> commit -> K steps -> read back
+    s2 = Solver(sc, rc)
+    h2d = sum(v[0].nbytes + v[1].nbytes for v in snap.values())
+    barrier()
+    t0 = time.perf_counter()
+    for lv, (ix, ff) in snap.items():
+        s2.load_leaves(lv, ix, ff)
+    s2.commit()
+    st2 = s2.step(args.steps)
+    out = snapshot(s2, rc)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    d2h = sum(v[0].nbytes + v[1].nbytes for v in out.values())
+    e2e_val = st2.leaf_updates / e2e_s
+    et = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    eu = torch.tensor([float(st2.leaf_updates)], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(eu, op=torch.distributed.ReduceOp.SUM)
+        e2e_val = float(eu.item()) / float(et.item())
+    s2.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = run_cpu_sample(steps=2, jmax=9)
+
+    if rank == 0:
+        leaves_last = [int(st.leaves[i]) for i in range(st.levels)]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (config 5 initial datum: rest + seeded 1e-3 transverse perturbation)",
+            "config": {"workload": "config 5: D2Q9 Navier-Stokes past a cylinder, levels 2..%d (finest %dx%d), "
+                                   "eps=1e-4, Re=1200" % (rc.j_max, 8 << (rc.j_max - 2), 4 << (rc.j_max - 2)),
+                       "parallelism": "replicas" if world > 1 else "single-gpu",
+                       "l2": f"flushed between timed steps (256 MiB write); state {state_bytes / 1e6:.0f} MB",
+                       "leaves_per_level_last_step": leaves_last,
+                       "fallback_leaves_last_step": int(st.fallback_leaves)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "stream+collide phase (K7/K8, one launch per level) per step",
+                         "algorithmic_bytes": stream_bytes, "peak_kind": peak_kind},
+            "step_roofline": {"bytes_model_per_step": sp.bytes_model,
+                              "achieved_gbs": sp.bytes_model / (ms_max / args.steps / 1e3) / 1e9,
+                              "frac": sp.bytes_model / (ms_max / args.steps / 1e3) / 1e9 / peak},
+            "phases_ms": phase_ms, "dominant_phase": dom,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": d2h // args.steps},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    s.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--jmax", type=int, default=0, help="override J_bar (default: config value 12)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_product(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -109,7 +109,9 @@ typedef struct mrlbm_step_stats {
     int64_t leaf_updates;                  /* sum over steps of |S(Lambda(t+dt))| */
     double ms_total;                       /* device time of the steps (CUDA events) */
     double ms_phase[8];                    /* see MRLBM_PHASE_* (only when profiling on) */
-    int64_t bytes_model;                   /* algorithmic fp64 bytes (SURVEY 8d model) */
+    int64_t bytes_model;                   /* algorithmic fp64 bytes of the last step (SURVEY 8d model) */
+    int64_t bytes_stream;                  /* algorithmic bytes of the last step's stream+collide phase */
+    int64_t kernel_launches;               /* CUDA kernels this call launched (graph nodes included) */
 } mrlbm_step_stats;
 
 enum {

@@ -55,6 +55,8 @@ class StepStats(C.Structure):
         ("ms_total", C.c_double),
         ("ms_phase", C.c_double * 8),
         ("bytes_model", C.c_int64),
+        ("bytes_stream", C.c_int64),
+        ("kernel_launches", C.c_int64),
     ]
 
 

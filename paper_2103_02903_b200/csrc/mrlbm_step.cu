@@ -1209,6 +1209,8 @@ struct mrlbm_ctx {
     double phase_ms[MRLBM_PHASE_COUNT]{};
     std::string err_msg;
     int grid_cap = 148 * 8;
+    long long kernels_per_step = 0; // counted while enqueueing one step
+    long long kcount = 0;
 };
 
 namespace {
@@ -1287,6 +1289,7 @@ int grid_for(mrlbm_ctx* c, long long n, int threads = 256)
 template <int D>
 void launch_compaction(mrlbm_ctx* c, int v, int m)
 {
+    c->kcount += 3;
     const int li = m - c->J0;
     const long long n = c->geo.cap[li];
     const int nt = static_cast<int>(c->ntiles[li]);
@@ -1313,6 +1316,7 @@ void enqueue_step(mrlbm_ctx* c)
     Aux aux = aux_of(c);
     cudaStream_t s = c->stream;
     const int T = 256;
+    c->kcount = 0;
     for (int li = 0; li < c->nlev; ++li)
     {
         cudaMemsetAsync(c->keep[li], 0, g.cap[li], s);
@@ -1322,44 +1326,45 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 0);
     // K1 projection of the old tree (bottom-up)
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux);
+        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux); }
     phase_mark(c, 1);
     // K2 details + flags
     for (int m = c->J0; m < c->J1; ++m)
-        k_details<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux);
+        { c->kcount++; k_details<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux); }
     phase_mark(c, 2);
     // K3 closure, enlargement, grading
     for (int m = c->J1 - 1; m > c->J0; --m)
-        k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);
+        { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m); }
     for (int m = c->J0; m < c->J1; ++m)
-        k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m);
+        { c->kcount++; k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m); }
     for (int m = c->J1 - 1; m > c->J0; --m)
-        k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+        { c->kcount++; k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m); }
     phase_mark(c, 3);
     // K4 kinds, fallback flags, reconstruction bands, ghosts, compaction
     for (int m = c->J0; m <= c->J1; ++m)
-        k_kinds<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+        { c->kcount++; k_kinds<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m); }
     for (int m = c->J0; m <= c->J1; ++m)
-        k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux);
-    k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);
+        { c->kcount++; k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux); }
+    { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux); }
     for (int m = c->J0; m <= c->J1; ++m)
-        k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+        { c->kcount++; k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m); }
     for (int m = c->J0; m <= c->J1; ++m)
         launch_compaction<D>(c, n, m);
     phase_mark(c, 4);
     // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
     for (int m = c->J0; m <= c->J1; ++m)
-        k_transfer<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux);
+        { c->kcount++; k_transfer<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux); }
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);
+        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux); }
     for (int m = c->J0 + 1; m <= c->J1; ++m)
-        k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);
+        { c->kcount++; k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux); }
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
     for (int m = c->J0; m <= c->J1; ++m)
-        k_stream_collide<D, Q><<<grid_for(c, g.cap[m - c->J0], 128), 128, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux);
-    k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);
+        { c->kcount++; k_stream_collide<D, Q><<<grid_for(c, g.cap[m - c->J0], 128), 128, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux); }
+    { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd); }
     phase_mark(c, 6);
+    c->kernels_per_step = c->kcount;
 }
 
 using StepFn = void (*)(mrlbm_ctx*);
@@ -1770,6 +1775,8 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
             nG += counts[li * 4 + 2];
         }
         stats->fallback_leaves = fb[0] + fb[1];
+        stats->kernel_launches = ctx->kernels_per_step * nsteps;
+        stats->bytes_stream = 8LL * ctx->q * (2 * nS + nG);
         stats->leaf_updates = upd;
         // SURVEY 8d compulsory fp64 model with N_old ~ N_new (last step's counts)
         stats->bytes_model = 8LL * ctx->q * (2 * nS + 3 * nI + 5 * nS + nI + 2 * nG);

@@ -35,3 +35,17 @@ def test_step_parity(cid, J, eps, steps):
     gpu.close()
     ora.close()
     print(f"config {cid} J={J} eps={eps}: {steps} steps, worst rel {worst:.3e}")
+
+
+def test_config2_blowup_same_step():
+    """Both sides report the non-finite state (status 3) at the same step."""
+    sc, rc, gpu, ora = make_pair(2, 8)
+    def first_fail(s):
+        for k in range(120):
+            try:
+                s.step(1)
+            except FloatingPointError:
+                return k
+        return None
+    kg, ko = first_fail(gpu), first_fail(ora)
+    assert kg is not None and kg == ko
