@@ -148,6 +148,12 @@ void mrlbm_destroy(mrlbm_ctx* ctx);
 int mrlbm_stream_table(int d, int gap, const int32_t eta[3], int side, int cap,
                        int32_t* offsets, double* weights, int* n);
 
+/* Exactness sets of that table (Decision D.13): dep_box = {xlo, xhi, ylo, yhi} of
+   the level-l cells the zero-detail recursion touches (must lie in the domain),
+   par_offsets = parents of the level-(l+1) cells it touches (must not be internal). */
+int mrlbm_stream_table_sets(int d, int gap, const int32_t eta[3], int side, int cap, int32_t* dep_box,
+                            int32_t* par_offsets, int* npar);
+
 /* Host-side builders for the five BASELINE configurations (Decisions).
    config_id 1..5 (config 3 with epsilon override 0 = the uniform run).
    j_max_override > 0 replaces J_bar (parity tests run reduced sizes);

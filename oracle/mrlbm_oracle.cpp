@@ -167,6 +167,12 @@ struct TableBuilder {
         return memo.emplace(key, std::move(out)).first->second;
     }
 
+    // Exactness conditions of a table (Decision D.13): every level-l cell the
+    // recursion touches must lie inside the domain (dep) and no cell it touches at
+    // level l+1 may belong to the complete tree, i.e. their parents (par) must not
+    // be internal.  Filled by build().
+    std::vector<std::array<int, D>> last_dep, last_par;
+
     // side 0 = E = (B - eta) \ B, side 1 = A = B \ (B - eta)
     std::vector<std::pair<std::array<int, D>, double>> build(int g, const int32_t* eta, int side)
     {
@@ -213,6 +219,41 @@ struct TableBuilder {
             const Form& f = rec(g, c, memo);
             for (const auto& [k, v] : f)
                 total[k] += v;
+        }
+        last_dep.clear();
+        last_par.clear();
+        std::map<std::array<I64, D>, int> par;
+        for (const auto& [key, form] : memo)
+        {
+            if (key.first == 0)
+            {
+                std::array<int, D> o{};
+                for (int i = 0; i < D; ++i)
+                    o[i] = static_cast<int>(key.second[i]);
+                last_dep.push_back(o);
+            }
+            else if (key.first == 1)
+            {
+                std::array<I64, D> pp{};
+                for (int i = 0; i < D; ++i)
+                    pp[i] = key.second[i] >> 1;
+                par[pp] = 1;
+            }
+        }
+        if (g == 0)
+            for (const auto& c : cells)
+            {
+                std::array<int, D> o{};
+                for (int i = 0; i < D; ++i)
+                    o[i] = static_cast<int>(c[i]);
+                last_dep.push_back(o);
+            }
+        for (const auto& [pp, one] : par)
+        {
+            std::array<int, D> o{};
+            for (int i = 0; i < D; ++i)
+                o[i] = static_cast<int>(pp[i]);
+            last_par.push_back(o);
         }
         std::vector<std::pair<std::array<int, D>, double>> out;
         for (const auto& [k, v] : total)
@@ -346,8 +387,9 @@ class Oracle {
     std::vector<std::vector<std::pair<Idx, std::vector<double>>>> staged;
     bool committed = false;
     int opp[MRLBM_MAX_Q]{};
-    // tables [gap][h][side] -> (offsets, weights)
+    // tables [gap][h][side] -> (offsets, weights), and their exactness sets
     std::vector<std::vector<std::array<std::vector<std::pair<std::array<int, D>, double>>, 2>>> tables;
+    std::vector<std::vector<std::array<std::vector<std::array<int, D>>, 2>>> tdep, tpar;
     std::int64_t fallback_last = 0;
     std::int64_t leaf_updates = 0;
     std::string err;
@@ -409,12 +451,20 @@ class Oracle {
         staged.resize(J1 - J0 + 1);
         TableBuilder<D> tb;
         tables.resize(J1 - J0 + 1);
+        tdep.resize(J1 - J0 + 1);
+        tpar.resize(J1 - J0 + 1);
         for (int g = 0; g <= J1 - J0; ++g)
         {
             tables[g].resize(q);
+            tdep[g].resize(q);
+            tpar[g].resize(q);
             for (int h = 0; h < q; ++h)
                 for (int side = 0; side < 2; ++side)
+                {
                     tables[g][h][side] = tb.build(g, sc.eta[h], side);
+                    tdep[g][h][side] = tb.last_dep;
+                    tpar[g][h][side] = tb.last_par;
+                }
         }
     }
 
@@ -979,63 +1029,60 @@ class Oracle {
                     oe.run([&] {
                     const Idx& k = cells[i];
                     const double* fstar = &L.lf[*L.li.slot(k) * q];
-                    // table validity (Decision D.13): 5^D box inside (or periodic)
-                    // and free of internal cells
-                    bool fallback = false;
-                    const int nb = (D == 1 ? 5 : 25);
-                    std::array<const double*, 25> bx{};
-                    for (int o = 0; o < nb && !fallback; ++o)
-                    {
-                        Idx c = k;
-                        if (D == 1)
-                            c[0] += o - 2;
-                        else
-                        {
-                            c[0] += o / 5 - 2;
-                            c[1] += o % 5 - 2;
-                        }
-                        if (!inside_or_periodic(l, c))
-                        {
-                            fallback = true;
-                            break;
-                        }
-                        c = wrapclamp(l, c);
-                        if (L.ii.slot(c))
-                        {
-                            fallback = true;
-                            break;
-                        }
-                        bx[o] = rec(l, c, memo);
-                    }
-                    fb[i] = fallback;
-                    nfb += fallback ? 1 : 0;
+                    bool any_fb = false;
                     for (int h = 0; h < q; ++h)
                     {
-                        double sE = 0.0, sA = 0.0;
-                        if (!fallback)
+                        double sums[2] = {0.0, 0.0};
+                        for (int side = 0; side < 2; ++side)
                         {
-                            for (int side = 0; side < 2; ++side)
+                            // table exactness (Decision D.13): dependency cells inside
+                            // (or periodic), parents of the level-(l+1) funnel not internal
+                            bool ok = true;
+                            for (const auto& o : tdep[g][h][side])
                             {
-                                double s = 0.0;
+                                Idx c = k;
+                                for (int a = 0; a < D; ++a)
+                                    c[a] += o[a];
+                                if (!inside_or_periodic(l, c))
+                                {
+                                    ok = false;
+                                    break;
+                                }
+                            }
+                            for (const auto& o : tpar[g][h][side])
+                            {
+                                if (!ok)
+                                    break;
+                                Idx c = k;
+                                for (int a = 0; a < D; ++a)
+                                    c[a] += o[a];
+                                if (L.ii.slot(wrapclamp(l, c)))
+                                    ok = false;
+                            }
+                            double s = 0.0;
+                            if (ok)
+                            {
                                 for (const auto& [off, w] : tables[g][h][side])
                                 {
-                                    const int o = (D == 1) ? off[0] + 2 : (off[0] + 2) * 5 + off[1] + 2;
-                                    s += w * bx[o][h];
+                                    Idx c = k;
+                                    for (int a = 0; a < D; ++a)
+                                        c[a] += off[a];
+                                    s += w * rec(l, wrapclamp(l, c), memo)[h];
                                 }
-                                (side == 0 ? sE : sA) = s;
                             }
+                            else
+                            {
+                                any_fb = true;
+                                rim_cells(l, k, sc.eta[h], side, rim);
+                                for (const auto& x : rim)
+                                    s += side == 0 ? rim_value(x, h, fstar, nfine, memo) : rec(J1, x, memo)[h];
+                            }
+                            sums[side] = s;
                         }
-                        else
-                        {
-                            rim_cells(l, k, sc.eta[h], 0, rim);
-                            for (const auto& x : rim)
-                                sE += rim_value(x, h, fstar, nfine, memo);
-                            rim_cells(l, k, sc.eta[h], 1, rim);
-                            for (const auto& x : rim)
-                                sA += rec(J1, x, memo)[h];
-                        }
-                        f[h] = fstar[h] + scale * (sE - sA);
+                        f[h] = fstar[h] + scale * (sums[0] - sums[1]);
                     }
+                    fb[i] = any_fb;
+                    nfb += any_fb ? 1 : 0;
                     // collide (Decision D.24)
                     M.multiply(f.data(), mm.data());
                     equilibrium(sc, mm.data(), meq.data());
@@ -1329,6 +1376,41 @@ int oracle_stream_table(int d, int gap, const int32_t eta[3], int side, int cap,
             *n = static_cast<int>(t.size());
         }
         return MRLBM_OK;
+    }
+    catch (...)
+    {
+        return MRLBM_ERR_NUMERIC;
+    }
+}
+
+int oracle_stream_table_sets(int d, int gap, const int32_t eta[3], int side, int cap, int32_t* dep, int* ndep,
+                             int32_t* par, int* npar)
+{
+    try
+    {
+        auto emit = [&](const auto& tb)
+        {
+            if (static_cast<int>(tb.last_dep.size()) > cap || static_cast<int>(tb.last_par.size()) > cap)
+                return MRLBM_ERR_CAPACITY;
+            for (std::size_t i = 0; i < tb.last_dep.size(); ++i)
+                for (int a = 0; a < d; ++a)
+                    dep[i * d + a] = tb.last_dep[i][a];
+            for (std::size_t i = 0; i < tb.last_par.size(); ++i)
+                for (int a = 0; a < d; ++a)
+                    par[i * d + a] = tb.last_par[i][a];
+            *ndep = static_cast<int>(tb.last_dep.size());
+            *npar = static_cast<int>(tb.last_par.size());
+            return MRLBM_OK;
+        };
+        if (d == 1)
+        {
+            TableBuilder<1> tb;
+            tb.build(gap, eta, side);
+            return emit(tb);
+        }
+        TableBuilder<2> tb;
+        tb.build(gap, eta, side);
+        return emit(tb);
     }
     catch (...)
     {

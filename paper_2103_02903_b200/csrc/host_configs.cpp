@@ -105,7 +105,7 @@ static void prediction_numerators(int d, int delta_code, long long* W)
 // Push formulation: start from the indicator of the E (side 0) or A (side 1)
 // finest cells of a leaf at gap g and push weights down one level at a time
 // through the adjoint of the prediction operator.
-int build_stream_table(int d, int g, const int32_t* eta, int side, std::vector<TableEntry>& out)
+int build_stream_table(int d, int g, const int32_t* eta, int side, std::vector<TableEntry>& out, TableSets* sets)
 {
     out.clear();
     if (d < 1 || d > 2 || g < 0 || g > 14)
@@ -127,6 +127,43 @@ int build_stream_table(int d, int g, const int32_t* eta, int side, std::vector<T
     long long W[4][9];
     for (int s = 0; s < (1 << d); ++s)
         prediction_numerators(d, s, W[s]);
+    if (sets)
+    {
+        // support propagation without cancellation: every cell the recursion touches
+        std::map<std::pair<long long, long long>, int> touched;
+        for (const auto& kv : cur)
+            touched[kv.first] = 1;
+        std::map<std::pair<long long, long long>, int> par;
+        for (int lvl = g; lvl > 0; --lvl)
+        {
+            std::map<std::pair<long long, long long>, int> nxt;
+            for (const auto& kv : touched)
+            {
+                const long long px = kv.first.first >> 1, py = (d == 2) ? (kv.first.second >> 1) : 0;
+                if (lvl == 1)
+                    par[{px, py}] = 1; // parent (level l) of a touched level-(l+1) cell
+                for (int ox = -1; ox <= 1; ++ox)
+                    for (int oy = (d == 2 ? -1 : 0); oy <= (d == 2 ? 1 : 0); ++oy)
+                        nxt[{px + ox, py + oy}] = 1;
+            }
+            touched.swap(nxt);
+        }
+        sets->dep_lo[0] = sets->dep_lo[1] = 1 << 30;
+        sets->dep_hi[0] = sets->dep_hi[1] = -(1 << 30);
+        for (const auto& kv : touched)
+        {
+            const int x = static_cast<int>(kv.first.first), y = static_cast<int>(kv.first.second);
+            sets->dep_lo[0] = std::min(sets->dep_lo[0], x);
+            sets->dep_hi[0] = std::max(sets->dep_hi[0], x);
+            sets->dep_lo[1] = std::min(sets->dep_lo[1], y);
+            sets->dep_hi[1] = std::max(sets->dep_hi[1], y);
+        }
+        if (touched.empty())
+            sets->dep_lo[0] = sets->dep_lo[1] = sets->dep_hi[0] = sets->dep_hi[1] = 0;
+        sets->par.clear();
+        for (const auto& kv : par)
+            sets->par.emplace_back(static_cast<int>(kv.first.first), static_cast<int>(kv.first.second));
+    }
     for (int lvl = g; lvl > 0; --lvl)
     {
         std::map<std::pair<long long, long long>, I128> nxt;
@@ -301,6 +338,30 @@ static void host_feq(const mrlbm_scheme_spec* sc, const double* cons, double* f)
             acc += sc->Minv[i * q + j] * meq[j];
         f[i] = acc;
     }
+}
+
+int mrlbm_stream_table_sets(int d, int gap, const int32_t eta[3], int side, int cap, int32_t* dep_box,
+                            int32_t* par_offsets, int* npar)
+{
+    std::vector<TableEntry> t;
+    TableSets ts{};
+    const int st = build_stream_table(d, gap, eta, side, t, &ts);
+    if (st != MRLBM_OK)
+        return st;
+    if (static_cast<int>(ts.par.size()) > cap)
+        return MRLBM_ERR_CAPACITY;
+    dep_box[0] = ts.dep_lo[0];
+    dep_box[1] = ts.dep_hi[0];
+    dep_box[2] = ts.dep_lo[1];
+    dep_box[3] = ts.dep_hi[1];
+    for (size_t i = 0; i < ts.par.size(); ++i)
+    {
+        par_offsets[i * d] = ts.par[i].first;
+        if (d == 2)
+            par_offsets[i * d + 1] = ts.par[i].second;
+    }
+    *npar = static_cast<int>(ts.par.size());
+    return MRLBM_OK;
 }
 
 int mrlbm_build_config(int id, int jmax_override, double eps_override, mrlbm_scheme_spec* sc, mrlbm_run_config* rc)

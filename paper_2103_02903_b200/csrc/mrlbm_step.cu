@@ -26,6 +26,7 @@
 #include <climits>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace mrlbm_b200 {
@@ -72,11 +73,21 @@ struct Aux {
     int* err;          // [0] unresolved stencil, [1] non-finite, [2] inconsistency
     int* fb_count;     // fallback leaves of the current step
     int2* fb_list;     // (level, lin)
+    unsigned* fb_mask; // per fallback leaf: bit (2h + side) set = table not exact
     long long fb_cap;
     long long* updates; // accumulated leaf updates
     const int2* tidx;   // [(g * q + h) * 2 + side] -> (start, count)
     const int2* toff;
     const double* tw;
+    const int4* tdep;   // [(g * q + h) * 2 + side] -> dependency box (xlo, xhi, ylo, yhi)
+    const int2* tpidx;  // [(g * q + h) * 2 + side] -> (start, count) into tpar
+    const int2* tpar;   // parents of the level-(l+1) funnel
+    const int2* guidx;  // [g] -> (start, count) into guoff: distinct table offsets of the gap
+    const int2* guoff;
+    const uint8_t* tu;  // per table entry: index into its gap's distinct offsets
+    const int4* udep;   // [g] union of the dependency boxes
+    const int2* upidx;  // [g] -> (start, count) into upar
+    const int2* upar;   // [g] union of the parent sets
 };
 
 // ---------------------------------------------------------------- helpers
@@ -373,68 +384,142 @@ __global__ void k_kinds(Geo g, Flags fl, int m)
     }
 }
 
-// table validity (Decision D.13): the 5^D box of a leaf is inside (or periodic)
-// and holds no internal cell; else the leaf streams by the recursive path
+// Table exactness (Decision D.13), per (population, side): the level-l cells the
+// zero-detail recursion touches lie in the domain (or periodic) and the parents of
+// the level-(l+1) cells it touches are not internal.  A leaf is a fallback leaf if
+// any pair fails: tested here on the union over pairs (equivalent for "any").
 template <int D>
 __global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
 {
     const int li = m - g.J0;
+    const int gap = g.J1 - m;
     const int nx = g.nx[li], ny = g.ny[li];
     const long long n = (long long)nx * ny;
+    const int4 ub = aux.udep[gap];
+    const int2 pi = aux.upidx[gap];
     GRID_STRIDE(i, 0, n)
     {
         if (fl.kind[li][i] != K_LEAF)
             continue;
         int x, y;
         lin2xy<D>((int)i, ny, x, y);
-        bool fb = false;
-        for (int ox = -2; ox <= 2 && !fb; ++ox)
-            for (int oy = (D == 1 ? 0 : -2); oy <= (D == 1 ? 0 : 2) && !fb; ++oy)
+        bool fb = (!g.per0 && (x + ub.x < 0 || x + ub.y >= nx)) ||
+                  (D == 2 && !g.per1 && (y + ub.z < 0 || y + ub.w >= ny));
+        for (int e = pi.x; e < pi.x + pi.y && !fb; ++e)
+        {
+            const int2 o = aux.upar[e];
+            int xx = x + o.x, yy = y + o.y;
+            if (xx < 0 || xx >= nx || (D == 2 && (yy < 0 || yy >= ny)))
             {
-                int xx = x + ox, yy = y + oy;
-                if (!g.per0 && (xx < 0 || xx >= nx))
-                {
-                    fb = true;
-                    break;
-                }
-                if (D == 2 && !g.per1 && (yy < 0 || yy >= ny))
-                {
-                    fb = true;
-                    break;
-                }
+                if ((!g.per0 && (xx < 0 || xx >= nx)) || (D == 2 && !g.per1 && (yy < 0 || yy >= ny)))
+                    continue; // outside a non-periodic wall: covered by the domain test
                 xx = mr_coord(xx, nx, 1);
                 if (D == 2)
                     yy = mr_coord(yy, ny, 1);
-                if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
-                    fb = true;
             }
+            if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
+                fb = true;
+        }
         if (fb)
         {
-            fl.kind[li][i] = K_LEAF | K_FB;
-            if (m < g.J1)
+            // exact per-(population, side) mask of the pairs whose table is not exact
+            unsigned mask = 0;
+            for (int pair = 0; pair < 2 * g.q; ++pair)
             {
-                const int k = atomicAdd(aux.fb_count, 1);
-                if (k < aux.fb_cap)
-                    aux.fb_list[k] = make_int2(m, (int)i);
-                else
-                    flag_err(aux.err, 2);
+                const int key = gap * 2 * g.q + pair;
+                const int4 db = aux.tdep[key];
+                bool ok = !((!g.per0 && (x + db.x < 0 || x + db.y >= nx)) ||
+                            (D == 2 && !g.per1 && (y + db.z < 0 || y + db.w >= ny)));
+                const int2 pp = aux.tpidx[key];
+                for (int k = pp.x; k < pp.x + pp.y && ok; ++k)
+                {
+                    const int2 o = aux.tpar[k];
+                    if (fl.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)] & K_INT)
+                        ok = false;
+                }
+                if (!ok)
+                    mask |= 1u << pair;
+            }
+            fl.kind[li][i] = K_LEAF | K_FB;
+            const int k = atomicAdd(aux.fb_count, 1);
+            if (k < aux.fb_cap)
+            {
+                aux.fb_list[k] = make_int2(m, (int)i);
+                aux.fb_mask[k] = mask;
             }
             else
-                atomicAdd(aux.fb_count + 1, 1); // gap-0 fallback leaves need no band
+                flag_err(aux.err, 2);
         }
     }
 }
 
-// mark the reconstruction band (2 cells outside / inside the leaf boundary) at
-// every finer level as virtual (materialised zero-detail reconstruction)
+// Mark the reconstruction band of every fallback leaf at every finer level as
+// virtual (materialised zero-detail reconstruction): a ring of width W on both
+// sides of the leaf boundary, W = 2 below the finest level (stencils of the
+// level above) and W = 1 at the finest level (the E/A rims themselves).
+// One warp per fallback leaf.
 template <int D>
-__global__ void k_band(Geo g, Flags fl, Aux aux)
+__device__ __forceinline__ long long band_count(int side, int W)
 {
+    const long long S = side + 2 * W;
+    if (D == 1)
+        return side <= 2 * W ? S : 4 * W;
+    return side <= 2 * W ? S * S : S * S - (long long)(side - 2 * W) * (side - 2 * W);
+}
+
+template <int D>
+__device__ __forceinline__ void band_cell(long long t, int side, int W, int bx0, int by0, int& x, int& y)
+{
+    const int S = side + 2 * W;
+    y = 0;
+    if (D == 1)
+    {
+        if (side <= 2 * W)
+            x = bx0 - W + (int)t;
+        else
+            x = t < 2 * W ? bx0 - W + (int)t : bx0 + side - W + (int)(t - 2 * W);
+        return;
+    }
+    if (side <= 2 * W)
+    {
+        x = bx0 - W + (int)(t / S);
+        y = by0 - W + (int)(t % S);
+        return;
+    }
+    const long long top = 2LL * W * S;
+    const long long mid = (long long)(side - 2 * W) * 4 * W;
+    if (t < top)
+    {
+        x = bx0 - W + (int)(t / S);
+        y = by0 - W + (int)(t % S);
+    }
+    else if (t < top + mid)
+    {
+        const long long u = t - top;
+        x = bx0 + W + (int)(u / (4 * W));
+        const int c = (int)(u % (4 * W));
+        y = c < 2 * W ? by0 - W + c : by0 + side - W + (c - 2 * W);
+    }
+    else
+    {
+        const long long u = t - top - mid;
+        x = bx0 + side - W + (int)(u / S);
+        y = by0 - W + (int)(u % S);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_band(Geo g, Flags fl, Aux aux)
+{
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
     const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
-    for (int it = blockIdx.x; it < nfb; it += gridDim.x)
+    for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nfb; it += warps)
     {
         const int2 e = aux.fb_list[it];
         const int l = e.x;
+        if (l == g.J1)
+            continue;
         int kx, ky;
         lin2xy<D>(e.y, g.ny[l - g.J0], kx, ky);
         for (int m = l + 1; m <= g.J1; ++m)
@@ -442,50 +527,12 @@ __global__ void k_band(Geo g, Flags fl, Aux aux)
             const int li = m - g.J0;
             const int nx = g.nx[li], ny = g.ny[li];
             const int side = 1 << (m - l);
-            const int bx0 = kx * side, by0 = ky * side;
-            const int S = side + 4;
-            long long total;
-            if (D == 1)
-                total = side <= 4 ? S : 8;
-            else
-                total = side <= 4 ? (long long)S * S : (long long)S * S - (long long)(side - 4) * (side - 4);
-            for (long long t = threadIdx.x; t < total; t += blockDim.x)
+            const int W = m == g.J1 ? 1 : 2;
+            const long long total = band_count<D>(side, W);
+            for (long long t = lane; t < total; t += 32)
             {
-                int x, y = 0;
-                if (D == 1)
-                {
-                    if (side <= 4)
-                        x = bx0 - 2 + (int)t;
-                    else
-                        x = t < 4 ? bx0 - 2 + (int)t : bx0 + side - 2 + (int)(t - 4);
-                }
-                else if (side <= 4)
-                {
-                    x = bx0 - 2 + (int)(t / S);
-                    y = by0 - 2 + (int)(t % S);
-                }
-                else
-                {
-                    const long long top = 4LL * S;
-                    if (t < top)
-                    {
-                        x = bx0 - 2 + (int)(t / S);
-                        y = by0 - 2 + (int)(t % S);
-                    }
-                    else if (t < top + (long long)(side - 4) * 8)
-                    {
-                        const long long u = t - top;
-                        x = bx0 + 2 + (int)(u / 8);
-                        const int c = (int)(u % 8);
-                        y = c < 4 ? by0 - 2 + c : by0 + side - 2 + (c - 4);
-                    }
-                    else
-                    {
-                        const long long u = t - top - (long long)(side - 4) * 8;
-                        x = bx0 + side - 2 + (int)(u / S);
-                        y = by0 - 2 + (int)(u % S);
-                    }
-                }
+                int x, y;
+                band_cell<D>(t, side, W, kx * side, ky * side, x, y);
                 if (!g.per0 && (x < 0 || x >= nx))
                     continue;
                 if (D == 2 && !g.per1 && (y < 0 || y >= ny))
@@ -501,9 +548,38 @@ __global__ void k_band(Geo g, Flags fl, Aux aux)
     }
 }
 
-// ghost layer: cells not in R within Chebyshev distance 2 of an R cell
+// ghost layer: cells not in R within Chebyshev distance 2 of an R cell.
+// 2D: separable dilation, pass 1 ORs R-membership over y +-2 into tmp, pass 2
+// ORs tmp over x +-2 (10 byte reads per cell instead of 25).
 template <int D>
-__global__ void k_ghost(Geo g, Flags fl, int m)
+__global__ void k_ghost_rows(Geo g, Flags fl, int m, uint8_t* tmp)
+{
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li];
+    const long long n = (long long)nx * ny;
+    GRID_STRIDE(i, 0, n)
+    {
+        int x, y;
+        lin2xy<D>((int)i, ny, x, y);
+        uint8_t r = 0;
+#pragma unroll
+        for (int oy = -2; oy <= 2; ++oy)
+        {
+            int yy = y + oy;
+            if (yy < 0 || yy >= ny)
+            {
+                if (!g.per1)
+                    continue;
+                yy = mr_coord(yy, ny, 1);
+            }
+            r |= fl.kind[li][xy2lin<D>(x, yy, ny)];
+        }
+        tmp[i] = r & (K_LEAF | K_INT);
+    }
+}
+
+template <int D>
+__global__ void k_ghost(Geo g, Flags fl, int m, const uint8_t* tmp)
 {
     const int li = m - g.J0;
     const int nx = g.nx[li], ny = g.ny[li];
@@ -515,23 +591,21 @@ __global__ void k_ghost(Geo g, Flags fl, int m)
         int x, y;
         lin2xy<D>((int)i, ny, x, y);
         bool near = false;
-        for (int ox = -2; ox <= 2 && !near; ++ox)
-            for (int oy = (D == 1 ? 0 : -2); oy <= (D == 1 ? 0 : 2); ++oy)
+#pragma unroll
+        for (int ox = -2; ox <= 2; ++ox)
+        {
+            int xx = x + ox;
+            if (xx < 0 || xx >= nx)
             {
-                int xx = x + ox, yy = y + oy;
-                if (!g.per0 && (xx < 0 || xx >= nx))
-                    continue;
-                if (D == 2 && !g.per1 && (yy < 0 || yy >= ny))
+                if (!g.per0)
                     continue;
                 xx = mr_coord(xx, nx, 1);
-                if (D == 2)
-                    yy = mr_coord(yy, ny, 1);
-                if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & (K_LEAF | K_INT))
-                {
-                    near = true;
-                    break;
-                }
             }
+            if (D == 2)
+                near = near || tmp[xy2lin<D>(xx, y, ny)] != 0;
+            else
+                near = near || (fl.kind[li][xx] & (K_LEAF | K_INT)) != 0;
+        }
         if (near)
             fl.kind[li][i] = K_VIRT;
     }
@@ -547,15 +621,16 @@ __device__ __forceinline__ int cat_of(uint8_t k)
     return (k & K_LEAF) ? 0 : (k & K_INT) ? 1 : (k & K_VIRT) ? 2 : 3;
 }
 
-__global__ void k_tile_count(const uint8_t* kind, long long n, int* tile_counts)
+// tile = kCellsPerThread rounds of kTileThreads consecutive cells (coalesced)
+__global__ void __launch_bounds__(kTileThreads) k_tile_count(const uint8_t* kind, long long n, int* tile_counts)
 {
     __shared__ int red[3][kTileThreads / 32];
-    const long long tile = blockIdx.x;
-    const long long base = tile * kTile + (long long)threadIdx.x * kCellsPerThread;
+    const long long base = (long long)blockIdx.x * kTile + threadIdx.x;
     int c[3] = {0, 0, 0};
-    for (int j = 0; j < kCellsPerThread; ++j)
+#pragma unroll 4
+    for (int r = 0; r < kCellsPerThread; ++r)
     {
-        const long long i = base + j;
+        const long long i = base + (long long)r * kTileThreads;
         if (i < n)
         {
             const int ct = cat_of(kind[i]);
@@ -577,7 +652,7 @@ __global__ void k_tile_count(const uint8_t* kind, long long n, int* tile_counts)
         int v = 0;
         for (int w = 0; w < kTileThreads / 32; ++w)
             v += red[threadIdx.x][w];
-        tile_counts[tile * 3 + threadIdx.x] = v;
+        tile_counts[(long long)blockIdx.x * 3 + threadIdx.x] = v;
     }
 }
 
@@ -617,62 +692,55 @@ __global__ void k_tile_scan(int* tile_counts, int ntiles, int* cnt)
         }
 }
 
-__global__ void k_tile_scatter(const uint8_t* kind, long long n, const int* tile_offsets, const int* cnt,
-                               int32_t* map, int32_t* cells)
+// ballot + popc ranks inside each warp, warp totals scanned in shared memory,
+// running per-category offsets across the rounds -> lexicographic slots
+__global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* kind, long long n, const int* tile_offsets,
+                                                               const int* cnt, int32_t* map, int32_t* cells)
 {
-    __shared__ int wsum[3][kTileThreads / 32];
-    const long long tile = blockIdx.x;
-    const long long base = tile * kTile + (long long)threadIdx.x * kCellsPerThread;
-    uint8_t kv[kCellsPerThread];
-    int c[3] = {0, 0, 0};
-    for (int j = 0; j < kCellsPerThread; ++j)
-    {
-        const long long i = base + j;
-        kv[j] = i < n ? kind[i] : 0;
-        const int ct = cat_of(kv[j]);
-        if (ct < 3)
-            ++c[ct];
-    }
-    // block exclusive scan of per-thread counts (warp shuffles + warp totals)
+    constexpr int NW = kTileThreads / 32;
+    __shared__ int wcount[3][NW];
+    __shared__ int run[3];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int pre[3];
-    for (int k = 0; k < 3; ++k)
+    const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x < 3)
     {
-        int v = c[k];
-        for (int o = 1; o < 32; o <<= 1)
+        const int catbase = threadIdx.x == 0 ? 0 : threadIdx.x == 1 ? cnt[0] : cnt[0] + cnt[1];
+        run[threadIdx.x] = catbase + tile_offsets[(long long)blockIdx.x * 3 + threadIdx.x];
+    }
+    const long long base = (long long)blockIdx.x * kTile + threadIdx.x;
+    for (int r = 0; r < kCellsPerThread; ++r)
+    {
+        const long long i = base + (long long)r * kTileThreads;
+        const int ct = i < n ? cat_of(kind[i]) : 3;
+        unsigned mk[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
         {
-            const int u = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o)
-                v += u;
+            mk[k] = __ballot_sync(0xffffffffu, ct == k);
+            if (lane == 0)
+                wcount[k][wid] = __popc(mk[k]);
         }
-        pre[k] = v - c[k];
-        if (lane == 31)
-            wsum[k][wid] = v;
-    }
-    __syncthreads();
-    const int catbase[3] = {0, cnt[0], cnt[0] + cnt[1]};
-    int pos[3];
-    for (int k = 0; k < 3; ++k)
-    {
-        int wpre = 0;
-        for (int w = 0; w < wid; ++w)
-            wpre += wsum[k][w];
-        pos[k] = catbase[k] + tile_offsets[tile * 3 + k] + wpre + pre[k];
-    }
-    for (int j = 0; j < kCellsPerThread; ++j)
-    {
-        const long long i = base + j;
-        if (i >= n)
-            break;
-        const int ct = cat_of(kv[j]);
+        __syncthreads();
         if (ct < 3)
         {
-            const int sl = pos[ct]++;
+            int off = run[ct];
+            for (int w = 0; w < wid; ++w)
+                off += wcount[ct][w];
+            const int sl = off + __popc(mk[ct] & lt);
             map[i] = sl;
             cells[sl] = (int)i;
         }
-        else
+        else if (i < n)
             map[i] = -1;
+        __syncthreads();
+        if (threadIdx.x < 3)
+        {
+            int t = 0;
+            for (int w = 0; w < NW; ++w)
+                t += wcount[threadIdx.x][w];
+            run[threadIdx.x] += t;
+        }
+        __syncthreads();
     }
 }
 
@@ -770,100 +838,94 @@ __global__ void k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
 }
 
 // ---------------------------------------------------------------- K7/K8 stream + collide
-__device__ void equilibrium(const SchemeDev& sc, const double* m, double* meq)
+// m^eq(conserved moments) with compile-time population indices (EQ = MRLBM_EQ_*).
+// Operation order mirrors oracle/mrlbm_oracle.cpp equilibrium() exactly.
+template <int EQ, int Q>
+__device__ __forceinline__ void equilibrium_t(const double* P, double lambda, const double (&m)[Q], double (&meq)[Q])
 {
-    const double* P = sc.eqp;
-    switch (sc.eq)
+    if constexpr (EQ == MRLBM_EQ_BURGERS_D1Q2)
     {
-        case MRLBM_EQ_BURGERS_D1Q2:
+        const double u = m[0];
+        meq[0] = u;
+        meq[1] = __dmul_rn(__dmul_rn(0.5, u), u);
+    }
+    else if constexpr (EQ == MRLBM_EQ_EULER_D1Q3X3)
+    {
+        const double gam = P[0];
+        const double lam2 = __dmul_rn(lambda, lambda);
+        const double rho = m[0], q = m[3], E = m[6];
+        const double u = __ddiv_rn(q, rho);
+        const double p = __dmul_rn(__dsub_rn(gam, 1.0), __dsub_rn(E, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rho), u), u)));
+        const double F[3] = {q, __dadd_rn(__dmul_rn(q, u), p), __dmul_rn(u, __dadd_rn(E, p))};
+        const double U[3] = {rho, q, E};
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
         {
-            const double u = m[0];
-            meq[0] = u;
-            meq[1] = __dmul_rn(__dmul_rn(0.5, u), u);
-            break;
+            meq[3 * i + 0] = U[i];
+            meq[3 * i + 1] = F[i];
+            meq[3 * i + 2] = __dmul_rn(lam2, U[i]);
         }
-        case MRLBM_EQ_EULER_D1Q3X3:
+    }
+    else if constexpr (EQ == MRLBM_EQ_ADVECTION_D2Q4)
+    {
+        const double u = m[0];
+        meq[0] = u;
+        meq[1] = __dmul_rn(P[0], u);
+        meq[2] = __dmul_rn(P[1], u);
+        meq[3] = 0.0;
+    }
+    else if constexpr (EQ == MRLBM_EQ_EULER_D2Q4X4)
+    {
+        const double gam = P[0];
+        const double rho = m[0], qx = m[4], qy = m[8], E = m[12];
+        const double u = __ddiv_rn(qx, rho);
+        const double v = __ddiv_rn(qy, rho);
+        const double ke = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
+        const double p = __dmul_rn(__dsub_rn(gam, 1.0), __dsub_rn(E, __dmul_rn(__dmul_rn(0.5, rho), ke)));
+        const double Fx[4] = {qx, __dadd_rn(__dmul_rn(qx, u), p), __dmul_rn(qx, v), __dmul_rn(u, __dadd_rn(E, p))};
+        const double Fy[4] = {qy, __dmul_rn(qy, u), __dadd_rn(__dmul_rn(qy, v), p), __dmul_rn(v, __dadd_rn(E, p))};
+        const double U[4] = {rho, qx, qy, E};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
         {
-            const double gam = P[0];
-            const double lam2 = __dmul_rn(sc.lambda, sc.lambda);
-            const double rho = m[0], q = m[3], E = m[6];
-            const double u = __ddiv_rn(q, rho);
-            const double p = __dmul_rn(__dsub_rn(gam, 1.0), __dsub_rn(E, __dmul_rn(__dmul_rn(__dmul_rn(0.5, rho), u), u)));
-            const double F[3] = {q, __dadd_rn(__dmul_rn(q, u), p), __dmul_rn(u, __dadd_rn(E, p))};
-            const double U[3] = {rho, q, E};
-            for (int i = 0; i < 3; ++i)
-            {
-                meq[3 * i + 0] = U[i];
-                meq[3 * i + 1] = F[i];
-                meq[3 * i + 2] = __dmul_rn(lam2, U[i]);
-            }
-            break;
+            meq[4 * i + 0] = U[i];
+            meq[4 * i + 1] = Fx[i];
+            meq[4 * i + 2] = Fy[i];
+            meq[4 * i + 3] = 0.0;
         }
-        case MRLBM_EQ_ADVECTION_D2Q4:
+    }
+    else if constexpr (EQ == MRLBM_EQ_NS_D2Q9)
+    {
+        const double cs2 = P[0];
+        const double rho = m[0], qx = m[1], qy = m[2];
+        meq[0] = rho;
+        meq[1] = qx;
+        meq[2] = qy;
+        if (P[1] == 0.0)
         {
-            const double u = m[0];
-            meq[0] = u;
-            meq[1] = __dmul_rn(P[0], u);
-            meq[2] = __dmul_rn(P[1], u);
-            meq[3] = 0.0;
-            break;
+            const double q2 = __dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy));
+            meq[3] = __dmul_rn(3.0, __dadd_rn(__dmul_rn(__dmul_rn(-2.0, cs2), rho), __ddiv_rn(q2, rho)));
+            meq[6] = __dmul_rn(9.0, __dsub_rn(__dmul_rn(__dmul_rn(cs2, cs2), rho), __ddiv_rn(__dmul_rn(cs2, q2), rho)));
         }
-        case MRLBM_EQ_EULER_D2Q4X4:
+        else
         {
-            const double gam = P[0];
-            const double rho = m[0], qx = m[4], qy = m[8], E = m[12];
-            const double u = __ddiv_rn(qx, rho);
-            const double v = __ddiv_rn(qy, rho);
-            const double ke = __dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v));
-            const double p = __dmul_rn(__dsub_rn(gam, 1.0), __dsub_rn(E, __dmul_rn(__dmul_rn(0.5, rho), ke)));
-            const double Fx[4] = {qx, __dadd_rn(__dmul_rn(qx, u), p), __dmul_rn(qx, v), __dmul_rn(u, __dadd_rn(E, p))};
-            const double Fy[4] = {qy, __dmul_rn(qy, u), __dadd_rn(__dmul_rn(qy, v), p), __dmul_rn(v, __dadd_rn(E, p))};
-            const double U[4] = {rho, qx, qy, E};
-            for (int i = 0; i < 4; ++i)
-            {
-                meq[4 * i + 0] = U[i];
-                meq[4 * i + 1] = Fx[i];
-                meq[4 * i + 2] = Fy[i];
-                meq[4 * i + 3] = 0.0;
-            }
-            break;
+            const double qn = __dsqrt_rn(__dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)));
+            meq[3] = __dmul_rn(3.0, __dadd_rn(__dmul_rn(__dmul_rn(-2.0, cs2), rho), __ddiv_rn(qn, rho)));
+            meq[6] = __dmul_rn(9.0, __dsub_rn(__dmul_rn(cs2, cs2), __ddiv_rn(__dmul_rn(cs2, qn), rho)));
         }
-        case MRLBM_EQ_NS_D2Q9:
-        {
-            const double cs2 = P[0];
-            const double rho = m[0], qx = m[1], qy = m[2];
-            meq[0] = rho;
-            meq[1] = qx;
-            meq[2] = qy;
-            if (P[1] == 0.0)
-            {
-                const double q2 = __dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy));
-                meq[3] = __dmul_rn(3.0, __dadd_rn(__dmul_rn(__dmul_rn(-2.0, cs2), rho), __ddiv_rn(q2, rho)));
-                meq[6] = __dmul_rn(9.0, __dsub_rn(__dmul_rn(__dmul_rn(cs2, cs2), rho), __ddiv_rn(__dmul_rn(cs2, q2), rho)));
-            }
-            else
-            {
-                const double qn = __dsqrt_rn(__dadd_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)));
-                meq[3] = __dmul_rn(3.0, __dadd_rn(__dmul_rn(__dmul_rn(-2.0, cs2), rho), __ddiv_rn(qn, rho)));
-                meq[6] = __dmul_rn(9.0, __dsub_rn(__dmul_rn(cs2, cs2), __ddiv_rn(__dmul_rn(cs2, qn), rho)));
-            }
-            meq[4] = __dmul_rn(__dmul_rn(-3.0, cs2), qx);
-            meq[5] = __dmul_rn(__dmul_rn(-3.0, cs2), qy);
-            meq[7] = __ddiv_rn(__dsub_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)), rho);
-            meq[8] = __ddiv_rn(__dmul_rn(qx, qy), rho);
-            break;
-        }
-        default:
-            break;
+        meq[4] = __dmul_rn(__dmul_rn(-3.0, cs2), qx);
+        meq[5] = __dmul_rn(__dmul_rn(-3.0, cs2), qy);
+        meq[7] = __ddiv_rn(__dsub_rn(__dmul_rn(qx, qx), __dmul_rn(qy, qy)), rho);
+        meq[8] = __ddiv_rn(__dmul_rn(qx, qy), rho);
     }
 }
 
-// value of the finest cell (x, y) for the fallback E/A sums: inside -> the
-// materialised reconstruction (leaf or virtual slot at J1); outside -> boundary
-// rule by direct evaluation
-template <int D, int Q>
-__device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev& sc, int x,
-                                            int y, int h, const double* fstar, Aux& aux)
+// value of the finest cell (x, y) for the recursive-path E/A sums: inside -> the
+// materialised zero-detail reconstruction (leaf or virtual slot at J1); outside
+// -> boundary rule by direct evaluation
+template <int D>
+__device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int x,
+                                            int y, int h, int leaf_li, long long leaf_slot, Aux& aux)
 {
     const int lj = g.J1 - g.J0;
     const int nx = g.nx[lj], ny = g.ny[lj];
@@ -874,8 +936,7 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         face = y < 0 ? 2 : 3;
     if (face < 0)
     {
-        const int lin = mr_lin<D>(g, g.J1, x, y);
-        const int sl = tn.map[lj][lin];
+        const int sl = tn.map[lj][mr_lin<D>(g, g.J1, x, y)];
         if (sl < 0)
         {
             flag_err(aux.err, 0);
@@ -883,10 +944,10 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         }
         return F1.f[lj][(long long)h * g.cap[lj] + sl];
     }
-    const int kind = sc.bc_kind[face];
+    const int kind = sc->bc_kind[face];
     if (kind == MRLBM_BC_COPY)
     {
-        // leaf covering the clamped finest cell
+        // value of the leaf covering the clamped finest cell
         const int cx = mr_coord(x, nx, 0), cy = D == 2 ? mr_coord(y, ny, 0) : 0;
         for (int m = g.J1; m >= g.J0; --m)
         {
@@ -899,17 +960,18 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         flag_err(aux.err, 0);
         return 0.0;
     }
-    const int hb = sc.opp[h];
+    const int hb = sc->opp[h];
     if (hb < 0)
     {
         flag_err(aux.err, 2);
         return 0.0;
     }
+    const double v = F1.f[leaf_li][(long long)hb * g.cap[leaf_li] + leaf_slot];
     if (kind == MRLBM_BC_BOUNCE_BACK)
-        return fstar[hb];
+        return v;
     if (kind == MRLBM_BC_ANTI_BOUNCE_BACK)
-        return -fstar[hb];
-    return __dadd_rn(fstar[hb], sc.bc_add[face][h]);
+        return -v;
+    return __dadd_rn(v, sc->bc_add[face][h]);
 }
 
 template <int D>
@@ -918,188 +980,333 @@ __device__ __forceinline__ bool in_box(int x, int y, int bx0, int bx1, int by0, 
     return x >= bx0 && x < bx1 && (D == 1 || (y >= by0 && y < by1));
 }
 
-// sum over the E (side 0) / A (side 1) finest cells in lexicographic order.
-// E and A lie in the one-cell rim inside / outside the leaf's finest box B, so
-// only rows x in {bx0-1, bx0, bx1-1, bx1} are scanned in full; the rows between
-// contribute their end columns {by0-1, by0, by1-1, by1} only.
-template <int D, int Q>
-__device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev& sc, int h, int side, int bx0,
-                          int bx1, int by0, int by1, const double* fstar, Aux& aux)
+// Sum over the E (side 0) / A (side 1) finest cells in lexicographic order
+// (|eta_i| <= 1).  E = (B - eta) \ B, A = B \ (B - eta), enumerated directly:
+// full rows where the row leaves B, else the single end column.
+template <int D>
+__device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int h, int side, int bx0,
+                          int bx1, int by0, int by1, int leaf_li, long long leaf_slot, Aux& aux)
 {
-    const int ex = sc.eta[h][0], ey = D == 1 ? 0 : sc.eta[h][1];
+    const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
     double s = 0.0;
     if (ex == 0 && ey == 0)
         return s;
-    auto visit = [&](int x, int y)
+    if (side == 0)
     {
-        const bool inb = in_box<D>(x, y, bx0, bx1, by0, by1);
-        const bool ine = in_box<D>(x + ex, y + ey, bx0, bx1, by0, by1);
-        if (side == 0 ? (ine && !inb) : (inb && !ine))
-            s = __dadd_rn(s, rim_value<D, Q>(g, tn, F1, sc, x, y, h, fstar, aux));
-    };
-    const int rows[4] = {bx0 - 1, bx0, bx1 - 1, bx1};
-    int prev_row = INT_MIN;
-    for (int r = 0; r < 4; ++r)
-    {
-        const int x = rows[r];
-        if (x == prev_row)
-            continue;
-        // interior rows strictly between the previous edge row and this one
-        if (D == 2 && prev_row != INT_MIN)
+        for (int x = bx0 - ex; x < bx1 - ex; ++x)
         {
-            const int ys[4] = {by0 - 1, by0, by1 - 1, by1};
-            for (int xi = prev_row + 1; xi < x; ++xi)
+            if (x < bx0 || x >= bx1)
             {
-                int prev = INT_MIN;
-                for (int k = 0; k < 4; ++k)
-                {
-                    if (ys[k] == prev)
-                        continue;
-                    prev = ys[k];
-                    visit(xi, ys[k]);
-                }
+                if (D == 1)
+                    s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, 0, h, leaf_li, leaf_slot, aux));
+                else
+                    for (int y = by0 - ey; y < by1 - ey; ++y)
+                        s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, y, h, leaf_li, leaf_slot, aux));
             }
+            else if (D == 2 && ey != 0)
+                s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, ey > 0 ? by0 - 1 : by1, h, leaf_li, leaf_slot, aux));
         }
-        prev_row = x;
-        if (D == 1)
-            visit(x, 0);
-        else
-            for (int y = by0 - 1; y <= by1; ++y)
-                visit(x, y);
+    }
+    else
+    {
+        for (int x = bx0; x < bx1; ++x)
+        {
+            if (x + ex < bx0 || x + ex >= bx1)
+            {
+                if (D == 1)
+                    s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, 0, h, leaf_li, leaf_slot, aux));
+                else
+                    for (int y = by0; y < by1; ++y)
+                        s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, y, h, leaf_li, leaf_slot, aux));
+            }
+            else if (D == 2 && ey != 0)
+                s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, ey > 0 ? by1 - 1 : by0, h, leaf_li, leaf_slot, aux));
+        }
     }
     return s;
 }
 
-template <int D, int Q>
-__global__ void __launch_bounds__(128) k_stream_collide(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* scg, int m,
-                                                        Aux aux)
+// K8: stream of the fallback leaves, one thread per (leaf, population).  Each side
+// uses the flattened table when it is exact for this leaf, else the recursive
+// reconstruction (materialised virtual cells at the finest level + boundary rule).
+// Writes post-stream populations into F0 at the leaf's slot; K7 collides them.
+template <int D>
+__global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* sc,
+                                                         Aux aux)
 {
-    __shared__ SchemeDev sc;
+    const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
+    const int q = g.q;
+    GRID_STRIDE(t, 0, (long long)nfb * q)
     {
-        const int* src = reinterpret_cast<const int*>(scg);
-        int* dst = reinterpret_cast<int*>(&sc);
-        for (int i = threadIdx.x; i < (int)(sizeof(SchemeDev) / sizeof(int)); i += blockDim.x)
-            dst[i] = src[i];
+        const int it = (int)(t / q), h = (int)(t % q);
+        const int2 e = aux.fb_list[it];
+        const unsigned mask = aux.fb_mask[it];
+        const int m = e.x, li = m - g.J0;
+        const long long slot = tn.map[li][e.y];
+        if (slot < 0)
+        {
+            flag_err(aux.err, 2);
+            continue;
+        }
+        const int ny = g.ny[li];
+        const long long cap = g.cap[li];
+        int x, y;
+        lin2xy<D>(e.y, ny, x, y);
+        const int gap = g.J1 - m;
+        double sums[2];
+        for (int side = 0; side < 2; ++side)
+        {
+            const int key = (gap * q + h) * 2 + side;
+            (void)key;
+            const bool ok = ((mask >> (2 * h + side)) & 1u) == 0;
+            double acc = 0.0;
+            if (ok)
+            {
+                const int2 ti = aux.tidx[key];
+                for (int k = ti.x; k < ti.x + ti.y; ++k)
+                {
+                    const int2 o = aux.toff[k];
+                    const int sl = tn.map[li][mr_lin<D>(g, m, x + o.x, y + o.y)];
+                    if (sl < 0)
+                    {
+                        flag_err(aux.err, 0);
+                        continue;
+                    }
+                    acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + sl]));
+                }
+            }
+            else
+            {
+                const int side_n = 1 << gap;
+                const int bx0 = x * side_n, bx1 = bx0 + side_n;
+                const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
+                acc = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, slot, aux);
+            }
+            sums[side] = acc;
+        }
+        const double scale = ldexp(1.0, D * (m - g.J1));
+        const long long o = (long long)h * cap + slot;
+        F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+    }
+}
+
+// K7: table-path stream + collision +
+// obstacle blend, one thread per leaf.  Fallback leaves take their post-stream
+// populations from K8 (already in F0).  BS = block size of the block-diagonal M.
+template <int D, int Q, int BS, int EQ>
+__global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F0, Fld F1, Flags fl,
+                                                           const SchemeDev* scg, int m, Aux aux)
+{
+    constexpr int kMaxE = 2 * Q * 25;
+    constexpr int kU = D == 1 ? 5 : 25; // distinct table offsets at one gap (5^D box)
+    constexpr int kT = 256;
+    __shared__ double sM[Q * BS], sMi[Q * BS], sS[Q], sP[8], sW[kMaxE];
+    __shared__ uint8_t sU[kMaxE];        // entry -> index into the distinct offsets
+    __shared__ int2 sIdx[2 * Q];
+    __shared__ int2 sUoff[kU];
+    __shared__ int sNU;
+    __shared__ int sSlot[kU][kT];        // per-thread neighbour slots
+    __shared__ double sFeq[Q];
+    const int gap = g.J1 - m;
+    for (int i = threadIdx.x; i < Q * BS; i += blockDim.x)
+    {
+        const int r = i / BS, c = i % BS;
+        const int col = (r / BS) * BS + c;
+        sM[i] = scg->M[r * Q + col];
+        sMi[i] = scg->Minv[r * Q + col];
+    }
+    for (int i = threadIdx.x; i < Q; i += blockDim.x)
+    {
+        sS[i] = scg->s[i];
+        sFeq[i] = scg->obs_feq[i];
+    }
+    if (threadIdx.x < 8)
+        sP[threadIdx.x] = scg->eqp[threadIdx.x];
+    // this gap's flattened tables and distinct offsets (deduplicated on the host)
+    {
+        const int2 gu = aux.guidx[gap];
+        const int base = aux.tidx[gap * 2 * Q].x;
+        const int2 last = aux.tidx[gap * 2 * Q + 2 * Q - 1];
+        const int ne = min(last.x + last.y - base, kMaxE);
+        for (int t = threadIdx.x; t < 2 * Q; t += blockDim.x)
+        {
+            const int2 ti = aux.tidx[gap * 2 * Q + t];
+            sIdx[t] = make_int2(ti.x - base, ti.y);
+        }
+        for (int e = threadIdx.x; e < ne; e += blockDim.x)
+        {
+            sU[e] = aux.tu[base + e];
+            sW[e] = aux.tw[base + e];
+        }
+        for (int u = threadIdx.x; u < gu.y && u < kU; u += blockDim.x)
+            sUoff[u] = aux.guoff[gu.x + u];
+        if (threadIdx.x == 0)
+            sNU = min(gu.y, kU);
     }
     __syncthreads();
+    const int nu = sNU;
     const int li = m - g.J0;
     const int nL = tn.cnt[li * 4 + 0];
     const int nx = g.nx[li], ny = g.ny[li];
     const long long cap = g.cap[li];
-    const int gap = g.J1 - m;
     const double scale = ldexp(1.0, D * (m - g.J1));
-    const int bs = sc.bs;
+    const double* Fin = F1.f[li];
+    double* Fout = F0.f[li];
+    const int32_t* map = tn.map[li];
+    const int per0 = g.per0, per1 = g.per1;
+    int* myslot = &sSlot[0][threadIdx.x];
     GRID_STRIDE(s, 0, nL)
     {
         const int lin = tn.cells[li][s];
-        int x, y;
-        lin2xy<D>(lin, ny, x, y);
         const bool fb = (fl.kind[li][lin] & K_FB) != 0;
-        double fs[Q], f[Q];
-        for (int h = 0; h < Q; ++h)
-            fs[h] = F1.f[li][(long long)h * cap + s];
-        if (!fb)
+        double f[Q];
+        if (fb)
         {
+#pragma unroll
             for (int h = 0; h < Q; ++h)
-            {
-                double sum[2];
-                for (int side = 0; side < 2; ++side)
-                {
-                    const int2 ti = aux.tidx[(gap * Q + h) * 2 + side];
-                    double acc = 0.0;
-                    for (int e = ti.x; e < ti.x + ti.y; ++e)
-                    {
-                        const int2 o = aux.toff[e];
-                        int xx = x + o.x, yy = y + o.y;
-                        if (g.per0)
-                            xx = mr_coord(xx, nx, 1);
-                        if (D == 2 && g.per1)
-                            yy = mr_coord(yy, ny, 1);
-                        const int sl = tn.map[li][xy2lin<D>(xx, yy, ny)];
-                        if (sl < 0)
-                        {
-                            flag_err(aux.err, 0);
-                            continue;
-                        }
-                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[e], F1.f[li][(long long)h * cap + sl]));
-                    }
-                    sum[side] = acc;
-                }
-                f[h] = __dadd_rn(fs[h], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
-            }
+                f[h] = Fout[(long long)h * cap + s];
         }
         else
         {
-            const int side_n = 1 << gap;
-            const int bx0 = x * side_n, bx1 = bx0 + side_n;
-            const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
-            for (int h = 0; h < Q; ++h)
+            int x, y;
+            lin2xy<D>(lin, ny, x, y);
+            // all neighbour slots first (independent loads), then pure gathers
+            for (int u = 0; u < nu; ++u)
             {
-                const double sE = rim_sum<D, Q>(g, tn, F1, sc, h, 0, bx0, bx1, by0, by1, fs, aux);
-                const double sA = rim_sum<D, Q>(g, tn, F1, sc, h, 1, bx0, bx1, by0, by1, fs, aux);
-                f[h] = __dadd_rn(fs[h], __dmul_rn(scale, __dsub_rn(sE, sA)));
+                const int2 o = sUoff[u];
+                int xx = x + o.x, yy = y + o.y;
+                if (per0)
+                    xx = mr_coord(xx, nx, 1);
+                if (D == 2 && per1)
+                    yy = mr_coord(yy, ny, 1);
+                myslot[u * kT] = map[xy2lin<D>(xx, yy, ny)];
+            }
+            if (gap == 0)
+            {
+                // finest level: every table has at most one entry (E = {-eta}, A = {0});
+                // branch-free so all 2Q gathers are independent and in flight together
+                double vE[Q], vA[Q], fs[Q];
+#pragma unroll
+                for (int h = 0; h < Q; ++h)
+                {
+                    const double* Fh = Fin + (long long)h * cap;
+                    const int2 tE = sIdx[2 * h], tA = sIdx[2 * h + 1];
+                    const int slE = tE.y ? myslot[sU[tE.x] * kT] : -1;
+                    const int slA = tA.y ? myslot[sU[tA.x] * kT] : -1;
+                    fs[h] = Fh[s];
+                    vE[h] = slE >= 0 ? Fh[slE] : 0.0;
+                    vA[h] = slA >= 0 ? Fh[slA] : 0.0;
+                }
+#pragma unroll
+                for (int h = 0; h < Q; ++h)
+                {
+                    const int2 tE = sIdx[2 * h], tA = sIdx[2 * h + 1];
+                    const double sE = tE.y ? __dadd_rn(0.0, __dmul_rn(sW[tE.x], vE[h])) : 0.0;
+                    const double sA = tA.y ? __dadd_rn(0.0, __dmul_rn(sW[tA.x], vA[h])) : 0.0;
+                    f[h] = __dadd_rn(fs[h], __dmul_rn(scale, __dsub_rn(sE, sA)));
+                }
+            }
+            else
+            {
+#pragma unroll
+                for (int h = 0; h < Q; ++h)
+                {
+                    const double* Fh = Fin + (long long)h * cap;
+                    const double fs = Fh[s];
+                    double sum[2];
+#pragma unroll
+                    for (int side = 0; side < 2; ++side)
+                    {
+                        const int2 ti = sIdx[2 * h + side];
+                        double acc = 0.0;
+#pragma unroll 8
+                        for (int e = ti.x; e < ti.x + ti.y; ++e)
+                        {
+                            const int sl = myslot[sU[e] * kT];
+                            const double v = sl >= 0 ? Fh[sl] : 0.0;
+                            acc = __dadd_rn(acc, __dmul_rn(sW[e], v));
+                        }
+                        sum[side] = acc;
+                    }
+                    f[h] = __dadd_rn(fs, __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+                }
             }
         }
-        // collide: m = M f; m' = (1-s) m + s meq; f* = M^-1 m'
+        // collide: m = M f (block diagonal, DenseMatrix::multiply order),
+        // m' = (1-s) m + s m^eq, f* = M^-1 m'
         double mo[Q], meq[Q];
+#pragma unroll
         for (int i = 0; i < Q; ++i)
         {
-            const int b0 = (i / bs) * bs;
+            const int b0 = (i / BS) * BS;
             double acc = 0.0;
-            for (int j = b0; j < b0 + bs; ++j)
-                acc = __dadd_rn(acc, __dmul_rn(sc.M[i * Q + j], f[j]));
+#pragma unroll
+            for (int j = 0; j < BS; ++j)
+                acc = __dadd_rn(acc, __dmul_rn(sM[i * BS + j], f[b0 + j]));
             mo[i] = acc;
         }
-        equilibrium(sc, mo, meq);
+        equilibrium_t<EQ, Q>(sP, scg->lambda, mo, meq);
+#pragma unroll
         for (int i = 0; i < Q; ++i)
-            mo[i] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, sc.s[i]), mo[i]), __dmul_rn(sc.s[i], meq[i]));
-        bool bad = false;
+            mo[i] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, sS[i]), mo[i]), __dmul_rn(sS[i], meq[i]));
+#pragma unroll
         for (int i = 0; i < Q; ++i)
         {
-            const int b0 = (i / bs) * bs;
+            const int b0 = (i / BS) * BS;
             double acc = 0.0;
-            for (int j = b0; j < b0 + bs; ++j)
-                acc = __dadd_rn(acc, __dmul_rn(sc.Minv[i * Q + j], mo[j]));
+#pragma unroll
+            for (int j = 0; j < BS; ++j)
+                acc = __dadd_rn(acc, __dmul_rn(sMi[i * BS + j], mo[b0 + j]));
             f[i] = acc;
         }
-        if (sc.obstacle == 1 && D == 2)
+        if constexpr (EQ == MRLBM_EQ_NS_D2Q9 && D == 2)
         {
-            // config 5 volume-fraction blend
-            const double dx = ldexp(1.0, -m);
-            const double x0 = __dadd_rn(sc.origin[0], __dmul_rn((double)x, dx));
-            const double y0 = __dadd_rn(sc.origin[1], __dmul_rn((double)y, dx));
-            const double x1 = __dadd_rn(x0, dx), y1 = __dadd_rn(y0, dx);
-            const bool cand = !(x1 < __dsub_rn(sc.obs_c[0], sc.obs_r) || x0 > __dadd_rn(sc.obs_c[0], sc.obs_r) ||
-                                y1 < __dsub_rn(sc.obs_c[1], sc.obs_r) || y0 > __dadd_rn(sc.obs_c[1], sc.obs_r));
-            if (cand)
+            if (scg->obstacle == 1)
             {
-                const int ns = sc.obs_ns;
-                const double r2 = __dmul_rn(sc.obs_r, sc.obs_r);
-                int cnt = 0;
-                for (int a = 0; a < ns; ++a)
+                // config 5 volume-fraction blend
+                int x, y;
+                lin2xy<D>(lin, ny, x, y);
+                const double dx = ldexp(1.0, -m);
+                const double ox = scg->origin[0], oy = scg->origin[1];
+                const double cx = scg->obs_c[0], cy = scg->obs_c[1], r = scg->obs_r;
+                const double x0 = __dadd_rn(ox, __dmul_rn((double)x, dx));
+                const double y0 = __dadd_rn(oy, __dmul_rn((double)y, dx));
+                const double x1 = __dadd_rn(x0, dx), y1 = __dadd_rn(y0, dx);
+                const bool cand = !(x1 < __dsub_rn(cx, r) || x0 > __dadd_rn(cx, r) || y1 < __dsub_rn(cy, r) ||
+                                    y0 > __dadd_rn(cy, r));
+                if (cand)
                 {
-                    const double sx = __dadd_rn(sc.origin[0], __dmul_rn(__dadd_rn((double)x, __ddiv_rn((double)a + 0.5, (double)ns)), dx));
-                    const double ddx = __dsub_rn(sx, sc.obs_c[0]);
-                    const double rx = __dmul_rn(ddx, ddx);
-                    for (int b = 0; b < ns; ++b)
+                    const int ns = scg->obs_ns;
+                    const double r2 = __dmul_rn(r, r);
+                    int cnt = 0;
+                    for (int a = 0; a < ns; ++a)
                     {
-                        const double sy = __dadd_rn(sc.origin[1], __dmul_rn(__dadd_rn((double)y, __ddiv_rn((double)b + 0.5, (double)ns)), dx));
-                        const double ddy = __dsub_rn(sy, sc.obs_c[1]);
-                        cnt += __dadd_rn(rx, __dmul_rn(ddy, ddy)) < r2;
+                        const double sx = __dadd_rn(ox, __dmul_rn(__dadd_rn((double)x, __ddiv_rn((double)a + 0.5, (double)ns)), dx));
+                        const double ddx = __dsub_rn(sx, cx);
+                        const double rx = __dmul_rn(ddx, ddx);
+                        for (int b = 0; b < ns; ++b)
+                        {
+                            const double sy = __dadd_rn(oy, __dmul_rn(__dadd_rn((double)y, __ddiv_rn((double)b + 0.5, (double)ns)), dx));
+                            const double ddy = __dsub_rn(sy, cy);
+                            cnt += __dadd_rn(rx, __dmul_rn(ddy, ddy)) < r2;
+                        }
                     }
-                }
-                if (cnt > 0)
-                {
-                    const double alpha = __ddiv_rn((double)cnt, (double)(ns * ns));
-                    for (int h = 0; h < Q; ++h)
-                        f[h] = __dadd_rn(__dmul_rn(alpha, sc.obs_feq[h]), __dmul_rn(__dsub_rn(1.0, alpha), f[h]));
+                    if (cnt > 0)
+                    {
+                        const double alpha = __ddiv_rn((double)cnt, (double)(ns * ns));
+#pragma unroll
+                        for (int h = 0; h < Q; ++h)
+                            f[h] = __dadd_rn(__dmul_rn(alpha, sFeq[h]), __dmul_rn(__dsub_rn(1.0, alpha), f[h]));
+                    }
                 }
             }
         }
+        bool bad = false;
+#pragma unroll
         for (int h = 0; h < Q; ++h)
         {
             bad = bad || !isfinite(f[h]);
-            F0.f[li][(long long)h * cap + s] = f[h];
+            Fout[(long long)h * cap + s] = f[h];
         }
         if (bad)
             flag_err(aux.err, 1);
@@ -1193,11 +1400,21 @@ struct mrlbm_ctx {
     int* err = nullptr;
     int* fbc = nullptr;
     int2* fbl = nullptr;
+    unsigned* fbm = nullptr;
     long long fbcap = 0;
     long long* upd = nullptr;
     int2* tidx = nullptr;
     int2* toff = nullptr;
     double* tw = nullptr;
+    int4* tdep = nullptr;
+    int2* tpidx = nullptr;
+    int2* tpar = nullptr;
+    int4* udep = nullptr;
+    int2* guidx = nullptr;
+    int2* guoff = nullptr;
+    uint8_t* tu = nullptr;
+    int2* upidx = nullptr;
+    int2* upar = nullptr;
     int cur = 0;
     bool committed = false;
     bool profiling = false;
@@ -1268,11 +1485,21 @@ Aux aux_of(mrlbm_ctx* c)
     a.err = c->err;
     a.fb_count = c->fbc;
     a.fb_list = c->fbl;
+    a.fb_mask = c->fbm;
     a.fb_cap = c->fbcap;
     a.updates = c->upd;
     a.tidx = c->tidx;
     a.toff = c->toff;
     a.tw = c->tw;
+    a.tdep = c->tdep;
+    a.tpidx = c->tpidx;
+    a.tpar = c->tpar;
+    a.udep = c->udep;
+    a.guidx = c->guidx;
+    a.guoff = c->guoff;
+    a.tu = c->tu;
+    a.upidx = c->upidx;
+    a.upar = c->upar;
     return a;
 }
 
@@ -1305,7 +1532,7 @@ void phase_mark(mrlbm_ctx* c, int k)
         cudaEventRecord(c->ev[k], c->stream);
 }
 
-template <int D, int Q>
+template <int D, int Q, int BS, int EQ>
 void enqueue_step(mrlbm_ctx* c)
 {
     const int o = c->cur, n = 1 - c->cur;
@@ -1347,7 +1574,11 @@ void enqueue_step(mrlbm_ctx* c)
         { c->kcount++; k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux); }
     { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux); }
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m); }
+    {
+        if (D == 2)
+            { c->kcount++; k_ghost_rows<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, c->keep[m - c->J0]); }
+        { c->kcount++; k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, c->keep[m - c->J0]); }
+    }
     for (int m = c->J0; m <= c->J1; ++m)
         launch_compaction<D>(c, n, m);
     phase_mark(c, 4);
@@ -1360,8 +1591,9 @@ void enqueue_step(mrlbm_ctx* c)
         { c->kcount++; k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux); }
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
+    { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux); }
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_stream_collide<D, Q><<<grid_for(c, g.cap[m - c->J0], 128), 128, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux); }
+        { c->kcount++; k_stream_collide<D, Q, BS, EQ><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux); }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd); }
     phase_mark(c, 6);
     c->kernels_per_step = c->kcount;
@@ -1369,18 +1601,18 @@ void enqueue_step(mrlbm_ctx* c)
 
 using StepFn = void (*)(mrlbm_ctx*);
 
-StepFn step_fn(int d, int q)
+StepFn step_fn(int d, int q, int nblocks, int eq)
 {
-    if (d == 1 && q == 2)
-        return enqueue_step<1, 2>;
-    if (d == 1 && q == 9)
-        return enqueue_step<1, 9>;
-    if (d == 2 && q == 4)
-        return enqueue_step<2, 4>;
-    if (d == 2 && q == 9)
-        return enqueue_step<2, 9>;
-    if (d == 2 && q == 16)
-        return enqueue_step<2, 16>;
+    if (d == 1 && q == 2 && nblocks == 1 && eq == MRLBM_EQ_BURGERS_D1Q2)
+        return enqueue_step<1, 2, 2, MRLBM_EQ_BURGERS_D1Q2>;
+    if (d == 1 && q == 9 && nblocks == 3 && eq == MRLBM_EQ_EULER_D1Q3X3)
+        return enqueue_step<1, 9, 3, MRLBM_EQ_EULER_D1Q3X3>;
+    if (d == 2 && q == 4 && nblocks == 1 && eq == MRLBM_EQ_ADVECTION_D2Q4)
+        return enqueue_step<2, 4, 4, MRLBM_EQ_ADVECTION_D2Q4>;
+    if (d == 2 && q == 16 && nblocks == 4 && eq == MRLBM_EQ_EULER_D2Q4X4)
+        return enqueue_step<2, 16, 4, MRLBM_EQ_EULER_D2Q4X4>;
+    if (d == 2 && q == 9 && nblocks == 1 && eq == MRLBM_EQ_NS_D2Q9)
+        return enqueue_step<2, 9, 9, MRLBM_EQ_NS_D2Q9>;
     return nullptr;
 }
 
@@ -1408,7 +1640,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     mrlbm_ctx* ctx = nullptr;
     if (!sc || !rc)
         return MRLBM_ERR_CONFIG;
-    if (sc->d < 1 || sc->d > 2 || !step_fn(sc->d, sc->q))
+    if (sc->d < 1 || sc->d > 2 || !step_fn(sc->d, sc->q, sc->nblocks, sc->equilibrium))
         return MRLBM_ERR_CONFIG;
     if (rc->j_min < 0 || rc->j_max <= rc->j_min || rc->j_max - rc->j_min + 1 > kL)
         return MRLBM_ERR_CONFIG;
@@ -1486,6 +1718,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         }
         ctx->fbcap = total_cells;
         CU(cudaMalloc(&ctx->fbl, sizeof(int2) * ctx->fbcap));
+        CU(cudaMalloc(&ctx->fbm, sizeof(unsigned) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbc, sizeof(int) * 2));
         CU(cudaMalloc(&ctx->err, sizeof(int) * 4));
         CU(cudaMemset(ctx->err, 0, sizeof(int) * 4));
@@ -1537,15 +1770,26 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         h.obs_r = rc->obstacle_radius;
         CU(cudaMalloc(&ctx->sch, sizeof(SchemeDev)));
         CU(cudaMemcpy(ctx->sch, &h, sizeof(SchemeDev), cudaMemcpyHostToDevice));
-        // flattened tables for every gap / population / side
-        std::vector<int2> idx, off;
+        // flattened tables + exactness sets for every gap / population / side
+        std::vector<int2> idx, off, pidx, par, upidx, upar, guidx, guoff;
+        std::vector<int4> dep, udep;
         std::vector<double> w;
+        std::vector<uint8_t> tu;
         for (int gp = 0; gp < ctx->nlev; ++gp)
+        {
+            int4 ub = make_int4(0, 0, 0, 0);
+            std::vector<std::pair<int, int>> un;
+            std::vector<std::pair<int, int>> gu; // distinct table offsets of this gap
+            guidx.push_back(make_int2(static_cast<int>(guoff.size()), 0));
             for (int hh = 0; hh < sc->q; ++hh)
+            {
+                if (std::abs(sc->eta[hh][0]) > 1 || (sc->d == 2 && std::abs(sc->eta[hh][1]) > 1))
+                    return set_err(ctx, MRLBM_ERR_CONFIG, "velocities with |eta_i| > 1 are not supported");
                 for (int side = 0; side < 2; ++side)
                 {
                     std::vector<TableEntry> t;
-                    const int rcode = build_stream_table(sc->d, gp, sc->eta[hh], side, t);
+                    TableSets ts{};
+                    const int rcode = build_stream_table(sc->d, gp, sc->eta[hh], side, t, &ts);
                     if (rcode != MRLBM_OK)
                         return set_err(ctx, rcode, "flattened table construction failed");
                     idx.push_back(make_int2(static_cast<int>(off.size()), static_cast<int>(t.size())));
@@ -1553,19 +1797,54 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
                     {
                         off.push_back(make_int2(e.off[0], e.off[1]));
                         w.push_back(e.w);
+                        const std::pair<int, int> o(e.off[0], e.off[1]);
+                        auto it = std::find(gu.begin(), gu.end(), o);
+                        tu.push_back(static_cast<uint8_t>(it - gu.begin()));
+                        if (it == gu.end())
+                            gu.push_back(o);
+                    }
+                    const int4 db = make_int4(ts.dep_lo[0], ts.dep_hi[0], ts.dep_lo[1], ts.dep_hi[1]);
+                    dep.push_back(db);
+                    ub = make_int4(std::min(ub.x, db.x), std::max(ub.y, db.y), std::min(ub.z, db.z), std::max(ub.w, db.w));
+                    pidx.push_back(make_int2(static_cast<int>(par.size()), static_cast<int>(ts.par.size())));
+                    for (const auto& p : ts.par)
+                    {
+                        par.push_back(make_int2(p.first, p.second));
+                        if (std::find(un.begin(), un.end(), p) == un.end())
+                            un.push_back(p);
                     }
                 }
+            }
+            guidx.back().y = static_cast<int>(gu.size());
+            for (const auto& o : gu)
+                guoff.push_back(make_int2(o.first, o.second));
+            udep.push_back(ub);
+            upidx.push_back(make_int2(static_cast<int>(upar.size()), static_cast<int>(un.size())));
+            for (const auto& p : un)
+                upar.push_back(make_int2(p.first, p.second));
+        }
         if (off.empty())
         {
             off.push_back(make_int2(0, 0));
             w.push_back(0.0);
         }
-        CU(cudaMalloc(&ctx->tidx, sizeof(int2) * idx.size()));
-        CU(cudaMalloc(&ctx->toff, sizeof(int2) * off.size()));
-        CU(cudaMalloc(&ctx->tw, sizeof(double) * w.size()));
-        CU(cudaMemcpy(ctx->tidx, idx.data(), sizeof(int2) * idx.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(ctx->toff, off.data(), sizeof(int2) * off.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(ctx->tw, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice));
+        if (par.empty())
+            par.push_back(make_int2(0, 0));
+        if (upar.empty())
+            upar.push_back(make_int2(0, 0));
+        if (guoff.empty())
+            guoff.push_back(make_int2(0, 0));
+        tu.push_back(0);
+        auto up = [&](auto*& dst, const auto& v) -> int
+        {
+            using T = typename std::decay_t<decltype(v)>::value_type;
+            CU(cudaMalloc(&dst, sizeof(T) * v.size()));
+            CU(cudaMemcpy(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+            return MRLBM_OK;
+        };
+        if (up(ctx->tidx, idx) || up(ctx->toff, off) || up(ctx->tw, w) || up(ctx->tdep, dep) || up(ctx->tpidx, pidx) ||
+            up(ctx->tpar, par) || up(ctx->udep, udep) || up(ctx->guidx, guidx) || up(ctx->guoff, guoff) || up(ctx->tu, tu) || up(ctx->upidx, upidx) || up(ctx->upar, upar))
+            return MRLBM_ERR_CUDA;
         for (auto& e : ctx->ev)
             CU(cudaEventCreate(&e));
         return MRLBM_OK;
@@ -1708,7 +1987,7 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
         return MRLBM_ERR_CONFIG;
     if (!ctx->committed)
         return set_err(ctx, MRLBM_ERR_STATE, "step before commit");
-    StepFn fn = step_fn(ctx->D, ctx->q);
+    StepFn fn = step_fn(ctx->D, ctx->q, ctx->sc.nblocks, ctx->sc.equilibrium);
     CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
     CU(cudaEventRecord(ctx->ev[14], ctx->stream));
     double phase[MRLBM_PHASE_COUNT] = {0};
@@ -1774,7 +2053,7 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
             nI += counts[li * 4 + 1];
             nG += counts[li * 4 + 2];
         }
-        stats->fallback_leaves = fb[0] + fb[1];
+        stats->fallback_leaves = fb[0];
         stats->kernel_launches = ctx->kernels_per_step * nsteps;
         stats->bytes_stream = 8LL * ctx->q * (2 * nS + nG);
         stats->leaf_updates = upd;
@@ -1898,10 +2177,20 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->err);
     cudaFree(ctx->fbc);
     cudaFree(ctx->fbl);
+    cudaFree(ctx->fbm);
     cudaFree(ctx->upd);
     cudaFree(ctx->tidx);
     cudaFree(ctx->toff);
     cudaFree(ctx->tw);
+    cudaFree(ctx->tdep);
+    cudaFree(ctx->tpidx);
+    cudaFree(ctx->tpar);
+    cudaFree(ctx->udep);
+    cudaFree(ctx->guidx);
+    cudaFree(ctx->guoff);
+    cudaFree(ctx->tu);
+    cudaFree(ctx->upidx);
+    cudaFree(ctx->upar);
     for (auto& e : ctx->ev)
         if (e)
             cudaEventDestroy(e);

@@ -177,3 +177,37 @@ def test_deep_gap_rounding():
         a_off, a_w = stream_table(2, g, (1, 1), 0)
         b_off, b_w = pyoracle.stream_table(2, g, (1, 1), 0)
         assert np.array_equal(a_w.view(np.uint64), b_w.view(np.uint64))
+
+
+@pytest.mark.parametrize("d,eta", [(1, (1,)), (1, (-1,)), (2, (1, 0)), (2, (0, 1)), (2, (1, 1)), (2, (-1, 1)), (2, (0, 0))])
+def test_table_exactness_sets(d, eta):
+    """Product (support propagation in push form) and oracle (memo keys of the pull
+    recursion) agree on the exactness sets of every table (Decision D.13)."""
+    from paper_2103_02903_b200 import _lib
+    L = _lib.lib()
+    O = pyoracle.oracle_lib()
+    O.oracle_stream_table_sets.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_void_p,
+                                           C.POINTER(C.c_int), C.c_void_p, C.POINTER(C.c_int)]
+    L.mrlbm_stream_table_sets.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_void_p,
+                                          C.c_void_p, C.POINTER(C.c_int)]
+    e = (C.c_int32 * 3)(*([int(v) for v in eta] + [0] * (3 - len(eta))))
+    for g in range(0, 6):
+        for side in (0, 1):
+            cap = 4096
+            dep = np.zeros((cap, d), dtype=np.int32)
+            par = np.zeros((cap, d), dtype=np.int32)
+            nd, npar = C.c_int(), C.c_int()
+            assert O.oracle_stream_table_sets(d, g, e, side, cap, vp(dep), C.byref(nd), vp(par), C.byref(npar)) == 0
+            box = np.zeros(4, dtype=np.int32)
+            par2 = np.zeros((cap, d), dtype=np.int32)
+            n2 = C.c_int()
+            assert L.mrlbm_stream_table_sets(d, g, e, side, cap, vp(box), vp(par2), C.byref(n2)) == 0
+            assert npar.value == n2.value
+            assert np.array_equal(par[: npar.value], par2[: n2.value])
+            if nd.value:
+                dd = dep[: nd.value]
+                assert box[0] == dd[:, 0].min() and box[1] == dd[:, 0].max()
+                if d == 2:
+                    assert box[2] == dd[:, 1].min() and box[3] == dd[:, 1].max()
+            # parents sit in the 3^d box around the leaf for |eta| <= 1
+            assert (np.abs(par[: npar.value]) <= 1).all()
