@@ -88,6 +88,19 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
 
 
+def reduce_replicas(ms, updates, device, world):
+    """Replicas-only aggregation: max device time over ranks, summed
+    leaf updates.  Works with any torch.distributed backend (gloo tests on CPU)."""
+    import torch
+    t = torch.tensor([float(ms)], device=device, dtype=torch.float64)
+    u = torch.tensor([float(updates)], device=device, dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(u.item())
+
+
 def snapshot(s, rc):
     out = {}
     for lv in range(rc.j_min, rc.j_max + 1):
@@ -200,13 +213,8 @@ def bench_product(args):
     ms = sum(a.elapsed_time(b) for a, b in evs)
     updates = st.leaf_updates - u0
     clocks = clk.summary()
-    tmax = torch.tensor([ms], device=dev, dtype=torch.float64)
-    utot = torch.tensor([float(updates)], device=dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(utot, op=torch.distributed.ReduceOp.SUM)
-    ms_max = float(tmax.item())
-    value = float(utot.item()) / (ms_max / 1e3)
+    ms_max, utot = reduce_replicas(ms, updates, dev, world)
+    value = utot / (ms_max / 1e3)
     state_bytes = 8 * sc.q * sum(int(st.leaves[i]) for i in range(st.levels))
 
     # ---- phase breakdown (profiling pass: eager launches + events per phase), continues the run
@@ -241,13 +249,8 @@ def bench_product(args):
     barrier()
     e2e_s = time.perf_counter() - t0
     d2h = sum(v[0].nbytes + v[1].nbytes for v in out.values())
-    e2e_val = st2.leaf_updates / e2e_s
-    et = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-    eu = torch.tensor([float(st2.leaf_updates)], device=dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(et, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(eu, op=torch.distributed.ReduceOp.SUM)
-        e2e_val = float(eu.item()) / float(et.item())
+    e2e_smax, e2e_u = reduce_replicas(e2e_s, st2.leaf_updates, dev, world)
+    e2e_val = e2e_u / e2e_smax
     s2.close()
 
     cpu = None

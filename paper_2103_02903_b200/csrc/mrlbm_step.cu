@@ -35,6 +35,9 @@ constexpr int kL = MRLBM_MAX_LEVELS;
 constexpr int kQ = MRLBM_MAX_Q;
 
 enum : uint8_t { K_LEAF = 1, K_INT = 2, K_VIRT = 4, K_FB = 8 };
+// fallback leaves with gap >= kDeepGap stream in the dedicated K8 kernel (long
+// serial rims, 2Q-way parallel per leaf); shallower ones inline in K7
+constexpr int kDeepGap = 1;
 
 struct Geo {
     int d, q, J0, J1, nlev, per0, per1;
@@ -56,6 +59,7 @@ struct Flags {
     uint8_t* kind[kL];
     uint8_t* rn[kL];
     uint8_t* keep[kL];
+    unsigned* fbm[kL]; // dense per cell: invalid (population, side) mask of fallback leaves
 };
 
 struct SchemeDev {
@@ -441,14 +445,21 @@ __global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
                     mask |= 1u << pair;
             }
             fl.kind[li][i] = K_LEAF | K_FB;
-            const int k = atomicAdd(aux.fb_count, 1);
-            if (k < aux.fb_cap)
+            fl.fbm[li][i] = mask;
+            if (gap > 0)
             {
-                aux.fb_list[k] = make_int2(m, (int)i);
-                aux.fb_mask[k] = mask;
+                // listed for the reconstruction band (and K8 when gap >= kDeepGap)
+                const int k = atomicAdd(aux.fb_count, 1);
+                if (k < aux.fb_cap)
+                {
+                    aux.fb_list[k] = make_int2(m, (int)i);
+                    aux.fb_mask[k] = mask;
+                }
+                else
+                    flag_err(aux.err, 2);
             }
             else
-                flag_err(aux.err, 2);
+                atomicAdd(aux.fb_count + 1, 1);
         }
     }
 }
@@ -1040,6 +1051,8 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
     {
         const int it = (int)(t / q), h = (int)(t % q);
         const int2 e = aux.fb_list[it];
+        if (g.J1 - e.x < kDeepGap)
+            continue; // streamed inline by K7
         const unsigned mask = aux.fb_mask[it];
         const int m = e.x, li = m - g.J0;
         const long long slot = tn.map[li][e.y];
@@ -1160,8 +1173,9 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
         const int lin = tn.cells[li][s];
         const bool fb = (fl.kind[li][lin] & K_FB) != 0;
         double f[Q];
-        if (fb)
+        if (fb && gap >= kDeepGap)
         {
+            // deep-gap fallback leaf: post-stream populations from K8
 #pragma unroll
             for (int h = 0; h < Q; ++h)
                 f[h] = Fout[(long long)h * cap + s];
@@ -1175,13 +1189,52 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
             {
                 const int2 o = sUoff[u];
                 int xx = x + o.x, yy = y + o.y;
+                bool in = true;
                 if (per0)
                     xx = mr_coord(xx, nx, 1);
-                if (D == 2 && per1)
-                    yy = mr_coord(yy, ny, 1);
-                myslot[u * kT] = map[xy2lin<D>(xx, yy, ny)];
+                else
+                    in = xx >= 0 && xx < nx;
+                if (D == 2)
+                {
+                    if (per1)
+                        yy = mr_coord(yy, ny, 1);
+                    else
+                        in = in && yy >= 0 && yy < ny;
+                }
+                myslot[u * kT] = in ? map[xy2lin<D>(xx, yy, ny)] : -1;
             }
-            if (gap == 0)
+            const unsigned mask = fb ? fl.fbm[li][lin] : 0u;
+            if (mask)
+            {
+                // shallow fallback leaf: table where exact, recursive rim elsewhere
+                const int side_n = 1 << gap;
+                const int bx0 = x * side_n, bx1 = bx0 + side_n;
+                const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
+                for (int h = 0; h < Q; ++h)
+                {
+                    const double* Fh = Fin + (long long)h * cap;
+                    double sum[2];
+                    for (int side = 0; side < 2; ++side)
+                    {
+                        double acc = 0.0;
+                        if ((mask >> (2 * h + side)) & 1u)
+                            acc = rim_sum<D>(g, tn, F1, scg, h, side, bx0, bx1, by0, by1, li, s, aux);
+                        else
+                        {
+                            const int2 ti = sIdx[2 * h + side];
+                            for (int e = ti.x; e < ti.x + ti.y; ++e)
+                            {
+                                const int sl = myslot[sU[e] * kT];
+                                const double v = sl >= 0 ? Fh[sl] : 0.0;
+                                acc = __dadd_rn(acc, __dmul_rn(sW[e], v));
+                            }
+                        }
+                        sum[side] = acc;
+                    }
+                    f[h] = __dadd_rn(Fh[s], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+                }
+            }
+            else if (gap == 0)
             {
                 // finest level: every table has at most one entry (E = {-eta}, A = {0});
                 // branch-free so all 2Q gathers are independent and in flight together
@@ -1393,6 +1446,7 @@ struct mrlbm_ctx {
     uint8_t* kind[kL]{};
     uint8_t* rn[kL]{};
     uint8_t* keep[kL]{};
+    unsigned* fbmd[kL]{};
     double* F[2][kL]{};
     int* tiles[kL]{};
     long long ntiles[kL]{};
@@ -1475,6 +1529,7 @@ Flags flags_of(mrlbm_ctx* c)
         f.kind[i] = c->kind[i];
         f.rn[i] = c->rn[i];
         f.keep[i] = c->keep[i];
+        f.fbm[i] = c->fbmd[i];
     }
     return f;
 }
@@ -1713,6 +1768,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             CU(cudaMalloc(&ctx->kind[li], n));
             CU(cudaMalloc(&ctx->rn[li], n));
             CU(cudaMalloc(&ctx->keep[li], n));
+            CU(cudaMalloc(&ctx->fbmd[li], sizeof(unsigned) * n));
             ctx->ntiles[li] = (n + kTile - 1) / kTile;
             CU(cudaMalloc(&ctx->tiles[li], sizeof(int) * 3 * ctx->ntiles[li]));
         }
@@ -2053,7 +2109,7 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
             nI += counts[li * 4 + 1];
             nG += counts[li * 4 + 2];
         }
-        stats->fallback_leaves = fb[0];
+        stats->fallback_leaves = fb[0] + fb[1];
         stats->kernel_launches = ctx->kernels_per_step * nsteps;
         stats->bytes_stream = 8LL * ctx->q * (2 * nS + nG);
         stats->leaf_updates = upd;
@@ -2171,6 +2227,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         cudaFree(ctx->kind[li]);
         cudaFree(ctx->rn[li]);
         cudaFree(ctx->keep[li]);
+        cudaFree(ctx->fbmd[li]);
         cudaFree(ctx->tiles[li]);
     }
     cudaFree(ctx->sch);

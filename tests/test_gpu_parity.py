@@ -49,3 +49,25 @@ def test_config2_blowup_same_step():
         return None
     kg, ko = first_fail(gpu), first_fail(ora)
     assert kg is not None and kg == ko
+
+
+def test_gpu_matches_golden_fixtures():
+    """GPU output on the committed oracle fixtures (tests/golden), bitwise."""
+    import os
+    from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    names = sorted(f for f in os.listdir(gdir) if f.endswith(".npz"))
+    assert names
+    for name in names:
+        data = np.load(os.path.join(gdir, name))
+        cid, J, eps, steps = int(data["cid"]), int(data["J"]), float(data["eps"]), int(data["steps"])
+        sc, rc = build_config(cid, J, eps)
+        s = Solver(sc, rc)
+        s.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(cid, sc, rc))
+        s.commit()
+        s.step(steps)
+        for lv in range(rc.j_min, rc.j_max + 1):
+            idx, f = s.read_leaves(lv)
+            assert np.array_equal(idx, data[f"idx{lv}"]), (name, lv)
+            assert np.array_equal(f.view(np.uint64), data[f"f{lv}"].view(np.uint64)), (name, lv)
+        s.close()
