@@ -136,6 +136,8 @@ int mrlbm_level_count(mrlbm_ctx* ctx, int level, int64_t* n);
 int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f);
 int mrlbm_set_profiling(mrlbm_ctx* ctx, int on);
 int mrlbm_set_graph(mrlbm_ctx* ctx, int on);
+/* per-kernel device times accumulated over profiled steps: lines "kernel level ms launches" */
+int mrlbm_profile_text(mrlbm_ctx* ctx, char* buf, int cap, int reset);
 void* mrlbm_stream_handle(mrlbm_ctx* ctx);   /* cudaStream_t of the context */
 int mrlbm_synchronize(mrlbm_ctx* ctx);
 const char* mrlbm_last_error(const mrlbm_ctx* ctx);

@@ -1037,7 +1037,7 @@ class Oracle {
                         {
                             // table exactness (Decision D.13): dependency cells inside
                             // (or periodic), parents of the level-(l+1) funnel not internal
-                            bool ok = true;
+                            bool dom_ok = true, par_ok = true;
                             for (const auto& o : tdep[g][h][side])
                             {
                                 Idx c = k;
@@ -1045,22 +1045,22 @@ class Oracle {
                                     c[a] += o[a];
                                 if (!inside_or_periodic(l, c))
                                 {
-                                    ok = false;
+                                    dom_ok = false;
                                     break;
                                 }
                             }
                             for (const auto& o : tpar[g][h][side])
                             {
-                                if (!ok)
+                                if (!dom_ok)
                                     break;
                                 Idx c = k;
                                 for (int a = 0; a < D; ++a)
                                     c[a] += o[a];
                                 if (L.ii.slot(wrapclamp(l, c)))
-                                    ok = false;
+                                    par_ok = false;
                             }
                             double s = 0.0;
-                            if (ok)
+                            if (dom_ok && (par_ok || g == 1))
                             {
                                 for (const auto& [off, w] : tables[g][h][side])
                                 {
@@ -1068,6 +1068,42 @@ class Oracle {
                                     for (int a = 0; a < D; ++a)
                                         c[a] += off[a];
                                     s += w * rec(l, wrapclamp(l, c), memo)[h];
+                                }
+                                if (!par_ok)
+                                {
+                                    // gap 1 with finer neighbours (Decision D.13b, "add
+                                    // the proper detail information"): the table sums the predicted
+                                    // rim values; add the detail of every rim cell that is a leaf
+                                    any_fb = true;
+                                    rim_cells(l, k, sc.eta[h], side, rim);
+                                    for (const auto& x : rim)
+                                    {
+                                        const Idx xc = wrapclamp(J1, x);
+                                        const double* v = value_R(J1, xc);
+                                        if (!v)
+                                            continue;
+                                        Idx p{};
+                                        std::array<int, D> delta{};
+                                        for (int a = 0; a < D; ++a)
+                                        {
+                                            p[a] = xc[a] >> 1;
+                                            delta[a] = static_cast<int>(xc[a] - 2 * p[a]);
+                                        }
+                                        std::vector<const double*> st(D == 1 ? 3 : 9);
+                                        for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
+                                        {
+                                            Idx cc = p;
+                                            if (D == 1)
+                                                cc[0] += o - 1;
+                                            else
+                                            {
+                                                cc[0] += o / 3 - 1;
+                                                cc[1] += o % 3 - 1;
+                                            }
+                                            st[o] = rec(l, wrapclamp(l, cc), memo);
+                                        }
+                                        s += v[h] - predict_from(st, delta, h);
+                                    }
                                 }
                             }
                             else

@@ -31,6 +31,7 @@ def lib():
         "mrlbm_read_leaves": (C.c_int, [vp, C.c_int, vp, vp]),
         "mrlbm_set_profiling": (C.c_int, [vp, C.c_int]),
         "mrlbm_set_graph": (C.c_int, [vp, C.c_int]),
+        "mrlbm_profile_text": (C.c_int, [vp, C.c_char_p, C.c_int, C.c_int]),
         "mrlbm_stream_handle": (vp, [vp]),
         "mrlbm_synchronize": (C.c_int, [vp]),
         "mrlbm_last_error": (C.c_char_p, [vp]),

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <climits>
 #include <cstring>
+#include <map>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -34,7 +35,7 @@ namespace mrlbm_b200 {
 constexpr int kL = MRLBM_MAX_LEVELS;
 constexpr int kQ = MRLBM_MAX_Q;
 
-enum : uint8_t { K_LEAF = 1, K_INT = 2, K_VIRT = 4, K_FB = 8 };
+enum : uint8_t { K_LEAF = 1, K_INT = 2, K_VIRT = 4, K_FB = 8, K_FBC = 16 };
 // fallback leaves with gap >= kDeepGap stream in the dedicated K8 kernel (long
 // serial rims, 2Q-way parallel per leaf); shallower ones inline in K7
 constexpr int kDeepGap = 1;
@@ -42,6 +43,7 @@ constexpr int kDeepGap = 1;
 struct Geo {
     int d, q, J0, J1, nlev, per0, per1;
     int nx[kL], ny[kL];
+    int lny[kL]; // log2(ny) when ny is a power of two, else -1
     long long cap[kL];
 };
 
@@ -78,6 +80,7 @@ struct Aux {
     int* fb_count;     // fallback leaves of the current step
     int2* fb_list;     // (level, lin)
     unsigned* fb_mask; // per fallback leaf: bit (2h + side) set = table not exact
+    unsigned* fb_dmask; // per fallback leaf: bit set = dependency leaves the domain
     long long fb_cap;
     long long* updates; // accumulated leaf updates
     const int2* tidx;   // [(g * q + h) * 2 + side] -> (start, count)
@@ -92,6 +95,7 @@ struct Aux {
     const int4* udep;   // [g] union of the dependency boxes
     const int2* upidx;  // [g] -> (start, count) into upar
     const int2* upar;   // [g] union of the parent sets
+    const int2* eta;    // [h] logical velocities (x, y)
 };
 
 // ---------------------------------------------------------------- helpers
@@ -112,6 +116,27 @@ __device__ __forceinline__ void lin2xy(int lin, int ny, int& x, int& y)
     {
         x = lin;
         y = 0;
+    }
+    else
+    {
+        x = lin / ny;
+        y = lin - x * ny;
+    }
+}
+
+// same with a shift when the row length is a power of two (all BASELINE configs)
+template <int D>
+__device__ __forceinline__ void lin2xy_l(int lin, int ny, int lny, int& x, int& y)
+{
+    if (D == 1)
+    {
+        x = lin;
+        y = 0;
+    }
+    else if (lny >= 0)
+    {
+        x = lin >> lny;
+        y = lin & (ny - 1);
     }
     else
     {
@@ -185,7 +210,7 @@ __global__ void k_project(Geo g, Tree t, Fld F, int m, Aux aux)
     GRID_STRIDE(s, nL, nL + nI)
     {
         int px, py;
-        lin2xy<D>(t.cells[m - g.J0][s], ny, px, py);
+        lin2xy_l<D>(t.cells[m - g.J0][s], ny, g.lny[li], px, py);
         int cs[1 << D];
         bool ok = true;
         for (int c = 0; c < (1 << D); ++c)
@@ -230,7 +255,7 @@ __global__ void k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, i
     {
         const int plin = t.cells[li][s];
         int px, py;
-        lin2xy<D>(plin, ny, px, py);
+        lin2xy_l<D>(plin, ny, g.lny[li], px, py);
         constexpr int NS = D == 1 ? 3 : 9;
         int st[NS];
         bool ok = true;
@@ -298,7 +323,7 @@ __global__ void k_closure(Geo g, Tree t, Flags fl, int m)
         if (!fl.keep[li][plin])
             continue;
         int px, py;
-        lin2xy<D>(plin, ny, px, py);
+        lin2xy_l<D>(plin, ny, g.lny[li], px, py);
         fl.keep[li - 1][xy2lin<D>(px >> 1, py >> 1, nyp)] = 1;
     }
 }
@@ -318,7 +343,7 @@ __global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, int m)
             continue;
         fl.rn[li][plin] = 1;
         int px, py;
-        lin2xy<D>(plin, ny, px, py);
+        lin2xy_l<D>(plin, ny, g.lny[li], px, py);
         for (int c = 0; c < (1 << D); ++c)
         {
             const int cx = 2 * px + (D == 1 ? c : (c >> 1)), cy = D == 1 ? 0 : 2 * py + (c & 1);
@@ -354,7 +379,7 @@ __global__ void k_grade(Geo g, Flags fl, int m)
         if (!fl.rn[li][i])
             continue;
         int px, py;
-        lin2xy<D>((int)i, ny, px, py);
+        lin2xy_l<D>((int)i, ny, g.lny[li], px, py);
         for (int ox = -1; ox <= 1; ++ox)
             for (int oy = (D == 1 ? 0 : -1); oy <= (D == 1 ? 0 : 1); ++oy)
             {
@@ -381,7 +406,7 @@ __global__ void k_kinds(Geo g, Flags fl, int m)
     GRID_STRIDE(i, 0, n)
     {
         int x, y;
-        lin2xy<D>((int)i, ny, x, y);
+        lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
         const bool inR = (m == g.J0) || fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, nyp)];
         const bool ref = (m < g.J1) && fl.rn[li][i];
         fl.kind[li][i] = inR ? (ref ? K_INT : K_LEAF) : 0;
@@ -392,78 +417,6 @@ __global__ void k_kinds(Geo g, Flags fl, int m)
 // zero-detail recursion touches lie in the domain (or periodic) and the parents of
 // the level-(l+1) cells it touches are not internal.  A leaf is a fallback leaf if
 // any pair fails: tested here on the union over pairs (equivalent for "any").
-template <int D>
-__global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
-{
-    const int li = m - g.J0;
-    const int gap = g.J1 - m;
-    const int nx = g.nx[li], ny = g.ny[li];
-    const long long n = (long long)nx * ny;
-    const int4 ub = aux.udep[gap];
-    const int2 pi = aux.upidx[gap];
-    GRID_STRIDE(i, 0, n)
-    {
-        if (fl.kind[li][i] != K_LEAF)
-            continue;
-        int x, y;
-        lin2xy<D>((int)i, ny, x, y);
-        bool fb = (!g.per0 && (x + ub.x < 0 || x + ub.y >= nx)) ||
-                  (D == 2 && !g.per1 && (y + ub.z < 0 || y + ub.w >= ny));
-        for (int e = pi.x; e < pi.x + pi.y && !fb; ++e)
-        {
-            const int2 o = aux.upar[e];
-            int xx = x + o.x, yy = y + o.y;
-            if (xx < 0 || xx >= nx || (D == 2 && (yy < 0 || yy >= ny)))
-            {
-                if ((!g.per0 && (xx < 0 || xx >= nx)) || (D == 2 && !g.per1 && (yy < 0 || yy >= ny)))
-                    continue; // outside a non-periodic wall: covered by the domain test
-                xx = mr_coord(xx, nx, 1);
-                if (D == 2)
-                    yy = mr_coord(yy, ny, 1);
-            }
-            if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
-                fb = true;
-        }
-        if (fb)
-        {
-            // exact per-(population, side) mask of the pairs whose table is not exact
-            unsigned mask = 0;
-            for (int pair = 0; pair < 2 * g.q; ++pair)
-            {
-                const int key = gap * 2 * g.q + pair;
-                const int4 db = aux.tdep[key];
-                bool ok = !((!g.per0 && (x + db.x < 0 || x + db.y >= nx)) ||
-                            (D == 2 && !g.per1 && (y + db.z < 0 || y + db.w >= ny)));
-                const int2 pp = aux.tpidx[key];
-                for (int k = pp.x; k < pp.x + pp.y && ok; ++k)
-                {
-                    const int2 o = aux.tpar[k];
-                    if (fl.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)] & K_INT)
-                        ok = false;
-                }
-                if (!ok)
-                    mask |= 1u << pair;
-            }
-            fl.kind[li][i] = K_LEAF | K_FB;
-            fl.fbm[li][i] = mask;
-            if (gap > 0)
-            {
-                // listed for the reconstruction band (and K8 when gap >= kDeepGap)
-                const int k = atomicAdd(aux.fb_count, 1);
-                if (k < aux.fb_cap)
-                {
-                    aux.fb_list[k] = make_int2(m, (int)i);
-                    aux.fb_mask[k] = mask;
-                }
-                else
-                    flag_err(aux.err, 2);
-            }
-            else
-                atomicAdd(aux.fb_count + 1, 1);
-        }
-    }
-}
-
 // Mark the reconstruction band of every fallback leaf at every finer level as
 // virtual (materialised zero-detail reconstruction): a ring of width W on both
 // sides of the leaf boundary, W = 2 below the finest level (stencils of the
@@ -532,7 +485,9 @@ __global__ void __launch_bounds__(256) k_band(Geo g, Flags fl, Aux aux)
         if (l == g.J1)
             continue;
         int kx, ky;
-        lin2xy<D>(e.y, g.ny[l - g.J0], kx, ky);
+        lin2xy_l<D>(e.y, g.ny[l - g.J0], g.lny[l - g.J0], kx, ky);
+        if (l == g.J1 - 1)
+            continue; // gap 1: rim values are predicted on the fly from level J1-1 (rim_value)
         for (int m = l + 1; m <= g.J1; ++m)
         {
             const int li = m - g.J0;
@@ -571,7 +526,7 @@ __global__ void k_ghost_rows(Geo g, Flags fl, int m, uint8_t* tmp)
     GRID_STRIDE(i, 0, n)
     {
         int x, y;
-        lin2xy<D>((int)i, ny, x, y);
+        lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
         uint8_t r = 0;
 #pragma unroll
         for (int oy = -2; oy <= 2; ++oy)
@@ -600,7 +555,7 @@ __global__ void k_ghost(Geo g, Flags fl, int m, const uint8_t* tmp)
         if (fl.kind[li][i] != 0)
             continue;
         int x, y;
-        lin2xy<D>((int)i, ny, x, y);
+        lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
         bool near = false;
 #pragma unroll
         for (int ox = -2; ox <= 2; ++ox)
@@ -619,6 +574,237 @@ __global__ void k_ghost(Geo g, Flags fl, int m, const uint8_t* tmp)
         }
         if (near)
             fl.kind[li][i] = K_VIRT;
+    }
+}
+
+// ---- vectorised dense passes (2D levels with ny % 16 == 0): 16 cells per thread
+// per iteration with 16-byte loads, so sparse levels cost one load per 16 cells.
+// Same results as the scalar kernels above.
+#define CHUNK_STRIDE(c, nchunks)                                                                            \
+    for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < (nchunks);                    \
+         c += (long long)gridDim.x * blockDim.x)
+
+union V16 {
+    uint4 v;
+    uint8_t b[16];
+};
+
+__global__ void k_kinds_v(Geo g, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int ny = g.ny[li], nyp = li > 0 ? g.ny[li - 1] : 1;
+    const long long nch = (long long)g.nx[li] * ny / 16;
+    const uint8_t* rn = fl.rn[li];
+    const uint8_t* rnp = li > 0 ? fl.rn[li - 1] : nullptr;
+    const bool top = m == g.J0, fin = m == g.J1;
+    CHUNK_STRIDE(c, nch)
+    {
+        const int lin0 = (int)(c * 16);
+        const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
+        V16 r, o;
+        r.v = fin ? make_uint4(0, 0, 0, 0) : reinterpret_cast<const uint4*>(rn)[c];
+        uint2 pr = make_uint2(0, 0);
+        if (!top)
+            pr = *reinterpret_cast<const uint2*>(rnp + (long long)(x >> 1) * nyp + (y0 >> 1));
+        const uint8_t* pb = reinterpret_cast<const uint8_t*>(&pr);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+        {
+            const bool inR = top || pb[j >> 1];
+            o.b[j] = inR ? (r.b[j] ? K_INT : K_LEAF) : 0;
+        }
+        reinterpret_cast<uint4*>(fl.kind[li])[c] = o.v;
+    }
+}
+
+// fallback flags: chunks without a plain leaf are skipped with one load
+template <int D>
+__device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int m, int li, int gap, long long i, int x,
+                                              int y, const int4& ub, const int2& pi, Aux& aux)
+{
+    const int nx = g.nx[li], ny = g.ny[li];
+    bool fb = (!g.per0 && (x + ub.x < 0 || x + ub.y >= nx)) || (D == 2 && !g.per1 && (y + ub.z < 0 || y + ub.w >= ny));
+    for (int e = pi.x; e < pi.x + pi.y && !fb; ++e)
+    {
+        const int2 o = aux.upar[e];
+        int xx = x + o.x, yy = y + o.y;
+        if (xx < 0 || xx >= nx || (D == 2 && (yy < 0 || yy >= ny)))
+        {
+            if ((!g.per0 && (xx < 0 || xx >= nx)) || (D == 2 && !g.per1 && (yy < 0 || yy >= ny)))
+                continue;
+            xx = mr_coord(xx, nx, 1);
+            if (D == 2)
+                yy = mr_coord(yy, ny, 1);
+        }
+        if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
+            fb = true;
+    }
+    if (!fb)
+        return;
+    unsigned mask = 0, dmask = 0;
+    for (int pair = 0; pair < 2 * g.q; ++pair)
+    {
+        const int key = gap * 2 * g.q + pair;
+        const int4 db = aux.tdep[key];
+        const bool dom = !((!g.per0 && (x + db.x < 0 || x + db.y >= nx)) || (D == 2 && !g.per1 && (y + db.z < 0 || y + db.w >= ny)));
+        bool ok = dom;
+        const int2 pp = aux.tpidx[key];
+        for (int k = pp.x; k < pp.x + pp.y && ok; ++k)
+        {
+            const int2 o = aux.tpar[k];
+            if (fl.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)] & K_INT)
+                ok = false;
+        }
+        if (!ok)
+            mask |= 1u << pair;
+        if (!dom)
+            dmask |= 1u << pair;
+    }
+    fl.fbm[li][i] = mask;
+    fl.kind[li][i] = K_LEAF | K_FB;
+    if (gap > 0)
+    {
+        const int k = atomicAdd(aux.fb_count, 1);
+        if (k < aux.fb_cap)
+        {
+            aux.fb_list[k] = make_int2(m, (int)i);
+            aux.fb_mask[k] = mask;
+            aux.fb_dmask[k] = dmask;
+        }
+        else
+            flag_err(aux.err, 2);
+    }
+    else
+        atomicAdd(aux.fb_count + 1, 1);
+}
+
+template <int D>
+__global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int gap = g.J1 - m;
+    const int ny = g.ny[li];
+    const long long n = (long long)g.nx[li] * ny;
+    const int4 ub = aux.udep[gap];
+    const int2 pi = aux.upidx[gap];
+    GRID_STRIDE(i, 0, n)
+    {
+        if (fl.kind[li][i] != K_LEAF)
+            continue;
+        int x, y;
+        lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
+        fallback_cell<D>(g, fl, m, li, gap, i, x, y, ub, pi, aux);
+    }
+}
+
+__global__ void k_fallback_v(Geo g, Flags fl, int m, Aux aux)
+{
+    const int li = m - g.J0;
+    const int gap = g.J1 - m;
+    const int ny = g.ny[li];
+    const long long nch = (long long)g.nx[li] * ny / 16;
+    const int4 ub = aux.udep[gap];
+    const int2 pi = aux.upidx[gap];
+    CHUNK_STRIDE(c, nch)
+    {
+        V16 k;
+        k.v = reinterpret_cast<const uint4*>(fl.kind[li])[c];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            any = any || k.b[j] == K_LEAF;
+        if (!any)
+            continue;
+        const int lin0 = (int)(c * 16);
+        const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
+        for (int j = 0; j < 16; ++j)
+            if (k.b[j] == K_LEAF)
+                fallback_cell<2>(g, fl, m, li, gap, lin0 + j, x, y0 + j, ub, pi, aux);
+    }
+}
+
+// ghost rows: tmp = OR of R membership over y +- 2 (same row)
+__global__ void k_ghost_rows_v(Geo g, Flags fl, int m, uint8_t* tmp)
+{
+    const int li = m - g.J0;
+    const int ny = g.ny[li];
+    const long long nch = (long long)g.nx[li] * ny / 16;
+    const uint8_t* kind = fl.kind[li];
+    CHUNK_STRIDE(c, nch)
+    {
+        const int lin0 = (int)(c * 16);
+        const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
+        V16 k, o;
+        k.v = reinterpret_cast<const uint4*>(kind)[c];
+        uint8_t w[20];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            w[j + 2] = k.b[j] & (K_LEAF | K_INT);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+        {
+            int yl = y0 - 2 + j, yr = y0 + 16 + j;
+            uint8_t vl = 0, vr = 0;
+            if (yl >= 0 || g.per1)
+                vl = kind[(long long)x * ny + mr_coord(yl, ny, 1)] & (K_LEAF | K_INT);
+            if (yr < ny || g.per1)
+                vr = kind[(long long)x * ny + mr_coord(yr, ny, 1)] & (K_LEAF | K_INT);
+            w[j] = vl;
+            w[18 + j] = vr;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            o.b[j] = w[j] | w[j + 1] | w[j + 2] | w[j + 3] | w[j + 4];
+        reinterpret_cast<uint4*>(tmp)[c] = o.v;
+    }
+}
+
+// ghosts: empty cells with an R cell within +-2 rows of tmp
+__global__ void k_ghost_v(Geo g, Flags fl, int m, const uint8_t* tmp)
+{
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li];
+    const long long nch = (long long)nx * ny / 16;
+    const int cpr = ny / 16; // chunks per row
+    CHUNK_STRIDE(c, nch)
+    {
+        V16 k;
+        k.v = reinterpret_cast<const uint4*>(fl.kind[li])[c];
+        bool any = false;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            any = any || k.b[j] == 0;
+        if (!any)
+            continue;
+        const int x = (int)(c / cpr), cy = (int)(c - (long long)x * cpr);
+        V16 acc;
+        acc.v = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int ox = -2; ox <= 2; ++ox)
+        {
+            int xx = x + ox;
+            if (xx < 0 || xx >= nx)
+            {
+                if (!g.per0)
+                    continue;
+                xx = mr_coord(xx, nx, 1);
+            }
+            const uint4 t = reinterpret_cast<const uint4*>(tmp)[(long long)xx * cpr + cy];
+            acc.v.x |= t.x;
+            acc.v.y |= t.y;
+            acc.v.z |= t.z;
+            acc.v.w |= t.w;
+        }
+        bool chg = false;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (k.b[j] == 0 && acc.b[j])
+            {
+                k.b[j] = K_VIRT;
+                chg = true;
+            }
+        if (chg)
+            reinterpret_cast<uint4*>(fl.kind[li])[c] = k.v;
     }
 }
 
@@ -782,7 +968,7 @@ __global__ void k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux a
             continue;
         }
         int x, y;
-        lin2xy<D>(lin, ny, x, y);
+        lin2xy_l<D>(lin, ny, g.lny[li], x, y);
         const int px = x >> 1, py = y >> 1, dx = x & 1, dy = y & 1;
         constexpr int NS = D == 1 ? 3 : 9;
         int st[NS];
@@ -822,7 +1008,7 @@ __global__ void k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
     {
         const int lin = tn.cells[li][s];
         int x, y;
-        lin2xy<D>(lin, ny, x, y);
+        lin2xy_l<D>(lin, ny, g.lny[li], x, y);
         const int px = x >> 1, py = y >> 1, dx = x & 1, dy = y & 1;
         constexpr int NS = D == 1 ? 3 : 9;
         int st[NS];
@@ -948,12 +1134,27 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
     if (face < 0)
     {
         const int sl = tn.map[lj][mr_lin<D>(g, g.J1, x, y)];
-        if (sl < 0)
+        if (sl >= 0)
+            return F1.f[lj][(long long)h * g.cap[lj] + sl];
+        // not materialised (rims of gap-1 leaves): one zero-detail prediction from
+        // level J1-1, same operands and order as k_virtual would use
+        const int lp = lj - 1;
+        const int xc = mr_coord(x, nx, g.per0), yc = D == 2 ? mr_coord(y, ny, g.per1) : 0;
+        const int px = xc >> 1, py = yc >> 1;
+        constexpr int NS = D == 1 ? 3 : 9;
+        double sv[NS];
+        for (int o = 0; o < NS; ++o)
         {
-            flag_err(aux.err, 0);
-            return 0.0;
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            const int ps = tn.map[lp][mr_lin<D>(g, g.J1 - 1, px + ox, py + oy)];
+            if (ps < 0)
+            {
+                flag_err(aux.err, 0);
+                return 0.0;
+            }
+            sv[o] = F1.f[lp][(long long)h * g.cap[lp] + ps];
         }
-        return F1.f[lj][(long long)h * g.cap[lj] + sl];
+        return mr_predict<D>(sv, xc & 1, yc & 1);
     }
     const int kind = sc->bc_kind[face];
     if (kind == MRLBM_BC_COPY)
@@ -1051,9 +1252,10 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
     {
         const int it = (int)(t / q), h = (int)(t % q);
         const int2 e = aux.fb_list[it];
-        if (g.J1 - e.x < kDeepGap)
-            continue; // streamed inline by K7
+        if (g.J1 - e.x < 2)
+            continue; // gap 1: k_stream_fb1
         const unsigned mask = aux.fb_mask[it];
+        const unsigned dmask = aux.fb_dmask[it];
         const int m = e.x, li = m - g.J0;
         const long long slot = tn.map[li][e.y];
         if (slot < 0)
@@ -1064,7 +1266,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
         const int ny = g.ny[li];
         const long long cap = g.cap[li];
         int x, y;
-        lin2xy<D>(e.y, ny, x, y);
+        lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
         const int gap = g.J1 - m;
         double sums[2];
         for (int side = 0; side < 2; ++side)
@@ -1073,7 +1275,8 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
             (void)key;
             const bool ok = ((mask >> (2 * h + side)) & 1u) == 0;
             double acc = 0.0;
-            if (ok)
+            const bool corr = !ok && gap == 1 && !((dmask >> (2 * h + side)) & 1u);
+            if (ok || corr)
             {
                 const int2 ti = aux.tidx[key];
                 for (int k = ti.x; k < ti.x + ti.y; ++k)
@@ -1088,7 +1291,37 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
                     acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + sl]));
                 }
             }
-            else
+            if (corr)
+            {
+                // Decision D.13b: add the details of the rim cells that are leaves
+                const int lj = li + 1;
+                const int nyj = g.ny[lj], nLj = tn.cnt[lj * 4 + 0];
+                const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
+                const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
+                for (int xr = bx0 - 1; xr <= bx1; ++xr)
+                    for (int yr = (D == 1 ? 0 : by0 - 1); yr <= (D == 1 ? 0 : by1); ++yr)
+                    {
+                        const bool inb = in_box<D>(xr, yr, bx0, bx1, by0, by1);
+                        const bool ine = in_box<D>(xr + ex, yr + ey, bx0, bx1, by0, by1);
+                        if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
+                            continue;
+                        const int xc = mr_coord(xr, g.nx[lj], g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
+                        const int sj = tn.map[lj][xy2lin<D>(xc, yc, nyj)];
+                        if (sj < 0 || sj >= nLj)
+                            continue;
+                        constexpr int NS = D == 1 ? 3 : 9;
+                        double sv[NS];
+                        for (int o = 0; o < NS; ++o)
+                        {
+                            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+                            const int ps = tn.map[li][mr_lin<D>(g, m, (xc >> 1) + ox, (yc >> 1) + oy)];
+                            sv[o] = ps >= 0 ? F1.f[li][(long long)h * cap + ps] : 0.0;
+                        }
+                        acc = __dadd_rn(acc, __dsub_rn(F1.f[lj][(long long)h * g.cap[lj] + sj],
+                                                       mr_predict<D>(sv, xc & 1, yc & 1)));
+                    }
+            }
+            if (!ok && !corr)
             {
                 const int side_n = 1 << gap;
                 const int bx0 = x * side_n, bx1 = bx0 + side_n;
@@ -1100,6 +1333,134 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
         const double scale = ldexp(1.0, D * (m - g.J1));
         const long long o = (long long)h * cap + slot;
         F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+    }
+}
+
+// Gap-1 fallback leaves, one thread per leaf.  The leaf's 5^D level-l slots and
+// the 4^D finest-level cells around its 2^D children are looked up once into shared
+// memory; then every (population, side) pair is summed from the cache: the
+// flattened table when exact, the table plus the details of the leaf rim cells
+// when only finer neighbours break it (Decision D.13b), else the boundary rim
+// (rim_sum).  Writes post-stream populations into F0; K7 collides them.
+template <int D>
+__global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld F1, const SchemeDev* sc, Aux aux)
+{
+    constexpr int kB = D == 1 ? 5 : 25;   // level-l box
+    constexpr int kR = D == 1 ? 4 : 16;   // finest-level 4^D box around the children
+    constexpr int kT = 128;
+    __shared__ int sBox[kB][kT];
+    __shared__ int sRim[kR][kT];
+    const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
+    const int q = g.q;
+    const int m = g.J1 - 1, li = m - g.J0, lj = li + 1;
+    if (li < 0)
+        return;
+    const int nx = g.nx[li], ny = g.ny[li], nxj = g.nx[lj], nyj = g.ny[lj];
+    const long long cap = g.cap[li], capj = g.cap[lj];
+    const int nLj = tn.cnt[lj * 4 + 0];
+    const double scale = ldexp(1.0, D * (m - g.J1));
+    const int gap = 1;
+    GRID_STRIDE(it, 0, nfb)
+    {
+        const int2 e = aux.fb_list[it];
+        if (e.x != m)
+            continue;
+        const unsigned mask = aux.fb_mask[it], dmask = aux.fb_dmask[it];
+        const long long slot = tn.map[li][e.y];
+        if (slot < 0)
+        {
+            flag_err(aux.err, 2);
+            continue;
+        }
+        int x, y;
+        lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
+        for (int b = 0; b < kB; ++b)
+        {
+            const int ox = D == 1 ? b - 2 : b / 5 - 2, oy = D == 1 ? 0 : b % 5 - 2;
+            int xx = x + ox, yy = y + oy;
+            bool in = true;
+            if (g.per0)
+                xx = mr_coord(xx, nx, 1);
+            else
+                in = xx >= 0 && xx < nx;
+            if (D == 2)
+            {
+                if (g.per1)
+                    yy = mr_coord(yy, ny, 1);
+                else
+                    in = in && yy >= 0 && yy < ny;
+            }
+            // clamped slot for out-of-domain stencil cells (MR boundary rule, D.8)
+            sBox[b][threadIdx.x] = tn.map[li][in ? xy2lin<D>(xx, yy, ny) : mr_lin<D>(g, m, x + ox, y + oy)];
+        }
+        for (int r = 0; r < kR; ++r)
+        {
+            const int rx = 2 * x - 1 + (D == 1 ? r : r / 4), ry = D == 1 ? 0 : 2 * y - 1 + r % 4;
+            bool in = (g.per0 || (rx >= 0 && rx < nxj)) && (D == 1 || g.per1 || (ry >= 0 && ry < nyj));
+            sRim[r][threadIdx.x] = in ? tn.map[lj][mr_lin<D>(g, g.J1, rx, ry)] : -1;
+        }
+        for (int h = 0; h < q; ++h)
+        {
+            const double* Fh = F1.f[li] + (long long)h * cap;
+            const double* Fj = F1.f[lj] + (long long)h * capj;
+            const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
+            double sum[2];
+            for (int side = 0; side < 2; ++side)
+            {
+                const int pair = 2 * h + side;
+                const bool ok = !((mask >> pair) & 1u);
+                const bool dom_bad = (dmask >> pair) & 1u;
+                double acc = 0.0;
+                if (!dom_bad)
+                {
+                    const int2 ti = aux.tidx[(gap * q + h) * 2 + side];
+                    for (int k = ti.x; k < ti.x + ti.y; ++k)
+                    {
+                        const int2 o = aux.toff[k];
+                        const int b = D == 1 ? o.x + 2 : (o.x + 2) * 5 + (o.y + 2);
+                        const int sl = sBox[b][threadIdx.x];
+                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], sl >= 0 ? Fh[sl] : 0.0));
+                    }
+                    if (!ok)
+                    {
+                        // Decision D.13b: + details of the rim cells that are finest leaves
+                        for (int r = 0; r < kR; ++r)
+                        {
+                            const int dx = D == 1 ? r : r / 4, dy = D == 1 ? 0 : r % 4;
+                            const int xr = 2 * x - 1 + dx, yr = D == 1 ? 0 : 2 * y - 1 + dy;
+                            const bool inb = dx >= 1 && dx <= 2 && (D == 1 || (dy >= 1 && dy <= 2));
+                            const bool ine = (dx + ex) >= 1 && (dx + ex) <= 2 && (D == 1 || ((dy + ey) >= 1 && (dy + ey) <= 2));
+                            if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
+                                continue;
+                            const int sj = sRim[r][threadIdx.x];
+                            if (sj < 0 || sj >= nLj)
+                                continue;
+                            const int xc = mr_coord(xr, nxj, g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
+                            // parent offset from the leaf: ((xc >> 1) - x) in {-1, 0, 1} modulo wrap
+                            const int pdx = (dx + 1) / 2 - 1, pdy = D == 1 ? 0 : (dy + 1) / 2 - 1;
+                            constexpr int NS = D == 1 ? 3 : 9;
+                            double sv[NS];
+                            for (int o = 0; o < NS; ++o)
+                            {
+                                const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+                                const int b = D == 1 ? pdx + ox + 2 : (pdx + ox + 2) * 5 + (pdy + oy + 2);
+                                const int ps = sBox[b][threadIdx.x];
+                                sv[o] = ps >= 0 ? Fh[ps] : 0.0;
+                            }
+                            acc = __dadd_rn(acc, __dsub_rn(Fj[sj], mr_predict<D>(sv, xc & 1, yc & 1)));
+                        }
+                    }
+                }
+                else
+                {
+                    const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
+                    acc = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, slot, aux);
+                }
+                sum[side] = acc;
+            }
+            const long long o = (long long)h * cap + slot;
+            F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+        }
     }
 }
 
@@ -1120,6 +1481,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
     __shared__ int sNU;
     __shared__ int sSlot[kU][kT];        // per-thread neighbour slots
     __shared__ double sFeq[Q];
+    __shared__ int2 sEta[Q];
     const int gap = g.J1 - m;
     for (int i = threadIdx.x; i < Q * BS; i += blockDim.x)
     {
@@ -1132,6 +1494,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
     {
         sS[i] = scg->s[i];
         sFeq[i] = scg->obs_feq[i];
+        sEta[i] = make_int2(scg->eta[i][0], scg->eta[i][1]);
     }
     if (threadIdx.x < 8)
         sP[threadIdx.x] = scg->eqp[threadIdx.x];
@@ -1171,9 +1534,11 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
     GRID_STRIDE(s, 0, nL)
     {
         const int lin = tn.cells[li][s];
-        const bool fb = (fl.kind[li][lin] & K_FB) != 0;
+        const uint8_t kd = fl.kind[li][lin];
+        const bool fb = (kd & K_FB) != 0;
+        const bool fbc = (kd & K_FBC) != 0;
         double f[Q];
-        if (fb && gap >= kDeepGap)
+        if (fb && !fbc && gap >= kDeepGap)
         {
             // deep-gap fallback leaf: post-stream populations from K8
 #pragma unroll
@@ -1183,7 +1548,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
         else
         {
             int x, y;
-            lin2xy<D>(lin, ny, x, y);
+            lin2xy_l<D>(lin, ny, g.lny[li], x, y);
             // all neighbour slots first (independent loads), then pure gathers
             for (int u = 0; u < nu; ++u)
             {
@@ -1318,7 +1683,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
             {
                 // config 5 volume-fraction blend
                 int x, y;
-                lin2xy<D>(lin, ny, x, y);
+                lin2xy_l<D>(lin, ny, g.lny[li], x, y);
                 const double dx = ldexp(1.0, -m);
                 const double ox = scg->origin[0], oy = scg->origin[1];
                 const double cx = scg->obs_c[0], cy = scg->obs_c[1], r = scg->obs_r;
@@ -1390,7 +1755,7 @@ __global__ void k_load_mark(Geo g, Flags fl, const int* lins, int n, int m)
         if (m > g.J0)
         {
             int x, y;
-            lin2xy<D>(lin, ny, x, y);
+            lin2xy_l<D>(lin, ny, g.lny[li], x, y);
             fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, g.ny[li - 1])] = 1;
         }
     }
@@ -1407,7 +1772,7 @@ __global__ void k_closure_dense(Geo g, Flags fl, int m)
         if (!fl.rn[li][i])
             continue;
         int x, y;
-        lin2xy<D>((int)i, ny, x, y);
+        lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
         fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, g.ny[li - 1])] = 1;
     }
 }
@@ -1455,6 +1820,7 @@ struct mrlbm_ctx {
     int* fbc = nullptr;
     int2* fbl = nullptr;
     unsigned* fbm = nullptr;
+    unsigned* fbdm = nullptr;
     long long fbcap = 0;
     long long* upd = nullptr;
     int2* tidx = nullptr;
@@ -1469,6 +1835,7 @@ struct mrlbm_ctx {
     uint8_t* tu = nullptr;
     int2* upidx = nullptr;
     int2* upar = nullptr;
+    int2* etad = nullptr;
     int cur = 0;
     bool committed = false;
     bool profiling = false;
@@ -1482,6 +1849,11 @@ struct mrlbm_ctx {
     int grid_cap = 148 * 8;
     long long kernels_per_step = 0; // counted while enqueueing one step
     long long kcount = 0;
+    // per-launch timing (profiling mode only): event after every kernel
+    std::vector<cudaEvent_t> kev;
+    std::vector<std::pair<std::string, int>> klabel;
+    std::map<std::pair<std::string, int>, std::pair<double, int>> kacc;
+    int kn = 0;
 };
 
 namespace {
@@ -1541,6 +1913,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.fb_count = c->fbc;
     a.fb_list = c->fbl;
     a.fb_mask = c->fbm;
+    a.fb_dmask = c->fbdm;
     a.fb_cap = c->fbcap;
     a.updates = c->upd;
     a.tidx = c->tidx;
@@ -1555,6 +1928,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.tu = c->tu;
     a.upidx = c->upidx;
     a.upar = c->upar;
+    a.eta = c->etad;
     return a;
 }
 
@@ -1568,6 +1942,8 @@ int grid_for(mrlbm_ctx* c, long long n, int threads = 256)
     return static_cast<int>(b);
 }
 
+void kmark(mrlbm_ctx* c, const char* name, int level);
+
 template <int D>
 void launch_compaction(mrlbm_ctx* c, int v, int m)
 {
@@ -1576,9 +1952,28 @@ void launch_compaction(mrlbm_ctx* c, int v, int m)
     const long long n = c->geo.cap[li];
     const int nt = static_cast<int>(c->ntiles[li]);
     k_tile_count<<<nt, kTileThreads, 0, c->stream>>>(c->kind[li], n, c->tiles[li]);
+    kmark(c, "k_tile_count", m);
     k_tile_scan<<<1, 1024, 0, c->stream>>>(c->tiles[li], nt, c->cnt[v] + li * 4);
+    kmark(c, "k_tile_scan", m);
     k_tile_scatter<<<nt, kTileThreads, 0, c->stream>>>(c->kind[li], n, c->tiles[li], c->cnt[v] + li * 4, c->map[v][li],
                                                        c->cells[v][li]);
+    kmark(c, "k_tile_scatter", m);
+}
+
+void kmark(mrlbm_ctx* c, const char* name, int level)
+{
+    if (!c->profiling)
+        return;
+    if (c->kn >= static_cast<int>(c->kev.size()))
+    {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->kev.push_back(e);
+        c->klabel.emplace_back();
+    }
+    cudaEventRecord(c->kev[c->kn], c->stream);
+    c->klabel[c->kn] = {name, level};
+    ++c->kn;
 }
 
 void phase_mark(mrlbm_ctx* c, int k)
@@ -1599,6 +1994,7 @@ void enqueue_step(mrlbm_ctx* c)
     cudaStream_t s = c->stream;
     const int T = 256;
     c->kcount = 0;
+    c->kn = 0;
     for (int li = 0; li < c->nlev; ++li)
     {
         cudaMemsetAsync(c->keep[li], 0, g.cap[li], s);
@@ -1608,48 +2004,74 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 0);
     // K1 projection of the old tree (bottom-up)
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux); }
+        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux);  kmark(c, "k_project", m); }
     phase_mark(c, 1);
     // K2 details + flags
     for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_details<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux); }
+        { c->kcount++; k_details<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux);  kmark(c, "k_details", m); }
     phase_mark(c, 2);
     // K3 closure, enlargement, grading
     for (int m = c->J1 - 1; m > c->J0; --m)
-        { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m); }
+        { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);  kmark(c, "k_closure", m); }
     for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m); }
+        { c->kcount++; k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m);  kmark(c, "k_enlarge", m); }
     for (int m = c->J1 - 1; m > c->J0; --m)
-        { c->kcount++; k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m); }
+        { c->kcount++; k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);  kmark(c, "k_grade", m); }
     phase_mark(c, 3);
     // K4 kinds, fallback flags, reconstruction bands, ghosts, compaction
-    for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_kinds<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m); }
-    for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux); }
-    { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux); }
+    auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
     for (int m = c->J0; m <= c->J1; ++m)
     {
+        c->kcount++;
+        if (vec_ok(m))
+            k_kinds_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m);
+        else
+            k_kinds<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+        kmark(c, "k_kinds", m);
+    }
+    for (int m = c->J0; m <= c->J1; ++m)
+    {
+        c->kcount++;
+        if (vec_ok(m))
+            k_fallback_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m, aux);
+        else
+            k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux);
+        kmark(c, "k_fallback", m);
+    }
+    { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);  kmark(c, "k_band", -1); }
+    for (int m = c->J0; m <= c->J1; ++m)
+    {
+        uint8_t* tmp = c->keep[m - c->J0];
+        if (vec_ok(m))
+        {
+            c->kcount += 2;
+            k_ghost_rows_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m, tmp);
+            kmark(c, "k_ghost_rows_v", m);
+            k_ghost_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m, tmp);
+            kmark(c, "k_ghost_v", m);
+            continue;
+        }
         if (D == 2)
-            { c->kcount++; k_ghost_rows<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, c->keep[m - c->J0]); }
-        { c->kcount++; k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, c->keep[m - c->J0]); }
+            { c->kcount++; k_ghost_rows<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, tmp);  kmark(c, "k_ghost_rows", m); }
+        { c->kcount++; k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, tmp);  kmark(c, "k_ghost", m); }
     }
     for (int m = c->J0; m <= c->J1; ++m)
         launch_compaction<D>(c, n, m);
     phase_mark(c, 4);
     // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_transfer<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux); }
+        { c->kcount++; k_transfer<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux);  kmark(c, "k_transfer", m); }
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux); }
+        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_project", m); }
     for (int m = c->J0 + 1; m <= c->J1; ++m)
-        { c->kcount++; k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux); }
+        { c->kcount++; k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_virtual", m); }
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
-    { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux); }
+    { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
+    { c->kcount++; k_stream_fb1<D><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, F0, F1, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_stream_collide<D, Q, BS, EQ><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux); }
-    { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd); }
+        { c->kcount++; k_stream_collide<D, Q, BS, EQ><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux);  kmark(c, "k_stream_collide", m); }
+    { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
     phase_mark(c, 6);
     c->kernels_per_step = c->kcount;
 }
@@ -1731,6 +2153,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         }
         g.nx[li] = static_cast<int>(nx);
         g.ny[li] = static_cast<int>(ny);
+        g.lny[li] = (ny & (ny - 1)) == 0 ? __builtin_ctzll(static_cast<unsigned long long>(ny)) : -1;
         g.cap[li] = nx * ny;
     }
     int dev = 0;
@@ -1775,6 +2198,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         ctx->fbcap = total_cells;
         CU(cudaMalloc(&ctx->fbl, sizeof(int2) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbm, sizeof(unsigned) * ctx->fbcap));
+        CU(cudaMalloc(&ctx->fbdm, sizeof(unsigned) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbc, sizeof(int) * 2));
         CU(cudaMalloc(&ctx->err, sizeof(int) * 4));
         CU(cudaMemset(ctx->err, 0, sizeof(int) * 4));
@@ -1898,7 +2322,10 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             CU(cudaMemcpy(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
             return MRLBM_OK;
         };
-        if (up(ctx->tidx, idx) || up(ctx->toff, off) || up(ctx->tw, w) || up(ctx->tdep, dep) || up(ctx->tpidx, pidx) ||
+        std::vector<int2> etav;
+        for (int hh = 0; hh < sc->q; ++hh)
+            etav.push_back(make_int2(sc->eta[hh][0], sc->d == 2 ? sc->eta[hh][1] : 0));
+        if (up(ctx->etad, etav) || up(ctx->tidx, idx) || up(ctx->toff, off) || up(ctx->tw, w) || up(ctx->tdep, dep) || up(ctx->tpidx, pidx) ||
             up(ctx->tpar, par) || up(ctx->udep, udep) || up(ctx->guidx, guidx) || up(ctx->guoff, guoff) || up(ctx->tu, tu) || up(ctx->upidx, upidx) || up(ctx->upar, upar))
             return MRLBM_ERR_CUDA;
         for (auto& e : ctx->ev)
@@ -2078,6 +2505,14 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
                     cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]);
                     phase[map_phase[k]] += ms;
                 }
+                for (int k = 0; k < ctx->kn; ++k)
+                {
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, k == 0 ? ctx->ev[0] : ctx->kev[k - 1], ctx->kev[k]);
+                    auto& a = ctx->kacc[ctx->klabel[k]];
+                    a.first += ms;
+                    a.second += 1;
+                }
             }
         }
         ctx->cur = 1 - ctx->cur;
@@ -2177,6 +2612,22 @@ int mrlbm_set_profiling(mrlbm_ctx* ctx, int on)
     return MRLBM_OK;
 }
 
+int mrlbm_profile_text(mrlbm_ctx* ctx, char* buf, int cap, int reset)
+{
+    if (!ctx || !buf || cap <= 0)
+        return MRLBM_ERR_CONFIG;
+    std::string out;
+    for (const auto& kv : ctx->kacc)
+        out += kv.first.first + " " + std::to_string(kv.first.second) + " " + std::to_string(kv.second.first) + " " +
+               std::to_string(kv.second.second) + "\n";
+    const int n = std::min<int>(cap - 1, static_cast<int>(out.size()));
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+    if (reset)
+        ctx->kacc.clear();
+    return MRLBM_OK;
+}
+
 int mrlbm_set_graph(mrlbm_ctx* ctx, int on)
 {
     if (!ctx)
@@ -2235,6 +2686,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->fbc);
     cudaFree(ctx->fbl);
     cudaFree(ctx->fbm);
+    cudaFree(ctx->fbdm);
     cudaFree(ctx->upd);
     cudaFree(ctx->tidx);
     cudaFree(ctx->toff);
@@ -2248,9 +2700,12 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->tu);
     cudaFree(ctx->upidx);
     cudaFree(ctx->upar);
+    cudaFree(ctx->etad);
     for (auto& e : ctx->ev)
         if (e)
             cudaEventDestroy(e);
+    for (auto& e : ctx->kev)
+        cudaEventDestroy(e);
     if (ctx->stream)
         cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -74,6 +74,16 @@ class Solver:
     def set_profiling(self, on=True):
         self._check(self.L.mrlbm_set_profiling(self.h, int(bool(on))))
 
+    def profile_text(self, reset=True):
+        """Per-kernel device times of the profiled steps: {(kernel, level): (ms, launches)}."""
+        buf = C.create_string_buffer(1 << 16)
+        self._check(self.L.mrlbm_profile_text(self.h, buf, len(buf), int(bool(reset))))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            k, lv, ms, n = line.split()
+            out[(k, int(lv))] = (float(ms), int(n))
+        return out
+
     def set_graph(self, on=True):
         self._check(self.L.mrlbm_set_graph(self.h, int(bool(on))))
 
