@@ -96,6 +96,8 @@ struct Aux {
     const int2* upidx;  // [g] -> (start, count) into upar
     const int2* upar;   // [g] union of the parent sets
     const int2* eta;    // [h] logical velocities (x, y)
+    const unsigned short* pmask; // [(g * q + h) * 2 + side] parents as bits of the 3^d box ((ox+1)*3+(oy+1))
+    const unsigned short* umask; // [g] union over the pairs
 };
 
 // ---------------------------------------------------------------- helpers
@@ -200,8 +202,8 @@ __device__ __forceinline__ void flag_err(int* err, int which)
 
 // ---------------------------------------------------------------- K1 / K6 project
 // internal value = (sum of the 2^D children in children order) / 2^D   (prediction.hpp:51-60)
-template <int D>
-__global__ void k_project(Geo g, Tree t, Fld F, int m, Aux aux)
+template <int D, int Q>
+__global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Aux aux)
 {
     const int li = m - g.J0;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
@@ -225,7 +227,8 @@ __global__ void k_project(Geo g, Tree t, Fld F, int m, Aux aux)
             flag_err(aux.err, 0);
             continue;
         }
-        for (int h = 0; h < g.q; ++h)
+        #pragma unroll
+        for (int h = 0; h < Q; ++h)
         {
             const double* src = F.f[li + 1] + (long long)h * cap1;
             double acc = 0.0;
@@ -240,8 +243,8 @@ __global__ void k_project(Geo g, Tree t, Fld F, int m, Aux aux)
 // d = f - predict; metric = max over siblings and populations
 // (PAPER.md:656); keep iff metric >= eps_l (Eq. 10), blow-up
 // refinement iff metric >= 2^{mu+D} eps_l
-template <int D>
-__global__ void k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, int m, Aux aux)
+template <int D, int Q>
+__global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, int m, Aux aux)
 {
     const int li = m - g.J0;
     const int l = m + 1;
@@ -279,7 +282,8 @@ __global__ void k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, i
             continue;
         }
         double metric = 0.0;
-        for (int h = 0; h < g.q; ++h)
+        #pragma unroll
+        for (int h = 0; h < Q; ++h)
         {
             const double* fm = F.f[li] + (long long)h * cap;
             const double* f1 = F.f[li + 1] + (long long)h * cap1;
@@ -622,23 +626,37 @@ template <int D>
 __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int m, int li, int gap, long long i, int x,
                                               int y, const int4& ub, const int2& pi, Aux& aux)
 {
+    (void)pi;
     const int nx = g.nx[li], ny = g.ny[li];
-    bool fb = (!g.per0 && (x + ub.x < 0 || x + ub.y >= nx)) || (D == 2 && !g.per1 && (y + ub.z < 0 || y + ub.w >= ny));
-    for (int e = pi.x; e < pi.x + pi.y && !fb; ++e)
-    {
-        const int2 o = aux.upar[e];
-        int xx = x + o.x, yy = y + o.y;
-        if (xx < 0 || xx >= nx || (D == 2 && (yy < 0 || yy >= ny)))
+    // internal cells of the 3^d box as bits (outside a non-periodic wall: not internal,
+    // the domain test covers those)
+    unsigned ib = 0;
+    const unsigned um = aux.umask[gap];
+    if (um)
+        for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
         {
-            if ((!g.per0 && (xx < 0 || xx >= nx)) || (D == 2 && !g.per1 && (yy < 0 || yy >= ny)))
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            const int bit = D == 1 ? (ox + 1) * 3 + 1 : o;
+            if (!((um >> bit) & 1u))
                 continue;
-            xx = mr_coord(xx, nx, 1);
-            if (D == 2)
+            int xx = x + ox, yy = y + oy;
+            if (xx < 0 || xx >= nx)
+            {
+                if (!g.per0)
+                    continue;
+                xx = mr_coord(xx, nx, 1);
+            }
+            if (D == 2 && (yy < 0 || yy >= ny))
+            {
+                if (!g.per1)
+                    continue;
                 yy = mr_coord(yy, ny, 1);
+            }
+            if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
+                ib |= 1u << bit;
         }
-        if (fl.kind[li][xy2lin<D>(xx, yy, ny)] & K_INT)
-            fb = true;
-    }
+    const bool fb = (ib & um) || (!g.per0 && (x + ub.x < 0 || x + ub.y >= nx)) ||
+                    (D == 2 && !g.per1 && (y + ub.z < 0 || y + ub.w >= ny));
     if (!fb)
         return;
     unsigned mask = 0, dmask = 0;
@@ -647,14 +665,7 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
         const int key = gap * 2 * g.q + pair;
         const int4 db = aux.tdep[key];
         const bool dom = !((!g.per0 && (x + db.x < 0 || x + db.y >= nx)) || (D == 2 && !g.per1 && (y + db.z < 0 || y + db.w >= ny)));
-        bool ok = dom;
-        const int2 pp = aux.tpidx[key];
-        for (int k = pp.x; k < pp.x + pp.y && ok; ++k)
-        {
-            const int2 o = aux.tpar[k];
-            if (fl.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)] & K_INT)
-                ok = false;
-        }
+        const bool ok = dom && !(ib & aux.pmask[key]);
         if (!ok)
             mask |= 1u << pair;
         if (!dom)
@@ -944,8 +955,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* ki
 // ---------------------------------------------------------------- K5 transfer, virtual values
 // new R cell: old value if it was in the old complete tree (copy / projected),
 // else prediction from the new level m-1 values (Decision D.24)
-template <int D>
-__global__ void k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux aux)
+template <int D, int Q>
+__global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux aux)
 {
     const int li = m - g.J0;
     const int nL = tn.cnt[li * 4 + 0], nI = tn.cnt[li * 4 + 1];
@@ -958,8 +969,14 @@ __global__ void k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux a
         const int os = to.map[li][lin];
         if (os >= 0 && os < onR)
         {
-            for (int h = 0; h < g.q; ++h)
-                F1.f[li][(long long)h * cap + s] = F0.f[li][(long long)h * cap + os];
+            // all loads first (F0 and F1 never alias), then the stores
+            double v[Q];
+#pragma unroll
+            for (int h = 0; h < Q; ++h)
+                v[h] = __ldg(F0.f[li] + (long long)h * cap + os);
+#pragma unroll
+            for (int h = 0; h < Q; ++h)
+                F1.f[li][(long long)h * cap + s] = v[h];
             continue;
         }
         if (m == g.J0)
@@ -986,7 +1003,8 @@ __global__ void k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux a
             continue;
         }
         const long long capp = g.cap[li - 1];
-        for (int h = 0; h < g.q; ++h)
+        #pragma unroll
+        for (int h = 0; h < Q; ++h)
         {
             double sv[NS];
             for (int o = 0; o < NS; ++o)
@@ -997,8 +1015,8 @@ __global__ void k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux a
 }
 
 // virtual cells (ghosts + reconstruction bands): zero-detail prediction from level m-1
-template <int D>
-__global__ void k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
+template <int D, int Q>
+__global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
 {
     const int li = m - g.J0;
     const int nR = tn.cnt[li * 4 + 0] + tn.cnt[li * 4 + 1], nV = tn.cnt[li * 4 + 2];
@@ -1024,7 +1042,8 @@ __global__ void k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
             flag_err(aux.err, 0);
             continue;
         }
-        for (int h = 0; h < g.q; ++h)
+        #pragma unroll
+        for (int h = 0; h < Q; ++h)
         {
             double sv[NS];
             for (int o = 0; o < NS; ++o)
@@ -1836,6 +1855,8 @@ struct mrlbm_ctx {
     int2* upidx = nullptr;
     int2* upar = nullptr;
     int2* etad = nullptr;
+    unsigned short* pmaskd = nullptr;
+    unsigned short* umaskd = nullptr;
     int cur = 0;
     bool committed = false;
     bool profiling = false;
@@ -1929,6 +1950,8 @@ Aux aux_of(mrlbm_ctx* c)
     a.upidx = c->upidx;
     a.upar = c->upar;
     a.eta = c->etad;
+    a.pmask = c->pmaskd;
+    a.umask = c->umaskd;
     return a;
 }
 
@@ -2004,11 +2027,11 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 0);
     // K1 projection of the old tree (bottom-up)
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux);  kmark(c, "k_project", m); }
+        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux);  kmark(c, "k_project", m); }
     phase_mark(c, 1);
     // K2 details + flags
     for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_details<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux);  kmark(c, "k_details", m); }
+        { c->kcount++; k_details<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux);  kmark(c, "k_details", m); }
     phase_mark(c, 2);
     // K3 closure, enlargement, grading
     for (int m = c->J1 - 1; m > c->J0; --m)
@@ -2060,11 +2083,11 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 4);
     // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_transfer<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux);  kmark(c, "k_transfer", m); }
+        { c->kcount++; k_transfer<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux);  kmark(c, "k_transfer", m); }
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_project", m); }
+        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_project", m); }
     for (int m = c->J0 + 1; m <= c->J1; ++m)
-        { c->kcount++; k_virtual<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_virtual", m); }
+        { c->kcount++; k_virtual<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_virtual", m); }
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
     { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
@@ -2255,8 +2278,10 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         std::vector<int4> dep, udep;
         std::vector<double> w;
         std::vector<uint8_t> tu;
+        std::vector<unsigned short> pmask, umask;
         for (int gp = 0; gp < ctx->nlev; ++gp)
         {
+            unsigned short um = 0;
             int4 ub = make_int4(0, 0, 0, 0);
             std::vector<std::pair<int, int>> un;
             std::vector<std::pair<int, int>> gu; // distinct table offsets of this gap
@@ -2287,6 +2312,15 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
                     dep.push_back(db);
                     ub = make_int4(std::min(ub.x, db.x), std::max(ub.y, db.y), std::min(ub.z, db.z), std::max(ub.w, db.w));
                     pidx.push_back(make_int2(static_cast<int>(par.size()), static_cast<int>(ts.par.size())));
+                    unsigned short pm = 0;
+                    for (const auto& p : ts.par)
+                    {
+                        if (std::abs(p.first) > 1 || std::abs(p.second) > 1)
+                            return set_err(ctx, MRLBM_ERR_CONFIG, "table parent outside the 3^d box");
+                        pm |= static_cast<unsigned short>(1u << ((p.first + 1) * 3 + (p.second + 1)));
+                    }
+                    pmask.push_back(pm);
+                    um |= pm;
                     for (const auto& p : ts.par)
                     {
                         par.push_back(make_int2(p.first, p.second));
@@ -2298,6 +2332,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             guidx.back().y = static_cast<int>(gu.size());
             for (const auto& o : gu)
                 guoff.push_back(make_int2(o.first, o.second));
+            umask.push_back(um);
             udep.push_back(ub);
             upidx.push_back(make_int2(static_cast<int>(upar.size()), static_cast<int>(un.size())));
             for (const auto& p : un)
@@ -2325,7 +2360,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         std::vector<int2> etav;
         for (int hh = 0; hh < sc->q; ++hh)
             etav.push_back(make_int2(sc->eta[hh][0], sc->d == 2 ? sc->eta[hh][1] : 0));
-        if (up(ctx->etad, etav) || up(ctx->tidx, idx) || up(ctx->toff, off) || up(ctx->tw, w) || up(ctx->tdep, dep) || up(ctx->tpidx, pidx) ||
+        if (up(ctx->pmaskd, pmask) || up(ctx->umaskd, umask) || up(ctx->etad, etav) || up(ctx->tidx, idx) || up(ctx->toff, off) || up(ctx->tw, w) || up(ctx->tdep, dep) || up(ctx->tpidx, pidx) ||
             up(ctx->tpar, par) || up(ctx->udep, udep) || up(ctx->guidx, guidx) || up(ctx->guoff, guoff) || up(ctx->tu, tu) || up(ctx->upidx, upidx) || up(ctx->upar, upar))
             return MRLBM_ERR_CUDA;
         for (auto& e : ctx->ev)
@@ -2701,6 +2736,8 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->upidx);
     cudaFree(ctx->upar);
     cudaFree(ctx->etad);
+    cudaFree(ctx->pmaskd);
+    cudaFree(ctx->umaskd);
     for (auto& e : ctx->ev)
         if (e)
             cudaEventDestroy(e);
