@@ -17,7 +17,10 @@ NVCC_FLAGS = [
 
 
 def build(verbose=False):
-    deps = SRC + [os.path.join(HERE, "csrc", "mrlbm_internal.h"), os.path.join(ROOT, "include", "mrlbm_gpu.h")]
+    gen = os.path.join(HERE, "csrc", "stream_gen.cuh")
+    if not os.path.exists(gen):
+        subprocess.run([sys.executable, os.path.join(HERE, "csrc", "gen_stream.py")], check=True)
+    deps = SRC + [os.path.join(HERE, "csrc", "mrlbm_internal.h"), gen, os.path.join(ROOT, "include", "mrlbm_gpu.h")]
     if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(p) for p in deps):
         return OUT
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

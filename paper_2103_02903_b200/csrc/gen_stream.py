@@ -1,0 +1,225 @@
+"""Generate stream_gen.cuh: fully unrolled flattened-table stream sums for the
+built-in velocity sets (K7 fast path).
+
+For every velocity set and gap class (0, 1, >= 2; the table offsets are identical
+for every gap >= 2, asserted below up to gap 14) the generated function
+  * loads the slots of all distinct table offsets of the class once per leaf,
+  * per population loads each distinct operand once and evaluates
+    sum_E then sum_A in table-entry order (lexicographic offsets, non-zero exact
+    weights -- the order csrc/host_configs.cpp produces) with the weights taken
+    from the runtime tables in shared memory,
+so the arithmetic is identical to the generic table loop (and to the oracle).
+
+Run: python paper_2103_02903_b200/csrc/gen_stream.py  (rewrites stream_gen.cuh)
+"""
+import itertools
+import os
+from fractions import Fraction
+
+C1 = Fraction(-1, 8)
+
+
+def pred_w(d, delta):
+    if d == 1:
+        s = 1 if delta[0] == 0 else -1
+        return {(-1,): -s * C1, (0,): Fraction(1), (1,): s * C1}
+    s0 = 1 if delta[0] == 0 else -1
+    s1 = 1 if delta[1] == 0 else -1
+    w = {(0, 0): Fraction(1)}
+
+    def add(k, v):
+        w[k] = w.get(k, 0) + v
+    add((1, 0), s0 * C1); add((-1, 0), -s0 * C1); add((0, 1), s1 * C1); add((0, -1), -s1 * C1)
+    t = -s0 * s1 * C1 * C1
+    add((1, 1), t); add((-1, 1), -t); add((1, -1), -t); add((-1, -1), t)
+    return w
+
+
+def table_offsets(d, g, eta, side):
+    n = 2 ** g
+    inb = lambda x: all(0 <= xi < n for xi in x)  # noqa: E731
+    cur = {}
+    for x in itertools.product(range(-1, n + 1), repeat=d):
+        xe = tuple(xi + e for xi, e in zip(x, eta))
+        if (inb(xe) and not inb(x)) if side == 0 else (inb(x) and not inb(xe)):
+            cur[x] = Fraction(1)
+    for _ in range(g):
+        nxt = {}
+        for c, w in cur.items():
+            p = tuple(ci >> 1 for ci in c)
+            dl = tuple(ci - 2 * pi for ci, pi in zip(c, p))
+            for o, wo in pred_w(d, dl).items():
+                k = tuple(pi + oi for pi, oi in zip(p, o))
+                nxt[k] = nxt.get(k, 0) + w * wo
+        cur = nxt
+    return [k for k, v in sorted(cur.items()) if v != 0]
+
+
+D2Q4 = [(1, 0), (0, 1), (-1, 0), (0, -1)]
+SETS = {
+    # name: (d, q, eta list, equilibrium enum)
+    "EQ1": (1, 2, [(1,), (-1,)]),
+    "EQ2": (1, 9, [(0,), (1,), (-1,)] * 3),
+    "EQ3": (2, 4, D2Q4),
+    "EQ4": (2, 16, D2Q4 * 4),
+    "EQ5": (2, 9, [(0, 0), (1, 0), (0, 1), (-1, 0), (0, -1), (1, 1), (-1, 1), (-1, -1), (1, -1)]),
+}
+
+
+def gen_class(name, d, q, etas, gclass, out):
+    g = gclass
+    tabs = {}
+    for h, eta in enumerate(etas):
+        for side in (0, 1):
+            tabs[(h, side)] = table_offsets(d, g, eta, side)
+            if gclass == 2:
+                for gg in range(3, 15 if d == 1 else 11):
+                    assert table_offsets(d, gg, eta, side) == tabs[(h, side)], (name, h, side, gg)
+    offs = sorted({o for v in tabs.values() for o in v})
+    oid = {o: i for i, o in enumerate(offs)}
+    fn = f"gen_stream_{name}_g{gclass}"
+    out.append(f"// {name}: gap class {gclass} ({len(offs)} distinct offsets)")
+    out.append(f"__device__ __forceinline__ void {fn}(const double* __restrict__ Fin, long long cap, "
+               f"const int32_t* __restrict__ map, int x, int y, int nx, int ny, int per0, int per1, "
+               f"long long s, const double* sW, double scale, double (&f)[{q}])")
+    out.append("{")
+    out.append("    (void)y; (void)ny; (void)per1; (void)nx; (void)per0;")
+    for o, i in oid.items():
+        ox = o[0]
+        oy = o[1] if d == 2 else 0
+        xs = f"x + ({ox})" if ox else "x"
+        if d == 1:
+            out.append(f"    const int sl{i} = map[gen_wrap({xs}, nx, per0)];")
+        else:
+            ys = f"y + ({oy})" if oy else "y"
+            out.append(f"    const int sl{i} = map[gen_wrap({xs}, nx, per0) * ny + gen_wrap({ys}, ny, per1)];")
+    widx = 0
+    for h in range(q):
+        used = sorted({oid[o] for side in (0, 1) for o in tabs[(h, side)]})
+        out.append("    {")
+        out.append(f"        const double* Fh = Fin + {h}LL * cap;")
+        out.append("        const double fs = Fh[s];")
+        for u in used:
+            out.append(f"        const double v{u} = sl{u} >= 0 ? Fh[sl{u}] : 0.0;")
+        sums = []
+        for side in (0, 1):
+            nm = "sE" if side == 0 else "sA"
+            out.append(f"        double {nm} = 0.0;")
+            for o in tabs[(h, side)]:
+                out.append(f"        {nm} = __dadd_rn({nm}, __dmul_rn(sW[{widx}], v{oid[o]}));")
+                widx += 1
+            sums.append(nm)
+        out.append(f"        f[{h}] = __dadd_rn(fs, __dmul_rn(scale, __dsub_rn(sE, sA)));")
+        out.append("    }")
+    out.append("}")
+    out.append("")
+    return widx
+
+
+def rim_cells_g1(d, eta, side):
+    """E (side 0) / A (side 1) finest cells of a gap-1 leaf, lexicographic, as
+    offsets (dx, dy) in the 4^d box [2x-1, 2x+3) x [2y-1, 2y+3)."""
+    out = []
+    rng = range(0, 4)
+    inb = lambda c: all(1 <= ci <= 2 for ci in c)  # noqa: E731
+    for c in itertools.product(rng, repeat=d):
+        ce = tuple(ci + e for ci, e in zip(c, eta))
+        if (inb(ce) and not inb(c)) if side == 0 else (inb(c) and not inb(ce)):
+            out.append(c)
+    return out
+
+
+def gen_fb1(name, d, q, etas, out):
+    """Gap-1 fallback leaves: table sums + details of the rim cells that are finest
+    leaves (Decision D.13b), per (population, side) selected by the masks."""
+    tabs = {(h, side): table_offsets(d, 1, eta, side) for h, eta in enumerate(etas) for side in (0, 1)}
+    nbox = 5 ** d
+    bidx = (lambda o: o[0] + 2) if d == 1 else (lambda o: (o[0] + 2) * 5 + (o[1] + 2))
+    out.append(f"// {name}: gap-1 fallback leaves (table + detail correction), box = 5^d level-l slots,")
+    out.append("// rim = 4^d finest slots; pairs with a dmask bit are left to the caller (boundary rim).")
+    out.append(f"__device__ __forceinline__ void gen_fb1_{name}(const double* __restrict__ Fin, long long cap, "
+               f"const double* __restrict__ Fj, long long capj, const int* box, const int* rim, int bstride, "
+               f"int nLj, unsigned mask, unsigned dmask, const double* sW, double (&sE)[{q}], double (&sA)[{q}])")
+    out.append("{")
+    widx = 0
+    nr = 4 ** d
+    for h, eta in enumerate(etas):
+        needed_box = set()
+        for side in (0, 1):
+            for o in tabs[(h, side)]:
+                needed_box.add(bidx(o))
+        out.append("    {")
+        out.append(f"        const double* Fh = Fin + {h}LL * cap;")
+        out.append(f"        const double* Fjh = Fj + {h}LL * capj;")
+        out.append("        (void)Fjh;")
+        for b in sorted(needed_box):
+            out.append(f"        const int b{b} = box[{b} * bstride];")
+            out.append(f"        const double v{b} = b{b} >= 0 ? Fh[b{b}] : 0.0;")
+        for side in (0, 1):
+            nm = "sE" if side == 0 else "sA"
+            pair = 2 * h + side
+            out.append(f"        if (!((dmask >> {pair}) & 1u))")
+            out.append("        {")
+            out.append("            double acc = 0.0;")
+            for o in tabs[(h, side)]:
+                out.append(f"            acc = __dadd_rn(acc, __dmul_rn(sW[{widx}], v{bidx(o)}));")
+                widx += 1
+            rims = rim_cells_g1(d, eta, side)
+            if rims:
+                out.append(f"            if ((mask >> {pair}) & 1u)")
+                out.append("            {")
+                extra = set()
+                for c in rims:
+                    p = tuple((ci + 1) // 2 - 1 for ci in c)
+                    for st in itertools.product((-1, 0, 1), repeat=d):
+                        extra.add(bidx(tuple(pi + si for pi, si in zip(p, st))))
+                for b in sorted(extra - needed_box):
+                    out.append(f"                const int b{b} = box[{b} * bstride];")
+                    out.append(f"                const double v{b} = b{b} >= 0 ? Fh[b{b}] : 0.0;")
+                for c in rims:
+                    r = c[0] if d == 1 else c[0] * 4 + c[1]
+                    p = tuple((ci + 1) // 2 - 1 for ci in c)
+                    par = tuple((ci + 1) & 1 for ci in c)  # child parity of the rim cell
+                    out.append("                {")
+                    out.append(f"                    const int sj = rim[{r} * bstride];")
+                    out.append("                    if (sj >= 0 && sj < nLj)")
+                    out.append("                    {")
+                    sv = []
+                    for st in itertools.product((-1, 0, 1), repeat=d):
+                        sv.append(f"v{bidx(tuple(pi + si for pi, si in zip(p, st)))}")
+                    out.append(f"                        const double sv[{len(sv)}] = {{{', '.join(sv)}}};")
+                    dy = par[1] if d == 2 else 0
+                    out.append(f"                        acc = __dadd_rn(acc, __dsub_rn(Fjh[sj], mr_predict<{d}>(sv, {par[0]}, {dy})));")
+                    out.append("                    }")
+                    out.append("                }")
+                out.append("            }")
+            out.append(f"            {nm}[{h}] = acc;")
+            out.append("        }")
+        out.append("    }")
+    out.append("}")
+    out.append("")
+    return widx
+
+
+def main():
+    out = ["// GENERATED by gen_stream.py -- do not edit.",
+           "// Unrolled flattened-table stream sums for the built-in velocity sets (K7 fast path).",
+           "#pragma once",
+           "",
+           "__device__ __forceinline__ int gen_wrap(int c, int n, int per)",
+           "{",
+           "    return per ? (c < 0 ? c + n : (c >= n ? c - n : c)) : c;",
+           "}",
+           ""]
+    for name, (d, q, etas) in SETS.items():
+        for gc in (0, 1, 2):
+            gen_class(name, d, q, etas, gc, out)
+    for name, (d, q, etas) in SETS.items():
+        gen_fb1(name, d, q, etas, out)
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "stream_gen.cuh")
+    open(path, "w").write("\n".join(out) + "\n")
+    print("wrote", path, len(out), "lines")
+
+
+if __name__ == "__main__":
+    main()

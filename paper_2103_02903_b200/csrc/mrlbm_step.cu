@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cstring>
 #include <map>
@@ -62,6 +63,7 @@ struct Flags {
     uint8_t* rn[kL];
     uint8_t* keep[kL];
     unsigned* fbm[kL]; // dense per cell: invalid (population, side) mask of fallback leaves
+    unsigned* fbd[kL]; // dense per cell: pairs whose dependencies leave the domain
 };
 
 struct SchemeDev {
@@ -190,6 +192,9 @@ __device__ __forceinline__ double mr_predict(const double* st, int dx, int dy)
         return __dsub_rn(a, __dmul_rn(__dmul_rn(s0, s1), qxy));
     }
 }
+
+// generated unrolled table sums for the built-in velocity sets (gen_stream.py)
+#include "stream_gen.cuh"
 
 __device__ __forceinline__ void flag_err(int* err, int which)
 {
@@ -334,12 +339,12 @@ __global__ void k_closure(Geo g, Tree t, Flags fl, int m)
 
 // rn |= keep;  H(a): (l, k - eta^h) for k in R(T) at level l = m + 1
 template <int D>
-__global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, int m)
+__global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, int m, unsigned emask)
 {
+    (void)sc;
     const int li = m - g.J0;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
     const int ny = g.ny[li];
-    const int nx1 = g.nx[li + 1], ny1 = g.ny[li + 1];
     GRID_STRIDE(s, nL, nL + nI)
     {
         const int plin = t.cells[li][s];
@@ -348,24 +353,23 @@ __global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, int m)
         fl.rn[li][plin] = 1;
         int px, py;
         lin2xy_l<D>(plin, ny, g.lny[li], px, py);
-        for (int c = 0; c < (1 << D); ++c)
+        // distinct parents of the shifted children: a static 3^D offset mask (emask);
+        // a target parent inside the domain always has an in-domain contributing child
+        const int nx = g.nx[li];
+        for (int o = 0; o < 9; ++o)
         {
-            const int cx = 2 * px + (D == 1 ? c : (c >> 1)), cy = D == 1 ? 0 : 2 * py + (c & 1);
-            for (int h = 0; h < sc->q; ++h)
-            {
-                const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
-                if (ex == 0 && ey == 0)
-                    continue;
-                int x = cx - ex, y = cy - ey;
-                if (!g.per0 && (x < 0 || x >= nx1))
-                    continue;
-                if (D == 2 && !g.per1 && (y < 0 || y >= ny1))
-                    continue;
-                x = mr_coord(x, nx1, 1);
-                if (D == 2)
-                    y = mr_coord(y, ny1, 1);
-                fl.rn[li][xy2lin<D>(x >> 1, y >> 1, ny)] = 1;
-            }
+            if (!((emask >> o) & 1u))
+                continue;
+            const int ox = o / 3 - 1, oy = o % 3 - 1;
+            int x = px + ox, y = py + (D == 1 ? 0 : oy);
+            if (!g.per0 && (x < 0 || x >= nx))
+                continue;
+            if (D == 2 && !g.per1 && (y < 0 || y >= ny))
+                continue;
+            x = mr_coord(x, nx, 1);
+            if (D == 2)
+                y = mr_coord(y, ny, 1);
+            fl.rn[li][xy2lin<D>(x, y, ny)] = 1;
         }
     }
 }
@@ -624,15 +628,15 @@ __global__ void k_kinds_v(Geo g, Flags fl, int m)
 // fallback flags: chunks without a plain leaf are skipped with one load
 template <int D>
 __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int m, int li, int gap, long long i, int x,
-                                              int y, const int4& ub, const int2& pi, Aux& aux)
+                                              int y, const int4& ub, const int2& pi, Aux& aux, int ib_in = -1)
 {
     (void)pi;
     const int nx = g.nx[li], ny = g.ny[li];
     // internal cells of the 3^d box as bits (outside a non-periodic wall: not internal,
     // the domain test covers those)
-    unsigned ib = 0;
+    unsigned ib = ib_in >= 0 ? (unsigned)ib_in : 0u;
     const unsigned um = aux.umask[gap];
-    if (um)
+    if (um && ib_in < 0)
         for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
@@ -672,8 +676,9 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
             dmask |= 1u << pair;
     }
     fl.fbm[li][i] = mask;
+    fl.fbd[li][i] = dmask;
     fl.kind[li][i] = K_LEAF | K_FB;
-    if (gap > 0)
+    if (gap >= 2)
     {
         const int k = atomicAdd(aux.fb_count, 1);
         if (k < aux.fb_cap)
@@ -686,7 +691,13 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
             flag_err(aux.err, 2);
     }
     else
-        atomicAdd(aux.fb_count + 1, 1);
+    {
+        // gap 0 / 1 fallback leaves are found by slot scans (K7 / k_stream_fb1);
+        // count them for the statistics with one atomic per warp
+        const unsigned am = __activemask();
+        if ((threadIdx.x & 31) == __ffs(am) - 1)
+            atomicAdd(aux.fb_count + 1, __popc(am));
+    }
 }
 
 template <int D>
@@ -728,9 +739,33 @@ __global__ void k_fallback_v(Geo g, Flags fl, int m, Aux aux)
             continue;
         const int lin0 = (int)(c * 16);
         const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
+        const int nx = g.nx[li];
+        // internal flags of rows x-1, x, x+1 over y0-1 .. y0+16 (clip / wrap)
+        uint8_t w[3][18];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+        {
+            int xr = x + r - 1;
+            const bool ok = (xr >= 0 && xr < nx) || g.per0;
+            xr = mr_coord(xr, nx, 1);
+            V16 v;
+            v.v = ok ? reinterpret_cast<const uint4*>(fl.kind[li] + (long long)xr * ny)[y0 >> 4] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                w[r][j + 1] = ok ? (v.b[j] & K_INT) : 0;
+            const int yl = y0 - 1, yr = y0 + 16;
+            w[r][0] = (ok && (yl >= 0 || g.per1)) ? (fl.kind[li][(long long)xr * ny + mr_coord(yl, ny, 1)] & K_INT) : 0;
+            w[r][17] = (ok && (yr < ny || g.per1)) ? (fl.kind[li][(long long)xr * ny + mr_coord(yr, ny, 1)] & K_INT) : 0;
+        }
         for (int j = 0; j < 16; ++j)
             if (k.b[j] == K_LEAF)
-                fallback_cell<2>(g, fl, m, li, gap, lin0 + j, x, y0 + j, ub, pi, aux);
+            {
+                int ib = 0;
+#pragma unroll
+                for (int o = 0; o < 9; ++o)
+                    ib |= (w[o / 3][j + (o % 3)] ? 1 : 0) << o;
+                fallback_cell<2>(g, fl, m, li, gap, lin0 + j, x, y0 + j, ub, pi, aux, ib);
+            }
     }
 }
 
@@ -1361,14 +1396,43 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
 // flattened table when exact, the table plus the details of the leaf rim cells
 // when only finer neighbours break it (Decision D.13b), else the boundary rim
 // (rim_sum).  Writes post-stream populations into F0; K7 collides them.
-template <int D>
-__global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld F1, const SchemeDev* sc, Aux aux)
+template <int EQ, int Q>
+__device__ __forceinline__ void gen_fb1(const double* Fin, long long cap, const double* Fj, long long capj, const int* box,
+                                        const int* rim, int bstride, int nLj, unsigned mask, unsigned dmask,
+                                        const double* sW, double (&sE)[Q], double (&sA)[Q])
+{
+    if constexpr (EQ == 1 && Q == 2)
+        gen_fb1_EQ1(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 2 && Q == 9)
+        gen_fb1_EQ2(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 3 && Q == 4)
+        gen_fb1_EQ3(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 4 && Q == 16)
+        gen_fb1_EQ4(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 5 && Q == 9)
+        gen_fb1_EQ5(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+}
+
+template <int D, int Q, int EQ, bool GEN>
+__global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* sc, Aux aux)
 {
     constexpr int kB = D == 1 ? 5 : 25;   // level-l box
     constexpr int kR = D == 1 ? 4 : 16;   // finest-level 4^D box around the children
     constexpr int kT = 128;
+    constexpr int kMaxE = 2 * Q * 25;
     __shared__ int sBox[kB][kT];
     __shared__ int sRim[kR][kT];
+    __shared__ double sW[kMaxE];
+    if (GEN && g.J1 - 1 >= g.J0)
+    {
+        // gap-1 table weights in table order
+        const int base = aux.tidx[1 * 2 * Q].x;
+        const int2 last = aux.tidx[1 * 2 * Q + 2 * Q - 1];
+        const int ne = min(last.x + last.y - base, kMaxE);
+        for (int e = threadIdx.x; e < ne; e += blockDim.x)
+            sW[e] = aux.tw[base + e];
+        __syncthreads();
+    }
     const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
     const int q = g.q;
     const int m = g.J1 - 1, li = m - g.J0, lj = li + 1;
@@ -1379,20 +1443,18 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
     const int nLj = tn.cnt[lj * 4 + 0];
     const double scale = ldexp(1.0, D * (m - g.J1));
     const int gap = 1;
-    GRID_STRIDE(it, 0, nfb)
+    (void)nfb;
+    const int nL = tn.cnt[li * 4 + 0];
+    // leaf-slot order (lexicographic) keeps neighbouring threads on neighbouring cells
+    GRID_STRIDE(sl_, 0, nL)
     {
-        const int2 e = aux.fb_list[it];
-        if (e.x != m)
+        const int lin = tn.cells[li][sl_];
+        if ((fl.kind[li][lin] & K_FB) == 0)
             continue;
-        const unsigned mask = aux.fb_mask[it], dmask = aux.fb_dmask[it];
-        const long long slot = tn.map[li][e.y];
-        if (slot < 0)
-        {
-            flag_err(aux.err, 2);
-            continue;
-        }
+        const unsigned mask = fl.fbm[li][lin], dmask = fl.fbd[li][lin];
+        const long long slot = sl_;
         int x, y;
-        lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
+        lin2xy_l<D>(lin, ny, g.lny[li], x, y);
         for (int b = 0; b < kB; ++b)
         {
             const int ox = D == 1 ? b - 2 : b / 5 - 2, oy = D == 1 ? 0 : b % 5 - 2;
@@ -1417,6 +1479,27 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
             const int rx = 2 * x - 1 + (D == 1 ? r : r / 4), ry = D == 1 ? 0 : 2 * y - 1 + r % 4;
             bool in = (g.per0 || (rx >= 0 && rx < nxj)) && (D == 1 || g.per1 || (ry >= 0 && ry < nyj));
             sRim[r][threadIdx.x] = in ? tn.map[lj][mr_lin<D>(g, g.J1, rx, ry)] : -1;
+        }
+        if constexpr (GEN)
+        {
+            double sE[Q], sA[Q];
+            gen_fb1<EQ, Q>(F1.f[li], cap, F1.f[lj], capj, &sBox[0][threadIdx.x], &sRim[0][threadIdx.x], kT, nLj, mask,
+                           dmask, sW, sE, sA);
+            if (dmask)
+                for (int h = 0; h < Q; ++h)
+                    for (int side = 0; side < 2; ++side)
+                        if ((dmask >> (2 * h + side)) & 1u)
+                        {
+                            const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
+                            (side ? sA[h] : sE[h]) = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, slot, aux);
+                        }
+#pragma unroll
+            for (int h = 0; h < Q; ++h)
+            {
+                const long long o = (long long)h * cap + slot;
+                F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sE[h], sA[h])));
+            }
+            continue;
         }
         for (int h = 0; h < q; ++h)
         {
@@ -1483,10 +1566,46 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
     }
 }
 
+// generated unrolled table sums (stream_gen.cuh) for the built-in velocity sets
+template <int EQ, int Q>
+__device__ __forceinline__ void gen_stream(int gap, const double* Fin, long long cap, const int32_t* map, int x, int y,
+                                           int nx, int ny, int per0, int per1, long long s, const double* sW,
+                                           double scale, double (&f)[Q])
+{
+#define GEN_CALL(N)                                                                                                    \
+    if (gap == 0)                                                                                                      \
+        gen_stream_EQ##N##_g0(Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
+    else if (gap == 1)                                                                                                 \
+        gen_stream_EQ##N##_g1(Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
+    else                                                                                                               \
+        gen_stream_EQ##N##_g2(Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);
+    if constexpr (EQ == 1 && Q == 2)
+    {
+        GEN_CALL(1)
+    }
+    else if constexpr (EQ == 2 && Q == 9)
+    {
+        GEN_CALL(2)
+    }
+    else if constexpr (EQ == 3 && Q == 4)
+    {
+        GEN_CALL(3)
+    }
+    else if constexpr (EQ == 4 && Q == 16)
+    {
+        GEN_CALL(4)
+    }
+    else if constexpr (EQ == 5 && Q == 9)
+    {
+        GEN_CALL(5)
+    }
+#undef GEN_CALL
+}
+
 // K7: table-path stream + collision +
 // obstacle blend, one thread per leaf.  Fallback leaves take their post-stream
 // populations from K8 (already in F0).  BS = block size of the block-diagonal M.
-template <int D, int Q, int BS, int EQ>
+template <int D, int Q, int BS, int EQ, bool GEN>
 __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F0, Fld F1, Flags fl,
                                                            const SchemeDev* scg, int m, Aux aux)
 {
@@ -1563,6 +1682,12 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
 #pragma unroll
             for (int h = 0; h < Q; ++h)
                 f[h] = Fout[(long long)h * cap + s];
+        }
+        else if (GEN && !fb)
+        {
+            int x, y;
+            lin2xy_l<D>(lin, ny, g.lny[li], x, y);
+            gen_stream<EQ, Q>(gap, Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);
         }
         else
         {
@@ -1831,6 +1956,7 @@ struct mrlbm_ctx {
     uint8_t* rn[kL]{};
     uint8_t* keep[kL]{};
     unsigned* fbmd[kL]{};
+    unsigned* fbdd[kL]{};
     double* F[2][kL]{};
     int* tiles[kL]{};
     long long ntiles[kL]{};
@@ -1861,6 +1987,8 @@ struct mrlbm_ctx {
     bool committed = false;
     bool profiling = false;
     bool use_graph = true;
+    bool use_gen = false; // generated stream path (built-in velocity sets)
+    unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
     std::vector<std::vector<int32_t>> st_lin;
     std::vector<std::vector<double>> st_f;
@@ -1923,6 +2051,7 @@ Flags flags_of(mrlbm_ctx* c)
         f.rn[i] = c->rn[i];
         f.keep[i] = c->keep[i];
         f.fbm[i] = c->fbmd[i];
+        f.fbd[i] = c->fbdd[i];
     }
     return f;
 }
@@ -2005,7 +2134,7 @@ void phase_mark(mrlbm_ctx* c, int k)
         cudaEventRecord(c->ev[k], c->stream);
 }
 
-template <int D, int Q, int BS, int EQ>
+template <int D, int Q, int BS, int EQ, bool GEN>
 void enqueue_step(mrlbm_ctx* c)
 {
     const int o = c->cur, n = 1 - c->cur;
@@ -2037,7 +2166,7 @@ void enqueue_step(mrlbm_ctx* c)
     for (int m = c->J1 - 1; m > c->J0; --m)
         { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);  kmark(c, "k_closure", m); }
     for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m);  kmark(c, "k_enlarge", m); }
+        { c->kcount++; k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m, c->emask);  kmark(c, "k_enlarge", m); }
     for (int m = c->J1 - 1; m > c->J0; --m)
         { c->kcount++; k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);  kmark(c, "k_grade", m); }
     phase_mark(c, 3);
@@ -2091,9 +2220,9 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
     { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
-    { c->kcount++; k_stream_fb1<D><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, F0, F1, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
+    { c->kcount++; k_stream_fb1<D, Q, EQ, GEN><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_stream_collide<D, Q, BS, EQ><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux);  kmark(c, "k_stream_collide", m); }
+        { c->kcount++; k_stream_collide<D, Q, BS, EQ, GEN><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux);  kmark(c, "k_stream_collide", m); }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
     phase_mark(c, 6);
     c->kernels_per_step = c->kcount;
@@ -2101,18 +2230,44 @@ void enqueue_step(mrlbm_ctx* c)
 
 using StepFn = void (*)(mrlbm_ctx*);
 
-StepFn step_fn(int d, int q, int nblocks, int eq)
+// the generated stream path applies when the velocities are exactly the built-in
+// set of the equilibrium kind (the order csrc/host_configs.cpp uses)
+bool builtin_velocities(const mrlbm_scheme_spec* sc)
 {
+    static const int d2q4[4][2] = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    static const int d2q9[9][2] = {{0, 0}, {1, 0}, {0, 1}, {-1, 0}, {0, -1}, {1, 1}, {-1, 1}, {-1, -1}, {1, -1}};
+    for (int h = 0; h < sc->q; ++h)
+    {
+        int ex = 0, ey = 0;
+        switch (sc->equilibrium)
+        {
+            case MRLBM_EQ_BURGERS_D1Q2: ex = h == 0 ? 1 : -1; break;
+            case MRLBM_EQ_EULER_D1Q3X3: ex = (h % 3 == 0) ? 0 : (h % 3 == 1 ? 1 : -1); break;
+            case MRLBM_EQ_ADVECTION_D2Q4:
+            case MRLBM_EQ_EULER_D2Q4X4: ex = d2q4[h % 4][0]; ey = d2q4[h % 4][1]; break;
+            case MRLBM_EQ_NS_D2Q9: ex = d2q9[h][0]; ey = d2q9[h][1]; break;
+            default: return false;
+        }
+        if (sc->eta[h][0] != ex || (sc->d == 2 && sc->eta[h][1] != ey))
+            return false;
+    }
+    return true;
+}
+
+StepFn step_fn(int d, int q, int nblocks, int eq, bool gen)
+{
+#define SF(D, Q, BS, E)                                                                                                    return gen ? enqueue_step<D, Q, BS, E, true> : enqueue_step<D, Q, BS, E, false>;
     if (d == 1 && q == 2 && nblocks == 1 && eq == MRLBM_EQ_BURGERS_D1Q2)
-        return enqueue_step<1, 2, 2, MRLBM_EQ_BURGERS_D1Q2>;
+        SF(1, 2, 2, MRLBM_EQ_BURGERS_D1Q2)
     if (d == 1 && q == 9 && nblocks == 3 && eq == MRLBM_EQ_EULER_D1Q3X3)
-        return enqueue_step<1, 9, 3, MRLBM_EQ_EULER_D1Q3X3>;
+        SF(1, 9, 3, MRLBM_EQ_EULER_D1Q3X3)
     if (d == 2 && q == 4 && nblocks == 1 && eq == MRLBM_EQ_ADVECTION_D2Q4)
-        return enqueue_step<2, 4, 4, MRLBM_EQ_ADVECTION_D2Q4>;
+        SF(2, 4, 4, MRLBM_EQ_ADVECTION_D2Q4)
     if (d == 2 && q == 16 && nblocks == 4 && eq == MRLBM_EQ_EULER_D2Q4X4)
-        return enqueue_step<2, 16, 4, MRLBM_EQ_EULER_D2Q4X4>;
+        SF(2, 16, 4, MRLBM_EQ_EULER_D2Q4X4)
     if (d == 2 && q == 9 && nblocks == 1 && eq == MRLBM_EQ_NS_D2Q9)
-        return enqueue_step<2, 9, 9, MRLBM_EQ_NS_D2Q9>;
+        SF(2, 9, 9, MRLBM_EQ_NS_D2Q9)
+#undef SF
     return nullptr;
 }
 
@@ -2140,7 +2295,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     mrlbm_ctx* ctx = nullptr;
     if (!sc || !rc)
         return MRLBM_ERR_CONFIG;
-    if (sc->d < 1 || sc->d > 2 || !step_fn(sc->d, sc->q, sc->nblocks, sc->equilibrium))
+    if (sc->d < 1 || sc->d > 2 || !step_fn(sc->d, sc->q, sc->nblocks, sc->equilibrium, false))
         return MRLBM_ERR_CONFIG;
     if (rc->j_min < 0 || rc->j_max <= rc->j_min || rc->j_max - rc->j_min + 1 > kL)
         return MRLBM_ERR_CONFIG;
@@ -2215,6 +2370,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             CU(cudaMalloc(&ctx->rn[li], n));
             CU(cudaMalloc(&ctx->keep[li], n));
             CU(cudaMalloc(&ctx->fbmd[li], sizeof(unsigned) * n));
+            CU(cudaMalloc(&ctx->fbdd[li], sizeof(unsigned) * n));
             ctx->ntiles[li] = (n + kTile - 1) / kTile;
             CU(cudaMalloc(&ctx->tiles[li], sizeof(int) * 3 * ctx->ntiles[li]));
         }
@@ -2376,6 +2532,19 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     }
     ctx->st_lin.resize(ctx->nlev);
     ctx->st_f.resize(ctx->nlev);
+    ctx->use_gen = builtin_velocities(sc) && std::getenv("MRLBM_NO_GEN") == nullptr;
+    for (int h = 0; h < sc->q; ++h)
+    {
+        const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;
+        if (ex == 0 && ey == 0)
+            continue;
+        for (int dl = 0; dl < (1 << sc->d); ++dl)
+        {
+            const int dx = sc->d == 1 ? dl : dl >> 1, dy = sc->d == 1 ? 0 : dl & 1;
+            const int ox = (dx - ex) >> 1, oy = (dy - ey) >> 1; // floor division
+            ctx->emask |= 1u << ((ox + 1) * 3 + (oy + 1));
+        }
+    }
     *out = ctx;
     return MRLBM_OK;
 }
@@ -2505,7 +2674,7 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
         return MRLBM_ERR_CONFIG;
     if (!ctx->committed)
         return set_err(ctx, MRLBM_ERR_STATE, "step before commit");
-    StepFn fn = step_fn(ctx->D, ctx->q, ctx->sc.nblocks, ctx->sc.equilibrium);
+    StepFn fn = step_fn(ctx->D, ctx->q, ctx->sc.nblocks, ctx->sc.equilibrium, ctx->use_gen);
     CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
     CU(cudaEventRecord(ctx->ev[14], ctx->stream));
     double phase[MRLBM_PHASE_COUNT] = {0};
@@ -2714,6 +2883,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         cudaFree(ctx->rn[li]);
         cudaFree(ctx->keep[li]);
         cudaFree(ctx->fbmd[li]);
+        cudaFree(ctx->fbdd[li]);
         cudaFree(ctx->tiles[li]);
     }
     cudaFree(ctx->sch);

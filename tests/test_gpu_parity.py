@@ -71,3 +71,17 @@ def test_gpu_matches_golden_fixtures():
             assert np.array_equal(idx, data[f"idx{lv}"]), (name, lv)
             assert np.array_equal(f.view(np.uint64), data[f"f{lv}"].view(np.uint64)), (name, lv)
         s.close()
+
+
+@pytest.mark.parametrize("cid,J", [(3, 6), (4, 6), (5, 6)])
+def test_generic_table_path_parity(cid, J, monkeypatch):
+    """The generic (non-generated) table loop stays bit-identical to the oracle."""
+    monkeypatch.setenv("MRLBM_NO_GEN", "1")
+    sc, rc, gpu, ora = make_pair(cid, J)
+    for k in range(12):
+        gpu.step(1)
+        ora.step(1)
+        rel, bitwise, _ = compare(gpu, ora, rc, f"generic config {cid} step {k}")
+        assert rel <= 1e-12
+    gpu.close()
+    ora.close()
