@@ -236,6 +236,18 @@ def bench_product(args):
         except Exception:
             traffic = None
 
+    # ---- steady regime (context only, not the headline): after the white-noise
+    # transient the mesh settles (~0.9 M leaves); continue the run to step 200
+    steady = None
+    if args.steady and world == 1:
+        done = args.warmup + args.steps + max(1, min(args.steps, 3))
+        if done < 200:
+            s.step(200 - done)
+        ss = s.step(20)
+        steady = {"after_steps": 200, "steps": 20, "ms_per_step": ss.ms_total / 20,
+                  "value": ss.leaf_updates and (sum(int(ss.leaves[i]) for i in range(ss.levels)) / (ss.ms_total / 20 / 1e3)),
+                  "leaves": sum(int(ss.leaves[i]) for i in range(ss.levels))}
+
     # ---- e2e through the C-ABI with host buffers: load snapshot -> commit -> K steps -> read back
     s2 = Solver(sc, rc)
     h2d = sum(v[0].nbytes + v[1].nbytes for v in snap.values())
@@ -285,6 +297,8 @@ def bench_product(args):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if steady is not None:
+            line["steady_state"] = steady
         print(json.dumps(line))
     s.close()
     if world > 1:
@@ -299,6 +313,7 @@ def main():
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--jmax", type=int, default=0, help="override J_bar (default: config value 12)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-steady", dest="steady", action="store_false", help="skip the steady-regime context run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
