@@ -1921,6 +1921,38 @@ __global__ void k_closure_dense(Geo g, Flags fl, int m)
     }
 }
 
+// load: coordinates (n x d) -> linear indices, with a domain check
+__global__ void k_idx_to_lin(const int32_t* idx, int n, int d, int nx, int ny, int32_t* lin, int* bad)
+{
+    GRID_STRIDE(i, 0, n)
+    {
+        const int x = idx[i * d], y = d == 2 ? idx[i * d + 1] : 0;
+        if (x < 0 || x >= nx || y < 0 || y >= ny)
+        {
+            atomicAdd(bad, 1);
+            lin[i] = 0;
+            continue;
+        }
+        lin[i] = d == 2 ? x * ny + y : x;
+    }
+}
+
+// read: linear indices -> coordinates
+__global__ void k_lin_to_idx(const int32_t* lin, int n, int d, int ny, int32_t* idx)
+{
+    GRID_STRIDE(i, 0, n)
+    {
+        const int l = lin[i];
+        if (d == 2)
+        {
+            idx[2 * i] = l / ny;
+            idx[2 * i + 1] = l - (l / ny) * ny;
+        }
+        else
+            idx[i] = l;
+    }
+}
+
 __global__ void k_load_scatter(const int* lins, const double* fin, int n, int q, const int32_t* map, const uint8_t* kind,
                                double* F, long long cap, int* err)
 {
@@ -1990,8 +2022,12 @@ struct mrlbm_ctx {
     bool use_gen = false; // generated stream path (built-in velocity sets)
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
-    std::vector<std::vector<int32_t>> st_lin;
-    std::vector<std::vector<double>> st_f;
+    // load staging (device): per level, coordinates -> linear indices; the values are
+    // staged in F[1] (free until the first step)
+    int32_t* ld_idx[kL]{};
+    int32_t* ld_lin[kL]{};
+    long long ld_n[kL]{};
+    int* ld_bad = nullptr;
     cudaEvent_t ev[16]{};
     double phase_ms[MRLBM_PHASE_COUNT]{};
     std::string err_msg;
@@ -2530,8 +2566,6 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         fprintf(stderr, "mrlbm_create: %s\n", msg.c_str());
         return st;
     }
-    ctx->st_lin.resize(ctx->nlev);
-    ctx->st_f.resize(ctx->nlev);
     ctx->use_gen = builtin_velocities(sc) && std::getenv("MRLBM_NO_GEN") == nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
@@ -2556,17 +2590,29 @@ int mrlbm_load_leaves(mrlbm_ctx* ctx, int level, int64_t n, const int32_t* idx, 
     if (level < ctx->J0 || level > ctx->J1 || n < 0)
         return set_err(ctx, MRLBM_ERR_CONFIG, "load: level out of range");
     const int li = level - ctx->J0;
-    auto& L = ctx->st_lin[li];
-    auto& V = ctx->st_f[li];
-    L.resize(n);
-    V.assign(f, f + n * ctx->q);
-    for (int64_t i = 0; i < n; ++i)
+    if (n > ctx->geo.cap[li])
+        return set_err(ctx, MRLBM_ERR_CONFIG, "load: more leaves than cells in the level");
+    if (!ctx->ld_idx[li])
     {
-        const int x = idx[i * ctx->D];
-        const int y = ctx->D == 2 ? idx[i * ctx->D + 1] : 0;
-        if (x < 0 || x >= ctx->geo.nx[li] || y < 0 || y >= ctx->geo.ny[li])
+        CU(cudaMalloc(&ctx->ld_idx[li], sizeof(int32_t) * ctx->D * ctx->geo.cap[li]));
+        CU(cudaMalloc(&ctx->ld_lin[li], sizeof(int32_t) * ctx->geo.cap[li]));
+    }
+    if (!ctx->ld_bad)
+        CU(cudaMalloc(&ctx->ld_bad, sizeof(int)));
+    ctx->ld_n[li] = n;
+    if (n)
+    {
+        // synchronous copies: the caller may reuse its buffers on return (pinned buffers go at full link speed)
+        CU(cudaMemcpyAsync(ctx->ld_idx[li], idx, sizeof(int32_t) * ctx->D * n, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->F[1][li], f, sizeof(double) * ctx->q * n, cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemsetAsync(ctx->ld_bad, 0, sizeof(int), ctx->stream));
+        k_idx_to_lin<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->ld_idx[li], (int)n, ctx->D, ctx->geo.nx[li],
+                                                                 ctx->geo.ny[li], ctx->ld_lin[li], ctx->ld_bad);
+        int bad = 0;
+        CU(cudaMemcpyAsync(&bad, ctx->ld_bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        if (bad)
             return set_err(ctx, MRLBM_ERR_CONFIG, "load: leaf outside the domain");
-        L[i] = ctx->D == 2 ? x * ctx->geo.ny[li] + y : x;
     }
     ctx->committed = false;
     return MRLBM_OK;
@@ -2585,33 +2631,19 @@ int mrlbm_commit(mrlbm_ctx* ctx)
         CU(cudaMemsetAsync(ctx->rn[li], 0, g.cap[li], ctx->stream));
     }
     CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
-    std::vector<int*> dl(ctx->nlev, nullptr);
-    std::vector<double*> dfv(ctx->nlev, nullptr);
-    auto cleanup = [&]()
-    {
-        for (auto p : dl)
-            if (p)
-                cudaFree(p);
-        for (auto p : dfv)
-            if (p)
-                cudaFree(p);
-    };
+    auto cleanup = [&]() {};
     int st = [&]() -> int
     {
         for (int li = 0; li < ctx->nlev; ++li)
         {
-            const long long n = ctx->st_lin[li].size();
+            const long long n = ctx->ld_n[li];
             if (!n)
                 continue;
-            CU(cudaMalloc(&dl[li], sizeof(int) * n));
-            CU(cudaMalloc(&dfv[li], sizeof(double) * n * ctx->q));
-            CU(cudaMemcpyAsync(dl[li], ctx->st_lin[li].data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
-            CU(cudaMemcpyAsync(dfv[li], ctx->st_f[li].data(), sizeof(double) * n * ctx->q, cudaMemcpyHostToDevice,
-                               ctx->stream));
+            const int* dl_li = ctx->ld_lin[li];
             if (ctx->D == 1)
-                k_load_mark<1><<<grid_for(ctx, n), 256, 0, ctx->stream>>>(g, fl, dl[li], (int)n, ctx->J0 + li);
+                k_load_mark<1><<<grid_for(ctx, n), 256, 0, ctx->stream>>>(g, fl, dl_li, (int)n, ctx->J0 + li);
             else
-                k_load_mark<2><<<grid_for(ctx, n), 256, 0, ctx->stream>>>(g, fl, dl[li], (int)n, ctx->J0 + li);
+                k_load_mark<2><<<grid_for(ctx, n), 256, 0, ctx->stream>>>(g, fl, dl_li, (int)n, ctx->J0 + li);
         }
         for (int m = ctx->J1 - 1; m > ctx->J0; --m)
         {
@@ -2635,10 +2667,10 @@ int mrlbm_commit(mrlbm_ctx* ctx)
         }
         for (int li = 0; li < ctx->nlev; ++li)
         {
-            const long long n = ctx->st_lin[li].size();
+            const long long n = ctx->ld_n[li];
             if (!n)
                 continue;
-            k_load_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(dl[li], dfv[li], (int)n, ctx->q, ctx->map[v][li],
+            k_load_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->ld_lin[li], ctx->F[1][li], (int)n, ctx->q, ctx->map[v][li],
                                                                      ctx->kind[li], ctx->F[0][li], g.cap[li], ctx->err);
         }
         CU(cudaGetLastError());
@@ -2646,7 +2678,7 @@ int mrlbm_commit(mrlbm_ctx* ctx)
         CU(cudaMemcpyAsync(counts, ctx->cnt[v], sizeof(int) * 4 * kL, cudaMemcpyDeviceToHost, ctx->stream));
         CU(cudaStreamSynchronize(ctx->stream));
         for (int li = 0; li < ctx->nlev; ++li)
-            if (counts[li * 4] != static_cast<int>(ctx->st_lin[li].size()))
+            if (counts[li * 4] != static_cast<int>(ctx->ld_n[li]))
                 return set_err(ctx, MRLBM_ERR_CONFIG, "load: leaves do not form a complete-leaf partition (level " +
                                                           std::to_string(ctx->J0 + li) + ")");
         return check_device_errors(ctx);
@@ -2654,10 +2686,8 @@ int mrlbm_commit(mrlbm_ctx* ctx)
     cleanup();
     if (st != MRLBM_OK)
         return st;
-    for (auto& s : ctx->st_lin)
-        std::vector<int32_t>().swap(s);
-    for (auto& s : ctx->st_f)
-        std::vector<double>().swap(s);
+    for (auto& n : ctx->ld_n)
+        n = 0;
     for (auto& gph : ctx->graph)
         if (gph)
         {
@@ -2782,29 +2812,22 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
         return MRLBM_OK;
     if (idx)
     {
-        std::vector<int32_t> lins(n);
-        CU(cudaMemcpyAsync(lins.data(), ctx->cells[ctx->cur][li], sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        const int ny = ctx->geo.ny[li];
-        for (int64_t i = 0; i < n; ++i)
+        if (!ctx->ld_idx[li])
         {
-            if (ctx->D == 1)
-                idx[i] = lins[i];
-            else
-            {
-                idx[2 * i] = lins[i] / ny;
-                idx[2 * i + 1] = lins[i] % ny;
-            }
+            CU(cudaMalloc(&ctx->ld_idx[li], sizeof(int32_t) * ctx->D * ctx->geo.cap[li]));
+            CU(cudaMalloc(&ctx->ld_lin[li], sizeof(int32_t) * ctx->geo.cap[li]));
         }
+        k_lin_to_idx<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->cells[ctx->cur][li], (int)n, ctx->D, ctx->geo.ny[li],
+                                                                 ctx->ld_idx[li]);
+        CU(cudaMemcpyAsync(idx, ctx->ld_idx[li], sizeof(int32_t) * ctx->D * n, cudaMemcpyDeviceToHost, ctx->stream));
     }
     if (f)
     {
         for (int h = 0; h < ctx->q; ++h)
             CU(cudaMemcpyAsync(f + h * n, ctx->F[0][li] + h * ctx->geo.cap[li], sizeof(double) * n,
                                cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
     }
+    CU(cudaStreamSynchronize(ctx->stream));
     return MRLBM_OK;
 }
 
@@ -2879,6 +2902,8 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     }
     for (int li = 0; li < kL; ++li)
     {
+        cudaFree(ctx->ld_idx[li]);
+        cudaFree(ctx->ld_lin[li]);
         cudaFree(ctx->kind[li]);
         cudaFree(ctx->rn[li]);
         cudaFree(ctx->keep[li]);
@@ -2887,6 +2912,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         cudaFree(ctx->tiles[li]);
     }
     cudaFree(ctx->sch);
+    cudaFree(ctx->ld_bad);
     cudaFree(ctx->err);
     cudaFree(ctx->fbc);
     cudaFree(ctx->fbl);

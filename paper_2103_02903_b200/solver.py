@@ -71,6 +71,17 @@ class Solver:
                                                  f.ctypes.data_as(C.c_void_p)))
         return idx, f
 
+    def read_leaves_into(self, level, idx, f):
+        """Read one level into caller-provided (e.g. pinned) buffers: idx (n, d) int32,
+        f (q, n) float64, both C-contiguous with n = level_count(level)."""
+        n = self.level_count(level)
+        assert idx.shape == (n, self.d) and f.shape == (self.q, n)
+        assert idx.flags.c_contiguous and f.flags.c_contiguous
+        if n:
+            self._check(self.L.mrlbm_read_leaves(self.h, int(level), idx.ctypes.data_as(C.c_void_p),
+                                                 f.ctypes.data_as(C.c_void_p)))
+        return n
+
     def set_profiling(self, on=True):
         self._check(self.L.mrlbm_set_profiling(self.h, int(bool(on))))
 
