@@ -80,7 +80,7 @@ def gen_class(name, d, q, etas, gclass, out):
     fn = f"gen_stream_{name}_g{gclass}"
     out.append(f"// {name}: gap class {gclass} ({len(offs)} distinct offsets)")
     out.append(f"__device__ __forceinline__ void {fn}(const double* __restrict__ Fin, long long cap, "
-               f"const int32_t* __restrict__ map, int x, int y, int nx, int ny, int per0, int per1, "
+               f"int x, int y, int nx, int ny, int per0, int per1, "
                f"long long s, const double* sW, double scale, double (&f)[{q}])")
     out.append("{")
     out.append("    (void)y; (void)ny; (void)per1; (void)nx; (void)per0;")
@@ -89,10 +89,10 @@ def gen_class(name, d, q, etas, gclass, out):
         oy = o[1] if d == 2 else 0
         xs = f"x + ({ox})" if ox else "x"
         if d == 1:
-            out.append(f"    const int sl{i} = map[gen_wrap({xs}, nx, per0)];")
+            out.append(f"    const long long sl{i} = gen_wrap({xs}, nx, per0);")
         else:
             ys = f"y + ({oy})" if oy else "y"
-            out.append(f"    const int sl{i} = map[gen_wrap({xs}, nx, per0) * ny + gen_wrap({ys}, ny, per1)];")
+            out.append(f"    const long long sl{i} = (long long)gen_wrap({xs}, nx, per0) * ny + gen_wrap({ys}, ny, per1);")
     widx = 0
     for h in range(q):
         used = sorted({oid[o] for side in (0, 1) for o in tabs[(h, side)]})
@@ -100,7 +100,7 @@ def gen_class(name, d, q, etas, gclass, out):
         out.append(f"        const double* Fh = Fin + {h}LL * cap;")
         out.append("        const double fs = Fh[s];")
         for u in used:
-            out.append(f"        const double v{u} = sl{u} >= 0 ? Fh[sl{u}] : 0.0;")
+            out.append(f"        const double v{u} = Fh[sl{u}];")
         sums = []
         for side in (0, 1):
             nm = "sE" if side == 0 else "sA"
@@ -136,10 +136,10 @@ def gen_fb1(name, d, q, etas, out):
     nbox = 5 ** d
     bidx = (lambda o: o[0] + 2) if d == 1 else (lambda o: (o[0] + 2) * 5 + (o[1] + 2))
     out.append(f"// {name}: gap-1 fallback leaves (table + detail correction), box = 5^d level-l slots,")
-    out.append("// rim = 4^d finest slots; pairs with a dmask bit are left to the caller (boundary rim).")
+    out.append("// rim = 4^d finest linear indices of leaves (-1: not a leaf); dmask pairs are left to the caller.")
     out.append(f"__device__ __forceinline__ void gen_fb1_{name}(const double* __restrict__ Fin, long long cap, "
                f"const double* __restrict__ Fj, long long capj, const int* box, const int* rim, int bstride, "
-               f"int nLj, unsigned mask, unsigned dmask, const double* sW, double (&sE)[{q}], double (&sA)[{q}])")
+               f"unsigned mask, unsigned dmask, const double* sW, double (&sE)[{q}], double (&sA)[{q}])")
     out.append("{")
     widx = 0
     nr = 4 ** d
@@ -153,8 +153,7 @@ def gen_fb1(name, d, q, etas, out):
         out.append(f"        const double* Fjh = Fj + {h}LL * capj;")
         out.append("        (void)Fjh;")
         for b in sorted(needed_box):
-            out.append(f"        const int b{b} = box[{b} * bstride];")
-            out.append(f"        const double v{b} = b{b} >= 0 ? Fh[b{b}] : 0.0;")
+            out.append(f"        const double v{b} = Fh[box[{b} * bstride]];")
         for side in (0, 1):
             nm = "sE" if side == 0 else "sA"
             pair = 2 * h + side
@@ -174,15 +173,14 @@ def gen_fb1(name, d, q, etas, out):
                     for st in itertools.product((-1, 0, 1), repeat=d):
                         extra.add(bidx(tuple(pi + si for pi, si in zip(p, st))))
                 for b in sorted(extra - needed_box):
-                    out.append(f"                const int b{b} = box[{b} * bstride];")
-                    out.append(f"                const double v{b} = b{b} >= 0 ? Fh[b{b}] : 0.0;")
+                    out.append(f"                const double v{b} = Fh[box[{b} * bstride]];")
                 for c in rims:
                     r = c[0] if d == 1 else c[0] * 4 + c[1]
                     p = tuple((ci + 1) // 2 - 1 for ci in c)
                     par = tuple((ci + 1) & 1 for ci in c)  # child parity of the rim cell
                     out.append("                {")
                     out.append(f"                    const int sj = rim[{r} * bstride];")
-                    out.append("                    if (sj >= 0 && sj < nLj)")
+                    out.append("                    if (sj >= 0)")
                     out.append("                    {")
                     sv = []
                     for st in itertools.product((-1, 0, 1), repeat=d):

@@ -1,17 +1,19 @@
 // mrlbm_step.cu — B200 (sm_100a) implementation of one adaptive MR-LBM time step
 // (Algorithm 1 body) behind the C-ABI in include/mrlbm_gpu.h.
 //
-// Data layout in HBM, per level m (DESIGN.md §Layout):
-//   map[v][m]   int32 dense over the level box: slot of the cell or -1
-//   cells[v][m] int32 slot -> linear cell index (row-major, last axis fastest)
+// Data layout in HBM, per level m (DESIGN.md §2):
+//   kind2[v][m] uint8 dense over the level box: leaf / internal / virtual (+ fallback)
+//               of tree version v (old and new trees alternate)
+//   cells[v][m] int32 slot -> linear cell index (row-major, last axis fastest);
 //               slots: leaves [0,nL) | internal [nL,nL+nI) | virtual [.., +nV),
 //               each range in lexicographic order == reference CellIndex order
-//               (cell_set.hpp:333-354)
-//   F0/F1[m]    fp64 SoA, one contiguous array per population, stride = level cells
-//   kind/rn/keep uint8 dense scratch flags (rebuilt every step)
-// Two tree versions v alternate (old -> new); F0 holds the state f*, F1 is the
-// transfer / reconstruction buffer.
-//
+//               (cell_set.hpp:333-354); used for iteration and read-back order
+//   F[0/1][m]   fp64 values DENSE over the level box, one contiguous array per
+//               population (index h*cells + linear index): stencil reads are direct
+//               row-coalesced loads, no index lookups.  F[curf] is the state f*;
+//               the transfer is done in place in it and the stream writes the other
+//               buffer, which becomes the next state.
+//   rn/keep/fbm/fbd dense per-step scratch flags
 // Arithmetic mirrors the reference operation order exactly (no FMA: --fmad=false):
 //   project  prediction.hpp:51-60     predict dense_matrix.hpp:42-54 (matvec)
 //   predict  prediction.hpp:143-173   (center + s0 qx + s1 qy - s0 s1 qxy)
@@ -49,9 +51,9 @@ struct Geo {
 };
 
 struct Tree {
-    int32_t* map[kL];
-    int32_t* cells[kL];
-    int* cnt; // [nlev][4] = nL, nI, nV, -
+    uint8_t* kind[kL];  // dense per cell: K_LEAF / K_INT / K_VIRT (+ K_FB) of this tree version
+    int32_t* cells[kL]; // slot -> linear index: leaves | internal | virtual, each lexicographic
+    int* cnt;           // [nlev][4] = nL, nI, nV, -
 };
 
 struct Fld {
@@ -216,31 +218,28 @@ __global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Au
     const long long cap = g.cap[li], cap1 = g.cap[li + 1];
     GRID_STRIDE(s, nL, nL + nI)
     {
+        const int plin = t.cells[li][s];
         int px, py;
-        lin2xy_l<D>(t.cells[m - g.J0][s], ny, g.lny[li], px, py);
+        lin2xy_l<D>(plin, ny, g.lny[li], px, py);
         int cs[1 << D];
-        bool ok = true;
         for (int c = 0; c < (1 << D); ++c)
         {
             const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
-            const int sl = t.map[li + 1][xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)];
-            cs[c] = sl;
-            ok = ok && sl >= 0;
+            cs[c] = xy2lin<D>(2 * px + dx, 2 * py + dy, ny1);
         }
-        if (!ok)
-        {
-            flag_err(aux.err, 0);
-            continue;
-        }
-        #pragma unroll
+        double v[Q];
+#pragma unroll
         for (int h = 0; h < Q; ++h)
         {
             const double* src = F.f[li + 1] + (long long)h * cap1;
             double acc = 0.0;
             for (int c = 0; c < (1 << D); ++c)
                 acc = __dadd_rn(acc, src[cs[c]]);
-            F.f[li][(long long)h * cap + s] = __ddiv_rn(acc, (double)(1 << D));
+            v[h] = __ddiv_rn(acc, (double)(1 << D));
         }
+#pragma unroll
+        for (int h = 0; h < Q; ++h)
+            F.f[li][(long long)h * cap + plin] = v[h];
     }
 }
 
@@ -270,16 +269,15 @@ __global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl,
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            const int sl = t.map[li][mr_lin<D>(g, m, px + ox, py + oy)];
-            st[o] = sl;
-            ok = ok && sl >= 0 && sl < nL + nI;
+            const int lin = mr_lin<D>(g, m, px + ox, py + oy);
+            st[o] = lin;
+            ok = ok && (t.kind[li][lin] & (K_LEAF | K_INT)); // grading: the stencil is in R
         }
         int cs[1 << D];
         for (int c = 0; c < (1 << D); ++c)
         {
             const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
-            cs[c] = t.map[li + 1][xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)];
-            ok = ok && cs[c] >= 0;
+            cs[c] = xy2lin<D>(2 * px + dx, 2 * py + dy, ny1);
         }
         if (!ok)
         {
@@ -970,10 +968,11 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* ki
             for (int w = 0; w < wid; ++w)
                 off += wcount[ct][w];
             const int sl = off + __popc(mk[ct] & lt);
-            map[i] = sl;
+            if (map)
+                map[i] = sl;
             cells[sl] = (int)i;
         }
-        else if (i < n)
+        else if (i < n && map)
             map[i] = -1;
         __syncthreads();
         if (threadIdx.x < 3)
@@ -991,29 +990,20 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* ki
 // new R cell: old value if it was in the old complete tree (copy / projected),
 // else prediction from the new level m-1 values (Decision D.24)
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld F0, Fld F1, int m, Aux aux)
+__global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld S, int m, Aux aux)
 {
+    // in place in the state buffer S: cells of the old complete tree keep their value
+    // (old leaf / projected internal); cells new to the complete tree are predicted
+    // from the (already transferred) new level m-1 values
     const int li = m - g.J0;
     const int nL = tn.cnt[li * 4 + 0], nI = tn.cnt[li * 4 + 1];
-    const int onR = to.cnt[li * 4 + 0] + to.cnt[li * 4 + 1];
     const int ny = g.ny[li];
     const long long cap = g.cap[li];
     GRID_STRIDE(s, 0, nL + nI)
     {
         const int lin = tn.cells[li][s];
-        const int os = to.map[li][lin];
-        if (os >= 0 && os < onR)
-        {
-            // all loads first (F0 and F1 never alias), then the stores
-            double v[Q];
-#pragma unroll
-            for (int h = 0; h < Q; ++h)
-                v[h] = __ldg(F0.f[li] + (long long)h * cap + os);
-#pragma unroll
-            for (int h = 0; h < Q; ++h)
-                F1.f[li][(long long)h * cap + s] = v[h];
+        if (to.kind[li][lin] & (K_LEAF | K_INT))
             continue;
-        }
         if (m == g.J0)
         {
             flag_err(aux.err, 2);
@@ -1024,13 +1014,12 @@ __global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld F
         const int px = x >> 1, py = y >> 1, dx = x & 1, dy = y & 1;
         constexpr int NS = D == 1 ? 3 : 9;
         int st[NS];
-        const int pnR = tn.cnt[(li - 1) * 4 + 0] + tn.cnt[(li - 1) * 4 + 1];
         bool ok = true;
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            st[o] = tn.map[li - 1][mr_lin<D>(g, m - 1, px + ox, py + oy)];
-            ok = ok && st[o] >= 0 && st[o] < pnR;
+            st[o] = mr_lin<D>(g, m - 1, px + ox, py + oy);
+            ok = ok && (tn.kind[li - 1][st[o]] & (K_LEAF | K_INT));
         }
         if (!ok)
         {
@@ -1038,20 +1027,24 @@ __global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld F
             continue;
         }
         const long long capp = g.cap[li - 1];
-        #pragma unroll
+        double v[Q];
+#pragma unroll
         for (int h = 0; h < Q; ++h)
         {
             double sv[NS];
             for (int o = 0; o < NS; ++o)
-                sv[o] = F1.f[li - 1][(long long)h * capp + st[o]];
-            F1.f[li][(long long)h * cap + s] = mr_predict<D>(sv, dx, dy);
+                sv[o] = S.f[li - 1][(long long)h * capp + st[o]];
+            v[h] = mr_predict<D>(sv, dx, dy);
         }
+#pragma unroll
+        for (int h = 0; h < Q; ++h)
+            S.f[li][(long long)h * cap + lin] = v[h];
     }
 }
 
 // virtual cells (ghosts + reconstruction bands): zero-detail prediction from level m-1
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld F1, int m, Aux aux)
+__global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld S, int m, Aux aux)
 {
     const int li = m - g.J0;
     const int nR = tn.cnt[li * 4 + 0] + tn.cnt[li * 4 + 1], nV = tn.cnt[li * 4 + 2];
@@ -1069,22 +1062,26 @@ __global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld F1, int m, 
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            st[o] = tn.map[li - 1][mr_lin<D>(g, m - 1, px + ox, py + oy)];
-            ok = ok && st[o] >= 0;
+            st[o] = mr_lin<D>(g, m - 1, px + ox, py + oy);
+            ok = ok && tn.kind[li - 1][st[o]] != 0;
         }
         if (!ok)
         {
             flag_err(aux.err, 0);
             continue;
         }
-        #pragma unroll
+        double v[Q];
+#pragma unroll
         for (int h = 0; h < Q; ++h)
         {
             double sv[NS];
             for (int o = 0; o < NS; ++o)
-                sv[o] = F1.f[li - 1][(long long)h * capp + st[o]];
-            F1.f[li][(long long)h * cap + s] = mr_predict<D>(sv, dx, dy);
+                sv[o] = S.f[li - 1][(long long)h * capp + st[o]];
+            v[h] = mr_predict<D>(sv, dx, dy);
         }
+#pragma unroll
+        for (int h = 0; h < Q; ++h)
+            S.f[li][(long long)h * cap + lin] = v[h];
     }
 }
 
@@ -1175,8 +1172,8 @@ __device__ __forceinline__ void equilibrium_t(const double* P, double lambda, co
 // materialised zero-detail reconstruction (leaf or virtual slot at J1); outside
 // -> boundary rule by direct evaluation
 template <int D>
-__device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int x,
-                                            int y, int h, int leaf_li, long long leaf_slot, Aux& aux)
+__device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const Fld& S, const SchemeDev* sc, int x,
+                                            int y, int h, int leaf_li, long long leaf_lin, Aux& aux)
 {
     const int lj = g.J1 - g.J0;
     const int nx = g.nx[lj], ny = g.ny[lj];
@@ -1187,9 +1184,9 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         face = y < 0 ? 2 : 3;
     if (face < 0)
     {
-        const int sl = tn.map[lj][mr_lin<D>(g, g.J1, x, y)];
-        if (sl >= 0)
-            return F1.f[lj][(long long)h * g.cap[lj] + sl];
+        const int lin = mr_lin<D>(g, g.J1, x, y);
+        if (tn.kind[lj][lin])
+            return S.f[lj][(long long)h * g.cap[lj] + lin];
         // not materialised (rims of gap-1 leaves): one zero-detail prediction from
         // level J1-1, same operands and order as k_virtual would use
         const int lp = lj - 1;
@@ -1200,13 +1197,13 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            const int ps = tn.map[lp][mr_lin<D>(g, g.J1 - 1, px + ox, py + oy)];
-            if (ps < 0)
+            const int pl = mr_lin<D>(g, g.J1 - 1, px + ox, py + oy);
+            if (!tn.kind[lp][pl])
             {
                 flag_err(aux.err, 0);
                 return 0.0;
             }
-            sv[o] = F1.f[lp][(long long)h * g.cap[lp] + ps];
+            sv[o] = S.f[lp][(long long)h * g.cap[lp] + pl];
         }
         return mr_predict<D>(sv, xc & 1, yc & 1);
     }
@@ -1219,9 +1216,9 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         {
             const int li = m - g.J0;
             const int sh = g.J1 - m;
-            const int sl = tn.map[li][xy2lin<D>(cx >> sh, cy >> sh, g.ny[li])];
-            if (sl >= 0 && sl < tn.cnt[li * 4 + 0])
-                return F1.f[li][(long long)h * g.cap[li] + sl];
+            const int lin = xy2lin<D>(cx >> sh, cy >> sh, g.ny[li]);
+            if (tn.kind[li][lin] & K_LEAF)
+                return S.f[li][(long long)h * g.cap[li] + lin];
         }
         flag_err(aux.err, 0);
         return 0.0;
@@ -1232,7 +1229,7 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         flag_err(aux.err, 2);
         return 0.0;
     }
-    const double v = F1.f[leaf_li][(long long)hb * g.cap[leaf_li] + leaf_slot];
+    const double v = S.f[leaf_li][(long long)hb * g.cap[leaf_li] + leaf_lin];
     if (kind == MRLBM_BC_BOUNCE_BACK)
         return v;
     if (kind == MRLBM_BC_ANTI_BOUNCE_BACK)
@@ -1251,7 +1248,7 @@ __device__ __forceinline__ bool in_box(int x, int y, int bx0, int bx1, int by0, 
 // full rows where the row leaves B, else the single end column.
 template <int D>
 __device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int h, int side, int bx0,
-                          int bx1, int by0, int by1, int leaf_li, long long leaf_slot, Aux& aux)
+                          int bx1, int by0, int by1, int leaf_li, long long leaf_lin, Aux& aux)
 {
     const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
     double s = 0.0;
@@ -1264,13 +1261,13 @@ __device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const Sch
             if (x < bx0 || x >= bx1)
             {
                 if (D == 1)
-                    s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, 0, h, leaf_li, leaf_slot, aux));
+                    s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, 0, h, leaf_li, leaf_lin, aux));
                 else
                     for (int y = by0 - ey; y < by1 - ey; ++y)
-                        s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, y, h, leaf_li, leaf_slot, aux));
+                        s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, y, h, leaf_li, leaf_lin, aux));
             }
             else if (D == 2 && ey != 0)
-                s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, ey > 0 ? by0 - 1 : by1, h, leaf_li, leaf_slot, aux));
+                s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, ey > 0 ? by0 - 1 : by1, h, leaf_li, leaf_lin, aux));
         }
     }
     else
@@ -1280,13 +1277,13 @@ __device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const Sch
             if (x + ex < bx0 || x + ex >= bx1)
             {
                 if (D == 1)
-                    s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, 0, h, leaf_li, leaf_slot, aux));
+                    s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, 0, h, leaf_li, leaf_lin, aux));
                 else
                     for (int y = by0; y < by1; ++y)
-                        s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, y, h, leaf_li, leaf_slot, aux));
+                        s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, y, h, leaf_li, leaf_lin, aux));
             }
             else if (D == 2 && ey != 0)
-                s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, ey > 0 ? by1 - 1 : by0, h, leaf_li, leaf_slot, aux));
+                s = __dadd_rn(s, rim_value<D>(g, tn, F1, sc, x, ey > 0 ? by1 - 1 : by0, h, leaf_li, leaf_lin, aux));
         }
     }
     return s;
@@ -1311,12 +1308,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
         const unsigned mask = aux.fb_mask[it];
         const unsigned dmask = aux.fb_dmask[it];
         const int m = e.x, li = m - g.J0;
-        const long long slot = tn.map[li][e.y];
-        if (slot < 0)
-        {
-            flag_err(aux.err, 2);
-            continue;
-        }
+        const long long slot = e.y; // dense storage: values live at the linear index
         const int ny = g.ny[li];
         const long long cap = g.cap[li];
         int x, y;
@@ -1336,8 +1328,8 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
                 for (int k = ti.x; k < ti.x + ti.y; ++k)
                 {
                     const int2 o = aux.toff[k];
-                    const int sl = tn.map[li][mr_lin<D>(g, m, x + o.x, y + o.y)];
-                    if (sl < 0)
+                    const int sl = mr_lin<D>(g, m, x + o.x, y + o.y);
+                    if (!tn.kind[li][sl])
                     {
                         flag_err(aux.err, 0);
                         continue;
@@ -1349,7 +1341,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
             {
                 // Decision D.13b: add the details of the rim cells that are leaves
                 const int lj = li + 1;
-                const int nyj = g.ny[lj], nLj = tn.cnt[lj * 4 + 0];
+                const int nyj = g.ny[lj];
                 const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
                 const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
                 for (int xr = bx0 - 1; xr <= bx1; ++xr)
@@ -1360,16 +1352,16 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
                         if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
                             continue;
                         const int xc = mr_coord(xr, g.nx[lj], g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
-                        const int sj = tn.map[lj][xy2lin<D>(xc, yc, nyj)];
-                        if (sj < 0 || sj >= nLj)
+                        const int sj = xy2lin<D>(xc, yc, nyj);
+                        if (!(tn.kind[lj][sj] & K_LEAF))
                             continue;
                         constexpr int NS = D == 1 ? 3 : 9;
                         double sv[NS];
                         for (int o = 0; o < NS; ++o)
                         {
                             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-                            const int ps = tn.map[li][mr_lin<D>(g, m, (xc >> 1) + ox, (yc >> 1) + oy)];
-                            sv[o] = ps >= 0 ? F1.f[li][(long long)h * cap + ps] : 0.0;
+                            const int ps = mr_lin<D>(g, m, (xc >> 1) + ox, (yc >> 1) + oy);
+                            sv[o] = F1.f[li][(long long)h * cap + ps];
                         }
                         acc = __dadd_rn(acc, __dsub_rn(F1.f[lj][(long long)h * g.cap[lj] + sj],
                                                        mr_predict<D>(sv, xc & 1, yc & 1)));
@@ -1398,19 +1390,19 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
 // (rim_sum).  Writes post-stream populations into F0; K7 collides them.
 template <int EQ, int Q>
 __device__ __forceinline__ void gen_fb1(const double* Fin, long long cap, const double* Fj, long long capj, const int* box,
-                                        const int* rim, int bstride, int nLj, unsigned mask, unsigned dmask,
+                                        const int* rim, int bstride, unsigned mask, unsigned dmask,
                                         const double* sW, double (&sE)[Q], double (&sA)[Q])
 {
     if constexpr (EQ == 1 && Q == 2)
-        gen_fb1_EQ1(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+        gen_fb1_EQ1(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
     else if constexpr (EQ == 2 && Q == 9)
-        gen_fb1_EQ2(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+        gen_fb1_EQ2(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
     else if constexpr (EQ == 3 && Q == 4)
-        gen_fb1_EQ3(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+        gen_fb1_EQ3(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
     else if constexpr (EQ == 4 && Q == 16)
-        gen_fb1_EQ4(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+        gen_fb1_EQ4(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
     else if constexpr (EQ == 5 && Q == 9)
-        gen_fb1_EQ5(Fin, cap, Fj, capj, box, rim, bstride, nLj, mask, dmask, sW, sE, sA);
+        gen_fb1_EQ5(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
 }
 
 template <int D, int Q, int EQ, bool GEN>
@@ -1440,7 +1432,6 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
         return;
     const int nx = g.nx[li], ny = g.ny[li], nxj = g.nx[lj], nyj = g.ny[lj];
     const long long cap = g.cap[li], capj = g.cap[lj];
-    const int nLj = tn.cnt[lj * 4 + 0];
     const double scale = ldexp(1.0, D * (m - g.J1));
     const int gap = 1;
     (void)nfb;
@@ -1452,7 +1443,7 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
         if ((fl.kind[li][lin] & K_FB) == 0)
             continue;
         const unsigned mask = fl.fbm[li][lin], dmask = fl.fbd[li][lin];
-        const long long slot = sl_;
+        const long long slot = lin; // dense storage
         int x, y;
         lin2xy_l<D>(lin, ny, g.lny[li], x, y);
         for (int b = 0; b < kB; ++b)
@@ -1471,19 +1462,20 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
                 else
                     in = in && yy >= 0 && yy < ny;
             }
-            // clamped slot for out-of-domain stencil cells (MR boundary rule, D.8)
-            sBox[b][threadIdx.x] = tn.map[li][in ? xy2lin<D>(xx, yy, ny) : mr_lin<D>(g, m, x + ox, y + oy)];
+            // linear index, clamped for out-of-domain stencil cells (MR boundary rule, D.8)
+            sBox[b][threadIdx.x] = in ? xy2lin<D>(xx, yy, ny) : mr_lin<D>(g, m, x + ox, y + oy);
         }
         for (int r = 0; r < kR; ++r)
         {
             const int rx = 2 * x - 1 + (D == 1 ? r : r / 4), ry = D == 1 ? 0 : 2 * y - 1 + r % 4;
             bool in = (g.per0 || (rx >= 0 && rx < nxj)) && (D == 1 || g.per1 || (ry >= 0 && ry < nyj));
-            sRim[r][threadIdx.x] = in ? tn.map[lj][mr_lin<D>(g, g.J1, rx, ry)] : -1;
+            const int rl = in ? mr_lin<D>(g, g.J1, rx, ry) : -1;
+            sRim[r][threadIdx.x] = (rl >= 0 && (tn.kind[lj][rl] & K_LEAF)) ? rl : -1; // finest leaves only
         }
         if constexpr (GEN)
         {
             double sE[Q], sA[Q];
-            gen_fb1<EQ, Q>(F1.f[li], cap, F1.f[lj], capj, &sBox[0][threadIdx.x], &sRim[0][threadIdx.x], kT, nLj, mask,
+            gen_fb1<EQ, Q>(F1.f[li], cap, F1.f[lj], capj, &sBox[0][threadIdx.x], &sRim[0][threadIdx.x], kT, mask,
                            dmask, sW, sE, sA);
             if (dmask)
                 for (int h = 0; h < Q; ++h)
@@ -1520,8 +1512,7 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
                     {
                         const int2 o = aux.toff[k];
                         const int b = D == 1 ? o.x + 2 : (o.x + 2) * 5 + (o.y + 2);
-                        const int sl = sBox[b][threadIdx.x];
-                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], sl >= 0 ? Fh[sl] : 0.0));
+                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], Fh[sBox[b][threadIdx.x]]));
                     }
                     if (!ok)
                     {
@@ -1535,7 +1526,7 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
                             if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
                                 continue;
                             const int sj = sRim[r][threadIdx.x];
-                            if (sj < 0 || sj >= nLj)
+                            if (sj < 0)
                                 continue;
                             const int xc = mr_coord(xr, nxj, g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
                             // parent offset from the leaf: ((xc >> 1) - x) in {-1, 0, 1} modulo wrap
@@ -1546,8 +1537,7 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
                             {
                                 const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
                                 const int b = D == 1 ? pdx + ox + 2 : (pdx + ox + 2) * 5 + (pdy + oy + 2);
-                                const int ps = sBox[b][threadIdx.x];
-                                sv[o] = ps >= 0 ? Fh[ps] : 0.0;
+                                sv[o] = Fh[sBox[b][threadIdx.x]];
                             }
                             acc = __dadd_rn(acc, __dsub_rn(Fj[sj], mr_predict<D>(sv, xc & 1, yc & 1)));
                         }
@@ -1568,17 +1558,17 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
 
 // generated unrolled table sums (stream_gen.cuh) for the built-in velocity sets
 template <int EQ, int Q>
-__device__ __forceinline__ void gen_stream(int gap, const double* Fin, long long cap, const int32_t* map, int x, int y,
-                                           int nx, int ny, int per0, int per1, long long s, const double* sW,
-                                           double scale, double (&f)[Q])
+__device__ __forceinline__ void gen_stream(int gap, const double* Fin, long long cap, int x, int y, int nx, int ny,
+                                           int per0, int per1, long long s, const double* sW, double scale,
+                                           double (&f)[Q])
 {
 #define GEN_CALL(N)                                                                                                    \
     if (gap == 0)                                                                                                      \
-        gen_stream_EQ##N##_g0(Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
+        gen_stream_EQ##N##_g0(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
     else if (gap == 1)                                                                                                 \
-        gen_stream_EQ##N##_g1(Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
+        gen_stream_EQ##N##_g1(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
     else                                                                                                               \
-        gen_stream_EQ##N##_g2(Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);
+        gen_stream_EQ##N##_g2(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);
     if constexpr (EQ == 1 && Q == 2)
     {
         GEN_CALL(1)
@@ -1666,7 +1656,6 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
     const double scale = ldexp(1.0, D * (m - g.J1));
     const double* Fin = F1.f[li];
     double* Fout = F0.f[li];
-    const int32_t* map = tn.map[li];
     const int per0 = g.per0, per1 = g.per1;
     int* myslot = &sSlot[0][threadIdx.x];
     GRID_STRIDE(s, 0, nL)
@@ -1681,13 +1670,13 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
             // deep-gap fallback leaf: post-stream populations from K8
 #pragma unroll
             for (int h = 0; h < Q; ++h)
-                f[h] = Fout[(long long)h * cap + s];
+                f[h] = Fout[(long long)h * cap + lin];
         }
         else if (GEN && !fb)
         {
             int x, y;
             lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-            gen_stream<EQ, Q>(gap, Fin, cap, map, x, y, nx, ny, per0, per1, s, sW, scale, f);
+            gen_stream<EQ, Q>(gap, Fin, cap, x, y, nx, ny, per0, per1, lin, sW, scale, f);
         }
         else
         {
@@ -1710,7 +1699,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
                     else
                         in = in && yy >= 0 && yy < ny;
                 }
-                myslot[u * kT] = in ? map[xy2lin<D>(xx, yy, ny)] : -1;
+                myslot[u * kT] = in ? xy2lin<D>(xx, yy, ny) : -1;
             }
             const unsigned mask = fb ? fl.fbm[li][lin] : 0u;
             if (mask)
@@ -1727,7 +1716,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
                     {
                         double acc = 0.0;
                         if ((mask >> (2 * h + side)) & 1u)
-                            acc = rim_sum<D>(g, tn, F1, scg, h, side, bx0, bx1, by0, by1, li, s, aux);
+                            acc = rim_sum<D>(g, tn, F1, scg, h, side, bx0, bx1, by0, by1, li, lin, aux);
                         else
                         {
                             const int2 ti = sIdx[2 * h + side];
@@ -1740,7 +1729,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
                         }
                         sum[side] = acc;
                     }
-                    f[h] = __dadd_rn(Fh[s], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+                    f[h] = __dadd_rn(Fh[lin], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
                 }
             }
             else if (gap == 0)
@@ -1755,7 +1744,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
                     const int2 tE = sIdx[2 * h], tA = sIdx[2 * h + 1];
                     const int slE = tE.y ? myslot[sU[tE.x] * kT] : -1;
                     const int slA = tA.y ? myslot[sU[tA.x] * kT] : -1;
-                    fs[h] = Fh[s];
+                    fs[h] = Fh[lin];
                     vE[h] = slE >= 0 ? Fh[slE] : 0.0;
                     vA[h] = slA >= 0 ? Fh[slA] : 0.0;
                 }
@@ -1774,7 +1763,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
                 for (int h = 0; h < Q; ++h)
                 {
                     const double* Fh = Fin + (long long)h * cap;
-                    const double fs = Fh[s];
+                    const double fs = Fh[lin];
                     double sum[2];
 #pragma unroll
                     for (int side = 0; side < 2; ++side)
@@ -1868,7 +1857,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
         for (int h = 0; h < Q; ++h)
         {
             bad = bad || !isfinite(f[h]);
-            Fout[(long long)h * cap + s] = f[h];
+            Fout[(long long)h * cap + lin] = f[h];
         }
         if (bad)
             flag_err(aux.err, 1);
@@ -1953,20 +1942,30 @@ __global__ void k_lin_to_idx(const int32_t* lin, int n, int d, int ny, int32_t* 
     }
 }
 
-__global__ void k_load_scatter(const int* lins, const double* fin, int n, int q, const int32_t* map, const uint8_t* kind,
-                               double* F, long long cap, int* err)
+__global__ void k_load_scatter(const int* lins, const double* fin, int n, int q, const uint8_t* kind, double* F,
+                               long long cap, int* err)
 {
     GRID_STRIDE(i, 0, n)
     {
         const int lin = lins[i];
-        const int sl = map[lin];
-        if (sl < 0 || kind[lin] != K_LEAF)
+        if (kind[lin] != K_LEAF)
         {
             atomicAdd(&err[2], 1);
             continue;
         }
         for (int h = 0; h < q; ++h)
-            F[(long long)h * cap + sl] = fin[(long long)h * n + i];
+            F[(long long)h * cap + lin] = fin[(long long)h * n + i];
+    }
+}
+
+// read: gather the leaves (slot order) of a level into packed SoA q x n
+__global__ void k_gather_leaves(const int32_t* cells, int n, int q, const double* F, long long cap, double* out)
+{
+    GRID_STRIDE(i, 0, n)
+    {
+        const int lin = cells[i];
+        for (int h = 0; h < q; ++h)
+            out[(long long)h * n + i] = F[(long long)h * cap + lin];
     }
 }
 
@@ -1981,10 +1980,9 @@ struct mrlbm_ctx {
     int D = 0, q = 0, J0 = 0, J1 = 0, nlev = 0;
     Geo geo{};
     cudaStream_t stream = nullptr;
-    int32_t* map[2][kL]{};
     int32_t* cells[2][kL]{};
+    uint8_t* kind2[2][kL]{}; // per tree version: dense cell kinds
     int* cnt[2]{};
-    uint8_t* kind[kL]{};
     uint8_t* rn[kL]{};
     uint8_t* keep[kL]{};
     unsigned* fbmd[kL]{};
@@ -2016,6 +2014,7 @@ struct mrlbm_ctx {
     unsigned short* pmaskd = nullptr;
     unsigned short* umaskd = nullptr;
     int cur = 0;
+    int curf = 0; // F[curf] holds the state f* (dense, indexed by the linear cell index)
     bool committed = false;
     bool profiling = false;
     bool use_graph = true;
@@ -2063,7 +2062,7 @@ Tree tree_of(mrlbm_ctx* c, int v)
     Tree t{};
     for (int i = 0; i < c->nlev; ++i)
     {
-        t.map[i] = c->map[v][i];
+        t.kind[i] = c->kind2[v][i];
         t.cells[i] = c->cells[v][i];
     }
     t.cnt = c->cnt[v];
@@ -2078,12 +2077,12 @@ Fld fld_of(mrlbm_ctx* c, int v)
     return f;
 }
 
-Flags flags_of(mrlbm_ctx* c)
+Flags flags_of(mrlbm_ctx* c, int v)
 {
     Flags f{};
     for (int i = 0; i < c->nlev; ++i)
     {
-        f.kind[i] = c->kind[i];
+        f.kind[i] = c->kind2[v][i];
         f.rn[i] = c->rn[i];
         f.keep[i] = c->keep[i];
         f.fbm[i] = c->fbmd[i];
@@ -2139,11 +2138,11 @@ void launch_compaction(mrlbm_ctx* c, int v, int m)
     const int li = m - c->J0;
     const long long n = c->geo.cap[li];
     const int nt = static_cast<int>(c->ntiles[li]);
-    k_tile_count<<<nt, kTileThreads, 0, c->stream>>>(c->kind[li], n, c->tiles[li]);
+    k_tile_count<<<nt, kTileThreads, 0, c->stream>>>(c->kind2[v][li], n, c->tiles[li]);
     kmark(c, "k_tile_count", m);
     k_tile_scan<<<1, 1024, 0, c->stream>>>(c->tiles[li], nt, c->cnt[v] + li * 4);
     kmark(c, "k_tile_scan", m);
-    k_tile_scatter<<<nt, kTileThreads, 0, c->stream>>>(c->kind[li], n, c->tiles[li], c->cnt[v] + li * 4, c->map[v][li],
+    k_tile_scatter<<<nt, kTileThreads, 0, c->stream>>>(c->kind2[v][li], n, c->tiles[li], c->cnt[v] + li * 4, nullptr,
                                                        c->cells[v][li]);
     kmark(c, "k_tile_scatter", m);
 }
@@ -2176,8 +2175,9 @@ void enqueue_step(mrlbm_ctx* c)
     const int o = c->cur, n = 1 - c->cur;
     const Geo& g = c->geo;
     Tree to = tree_of(c, o), tn = tree_of(c, n);
-    Fld F0 = fld_of(c, 0), F1 = fld_of(c, 1);
-    Flags fl = flags_of(c);
+    // S = state f* (read, transferred in place), T = stream output (next state)
+    Fld Sf = fld_of(c, c->curf), Tf = fld_of(c, 1 - c->curf);
+    Flags fl = flags_of(c, n);
     Aux aux = aux_of(c);
     cudaStream_t s = c->stream;
     const int T = 256;
@@ -2192,11 +2192,11 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 0);
     // K1 projection of the old tree (bottom-up)
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, m, aux);  kmark(c, "k_project", m); }
+        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
     phase_mark(c, 1);
     // K2 details + flags
     for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_details<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, F0, fl, c->sch, m, aux);  kmark(c, "k_details", m); }
+        { c->kcount++; k_details<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, fl, c->sch, m, aux);  kmark(c, "k_details", m); }
     phase_mark(c, 2);
     // K3 closure, enlargement, grading
     for (int m = c->J1 - 1; m > c->J0; --m)
@@ -2248,17 +2248,17 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 4);
     // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_transfer<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, F0, F1, m, aux);  kmark(c, "k_transfer", m); }
+        { c->kcount++; k_transfer<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, Sf, m, aux);  kmark(c, "k_transfer", m); }
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_project", m); }
+        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, Sf, m, aux);  kmark(c, "k_project", m); }
     for (int m = c->J0 + 1; m <= c->J1; ++m)
-        { c->kcount++; k_virtual<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, F1, m, aux);  kmark(c, "k_virtual", m); }
+        { c->kcount++; k_virtual<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, Sf, m, aux);  kmark(c, "k_virtual", m); }
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
-    { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
-    { c->kcount++; k_stream_fb1<D, Q, EQ, GEN><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, F0, F1, fl, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
+    { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
+    { c->kcount++; k_stream_fb1<D, Q, EQ, GEN><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
     for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_stream_collide<D, Q, BS, EQ, GEN><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, F0, F1, fl, c->sch, m, aux);  kmark(c, "k_stream_collide", m); }
+        { c->kcount++; k_stream_collide<D, Q, BS, EQ, GEN><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, m, aux);  kmark(c, "k_stream_collide", m); }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
     phase_mark(c, 6);
     c->kernels_per_step = c->kcount;
@@ -2396,13 +2396,12 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             total_cells += n;
             for (int v = 0; v < 2; ++v)
             {
-                CU(cudaMalloc(&ctx->map[v][li], sizeof(int32_t) * n));
                 CU(cudaMalloc(&ctx->cells[v][li], sizeof(int32_t) * n));
-                CU(cudaMemset(ctx->map[v][li], 0xff, sizeof(int32_t) * n));
+                CU(cudaMalloc(&ctx->kind2[v][li], n));
+                CU(cudaMemset(ctx->kind2[v][li], 0, n));
                 CU(cudaMalloc(&ctx->F[v][li], sizeof(double) * n * ctx->q));
                 CU(cudaMemset(ctx->F[v][li], 0, sizeof(double) * n * ctx->q));
             }
-            CU(cudaMalloc(&ctx->kind[li], n));
             CU(cudaMalloc(&ctx->rn[li], n));
             CU(cudaMalloc(&ctx->keep[li], n));
             CU(cudaMalloc(&ctx->fbmd[li], sizeof(unsigned) * n));
@@ -2623,8 +2622,9 @@ int mrlbm_commit(mrlbm_ctx* ctx)
     if (!ctx)
         return MRLBM_ERR_CONFIG;
     const Geo& g = ctx->geo;
-    Flags fl = flags_of(ctx);
     const int v = ctx->cur;
+    Flags fl = flags_of(ctx, v);
+    ctx->curf = 0;
     for (int li = 0; li < ctx->nlev; ++li)
     {
         CU(cudaMemsetAsync(ctx->keep[li], 0, g.cap[li], ctx->stream));
@@ -2670,8 +2670,8 @@ int mrlbm_commit(mrlbm_ctx* ctx)
             const long long n = ctx->ld_n[li];
             if (!n)
                 continue;
-            k_load_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->ld_lin[li], ctx->F[1][li], (int)n, ctx->q, ctx->map[v][li],
-                                                                     ctx->kind[li], ctx->F[0][li], g.cap[li], ctx->err);
+            k_load_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->ld_lin[li], ctx->F[1][li], (int)n, ctx->q,
+                                                                     ctx->kind2[v][li], ctx->F[0][li], g.cap[li], ctx->err);
         }
         CU(cudaGetLastError());
         int counts[4 * kL];
@@ -2750,6 +2750,7 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
             }
         }
         ctx->cur = 1 - ctx->cur;
+        ctx->curf = 1 - ctx->curf;
     }
     CU(cudaEventRecord(ctx->ev[15], ctx->stream));
     const int st = check_device_errors(ctx);
@@ -2823,9 +2824,10 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
     }
     if (f)
     {
-        for (int h = 0; h < ctx->q; ++h)
-            CU(cudaMemcpyAsync(f + h * n, ctx->F[0][li] + h * ctx->geo.cap[li], sizeof(double) * n,
-                               cudaMemcpyDeviceToHost, ctx->stream));
+        double* stage = ctx->F[1 - ctx->curf][li]; // the non-state buffer is free between steps
+        k_gather_leaves<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->cells[ctx->cur][li], (int)n, ctx->q,
+                                                                   ctx->F[ctx->curf][li], ctx->geo.cap[li], stage);
+        CU(cudaMemcpyAsync(f, stage, sizeof(double) * ctx->q * n, cudaMemcpyDeviceToHost, ctx->stream));
     }
     CU(cudaStreamSynchronize(ctx->stream));
     return MRLBM_OK;
@@ -2895,7 +2897,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         cudaFree(ctx->cnt[v]);
         for (int li = 0; li < kL; ++li)
         {
-            cudaFree(ctx->map[v][li]);
+            cudaFree(ctx->kind2[v][li]);
             cudaFree(ctx->cells[v][li]);
             cudaFree(ctx->F[v][li]);
         }
@@ -2904,7 +2906,6 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     {
         cudaFree(ctx->ld_idx[li]);
         cudaFree(ctx->ld_lin[li]);
-        cudaFree(ctx->kind[li]);
         cudaFree(ctx->rn[li]);
         cudaFree(ctx->keep[li]);
         cudaFree(ctx->fbmd[li]);
