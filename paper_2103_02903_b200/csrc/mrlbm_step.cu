@@ -243,6 +243,52 @@ __global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Au
     }
 }
 
+// K6: projection of the new tree, restricted to "dirty" internal nodes.  A node is
+// dirty if it is new to the complete tree or one of its children is dirty; a clean
+// node keeps the value K1 computed this step (same children, same values, same
+// summation order -> bit-identical).  dirty[] (per level, written for every new
+// internal node) carries the flag bottom-up; leaves are dirty iff not in the old tree.
+template <int D, int Q>
+__global__ void __launch_bounds__(256) k_project_new(Geo g, Tree to, Tree tn, Fld F, int m, uint8_t* const* dirty)
+{
+    const int li = m - g.J0;
+    const int nL = tn.cnt[li * 4 + 0], nI = tn.cnt[li * 4 + 1];
+    const int ny = g.ny[li], ny1 = g.ny[li + 1];
+    const long long cap = g.cap[li], cap1 = g.cap[li + 1];
+    const uint8_t* dchild = dirty[li + 1];
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        const int plin = tn.cells[li][s];
+        int px, py;
+        lin2xy_l<D>(plin, ny, g.lny[li], px, py);
+        int cs[1 << D];
+        bool d = !(to.kind[li][plin] & (K_LEAF | K_INT));
+        for (int c = 0; c < (1 << D); ++c)
+        {
+            const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+            cs[c] = xy2lin<D>(2 * px + dx, 2 * py + dy, ny1);
+            const uint8_t kc = tn.kind[li + 1][cs[c]];
+            d = d || ((kc & K_INT) ? dchild[cs[c]] != 0 : !(to.kind[li + 1][cs[c]] & (K_LEAF | K_INT)));
+        }
+        dirty[li][plin] = d;
+        if (!d)
+            continue;
+        double v[Q];
+#pragma unroll
+        for (int h = 0; h < Q; ++h)
+        {
+            const double* src = F.f[li + 1] + (long long)h * cap1;
+            double acc = 0.0;
+            for (int c = 0; c < (1 << D); ++c)
+                acc = __dadd_rn(acc, src[cs[c]]);
+            v[h] = __ddiv_rn(acc, (double)(1 << D));
+        }
+#pragma unroll
+        for (int h = 0; h < Q; ++h)
+            F.f[li][(long long)h * cap + plin] = v[h];
+    }
+}
+
 // ---------------------------------------------------------------- K2 details
 // d = f - predict; metric = max over siblings and populations
 // (PAPER.md:656); keep iff metric >= eps_l (Eq. 10), blow-up
@@ -862,22 +908,42 @@ __device__ __forceinline__ int cat_of(uint8_t k)
     return (k & K_LEAF) ? 0 : (k & K_INT) ? 1 : (k & K_VIRT) ? 2 : 3;
 }
 
-// tile = kCellsPerThread rounds of kTileThreads consecutive cells (coalesced)
+// tile = kTileThreads threads x kCellsPerThread consecutive cells (one 16-byte load each)
+__device__ __forceinline__ void load16(const uint8_t* kind, long long base, long long n, uint8_t (&b)[16])
+{
+    if (base + 16 <= n)
+    {
+        union {
+            uint4 v;
+            uint8_t c[16];
+        } u;
+        u.v = *reinterpret_cast<const uint4*>(kind + base);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            b[j] = u.c[j];
+    }
+    else
+    {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            b[j] = base + j < n ? kind[base + j] : 0;
+    }
+}
+
 __global__ void __launch_bounds__(kTileThreads) k_tile_count(const uint8_t* kind, long long n, int* tile_counts)
 {
+    static_assert(kCellsPerThread == 16, "one 16-byte load per thread");
     __shared__ int red[3][kTileThreads / 32];
-    const long long base = (long long)blockIdx.x * kTile + threadIdx.x;
+    const long long base = (long long)blockIdx.x * kTile + (long long)threadIdx.x * 16;
+    uint8_t b[16];
+    load16(kind, base, n, b);
     int c[3] = {0, 0, 0};
-#pragma unroll 4
-    for (int r = 0; r < kCellsPerThread; ++r)
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
     {
-        const long long i = base + (long long)r * kTileThreads;
-        if (i < n)
-        {
-            const int ct = cat_of(kind[i]);
-            if (ct < 3)
-                ++c[ct];
-        }
+        c[0] += b[j] & K_LEAF ? 1 : 0;
+        c[1] += b[j] & K_INT ? 1 : 0;
+        c[2] += b[j] & K_VIRT ? 1 : 0;
     }
     for (int k = 0; k < 3; ++k)
     {
@@ -933,56 +999,66 @@ __global__ void k_tile_scan(int* tile_counts, int ntiles, int* cnt)
         }
 }
 
-// ballot + popc ranks inside each warp, warp totals scanned in shared memory,
-// running per-category offsets across the rounds -> lexicographic slots
+// per-thread counts of its 16 cells -> block exclusive scan (warp shuffles + warp
+// totals in shared memory) -> each thread writes its cells' slots in order:
+// lexicographic slots per category
 __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* kind, long long n, const int* tile_offsets,
                                                                const int* cnt, int32_t* map, int32_t* cells)
 {
     constexpr int NW = kTileThreads / 32;
-    __shared__ int wcount[3][NW];
-    __shared__ int run[3];
+    __shared__ int wsum[3][NW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    if (threadIdx.x < 3)
-    {
-        const int catbase = threadIdx.x == 0 ? 0 : threadIdx.x == 1 ? cnt[0] : cnt[0] + cnt[1];
-        run[threadIdx.x] = catbase + tile_offsets[(long long)blockIdx.x * 3 + threadIdx.x];
-    }
-    const long long base = (long long)blockIdx.x * kTile + threadIdx.x;
-    for (int r = 0; r < kCellsPerThread; ++r)
-    {
-        const long long i = base + (long long)r * kTileThreads;
-        const int ct = i < n ? cat_of(kind[i]) : 3;
-        unsigned mk[3];
+    const long long base = (long long)blockIdx.x * kTile + (long long)threadIdx.x * 16;
+    uint8_t b[16];
+    load16(kind, base, n, b);
+    int c[3] = {0, 0, 0};
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
+    for (int j = 0; j < 16; ++j)
+    {
+        c[0] += b[j] & K_LEAF ? 1 : 0;
+        c[1] += b[j] & K_INT ? 1 : 0;
+        c[2] += b[j] & K_VIRT ? 1 : 0;
+    }
+    int pre[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        int v = c[k];
+        for (int o = 1; o < 32; o <<= 1)
         {
-            mk[k] = __ballot_sync(0xffffffffu, ct == k);
-            if (lane == 0)
-                wcount[k][wid] = __popc(mk[k]);
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
         }
-        __syncthreads();
-        if (ct < 3)
+        pre[k] = v - c[k];
+        if (lane == 31)
+            wsum[k][wid] = v;
+    }
+    __syncthreads();
+    const int catbase[3] = {0, cnt[0], cnt[0] + cnt[1]};
+    int pos[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        int wpre = 0;
+        for (int w = 0; w < wid; ++w)
+            wpre += wsum[k][w];
+        pos[k] = catbase[k] + tile_offsets[(long long)blockIdx.x * 3 + k] + wpre + pre[k];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+    {
+        const long long i = base + j;
+        const int ct = cat_of(b[j]);
+        if (i < n && ct < 3)
         {
-            int off = run[ct];
-            for (int w = 0; w < wid; ++w)
-                off += wcount[ct][w];
-            const int sl = off + __popc(mk[ct] & lt);
+            const int sl = pos[ct]++;
             if (map)
                 map[i] = sl;
             cells[sl] = (int)i;
         }
         else if (i < n && map)
             map[i] = -1;
-        __syncthreads();
-        if (threadIdx.x < 3)
-        {
-            int t = 0;
-            for (int w = 0; w < NW; ++w)
-                t += wcount[threadIdx.x][w];
-            run[threadIdx.x] += t;
-        }
-        __syncthreads();
     }
 }
 
@@ -1985,6 +2061,7 @@ struct mrlbm_ctx {
     int* cnt[2]{};
     uint8_t* rn[kL]{};
     uint8_t* keep[kL]{};
+    uint8_t** dirty_d = nullptr; // device array of keep[] pointers (K6 dirty flags; keep is free after K4)
     unsigned* fbmd[kL]{};
     unsigned* fbdd[kL]{};
     double* F[2][kL]{};
@@ -2250,7 +2327,7 @@ void enqueue_step(mrlbm_ctx* c)
     for (int m = c->J0; m <= c->J1; ++m)
         { c->kcount++; k_transfer<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, Sf, m, aux);  kmark(c, "k_transfer", m); }
     for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, Sf, m, aux);  kmark(c, "k_project", m); }
+        { c->kcount++; k_project_new<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, tn, Sf, m, c->dirty_d);  kmark(c, "k_project_new", m); }
     for (int m = c->J0 + 1; m <= c->J1; ++m)
         { c->kcount++; k_virtual<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, Sf, m, aux);  kmark(c, "k_virtual", m); }
     phase_mark(c, 5);
@@ -2410,6 +2487,8 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             CU(cudaMalloc(&ctx->tiles[li], sizeof(int) * 3 * ctx->ntiles[li]));
         }
         ctx->fbcap = total_cells;
+        CU(cudaMalloc(&ctx->dirty_d, sizeof(uint8_t*) * kL));
+        CU(cudaMemcpy(ctx->dirty_d, ctx->keep, sizeof(uint8_t*) * kL, cudaMemcpyHostToDevice));
         CU(cudaMalloc(&ctx->fbl, sizeof(int2) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbm, sizeof(unsigned) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbdm, sizeof(unsigned) * ctx->fbcap));
@@ -2913,6 +2992,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         cudaFree(ctx->tiles[li]);
     }
     cudaFree(ctx->sch);
+    cudaFree(ctx->dirty_d);
     cudaFree(ctx->ld_bad);
     cudaFree(ctx->err);
     cudaFree(ctx->fbc);
