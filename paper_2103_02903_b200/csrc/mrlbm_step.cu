@@ -207,6 +207,35 @@ __device__ __forceinline__ void flag_err(int* err, int which)
     for (long long i = (long long)(begin) + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)(end); \
          i += (long long)gridDim.x * blockDim.x)
 
+// Multi-level launches: one grid covers several levels; block ranges per level are
+// prefix sums computed on the host.  Each block derives its level and its block
+// index / count within the level (grid-stride loops then run per level).
+struct LGrid {
+    int start[kL + 1];
+    int m0, nl;
+};
+
+__device__ __forceinline__ void lgrid_setup(const LGrid& lg, int& m, int& lvb, int& lvg)
+{
+    int i = 0;
+    while (i + 1 < lg.nl && (int)blockIdx.x >= lg.start[i + 1])
+        ++i;
+    m = lg.m0 + i;
+    lvb = (int)blockIdx.x - lg.start[i];
+    lvg = lg.start[i + 1] - lg.start[i];
+}
+
+#define LGRID_STRIDE(i, begin, end)                                                                                  \
+    for (long long i = (long long)(begin) + (long long)lvb_ * blockDim.x + threadIdx.x; i < (long long)(end);      \
+         i += (long long)lvg_ * blockDim.x)
+#define LSETUP                                                                                                      \
+    int m, lvb_, lvg_;                                                                                              \
+    lgrid_setup(lg_, m, lvb_, lvg_)
+
+struct TileP {
+    int* t[kL];
+};
+
 // ---------------------------------------------------------------- K1 / K6 project
 // internal value = (sum of the 2^D children in children order) / 2^D   (prediction.hpp:51-60)
 template <int D, int Q>
@@ -294,8 +323,9 @@ __global__ void __launch_bounds__(256) k_project_new(Geo g, Tree to, Tree tn, Fl
 // (PAPER.md:656); keep iff metric >= eps_l (Eq. 10), blow-up
 // refinement iff metric >= 2^{mu+D} eps_l
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, int m, Aux aux)
+__global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, LGrid lg_, Aux aux)
 {
+    LSETUP;
     const int li = m - g.J0;
     const int l = m + 1;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
@@ -304,7 +334,7 @@ __global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl,
     const double eps_l = ldexp(sc->eps, D * (l - g.J1));
     const double eps_b = ldexp(eps_l, sc->mu + D);
     const bool can_b = (l > g.J0) && (l < g.J1);
-    GRID_STRIDE(s, nL, nL + nI)
+    LGRID_STRIDE(s, nL, nL + nI)
     {
         const int plin = t.cells[li][s];
         int px, py;
@@ -383,13 +413,14 @@ __global__ void k_closure(Geo g, Tree t, Flags fl, int m)
 
 // rn |= keep;  H(a): (l, k - eta^h) for k in R(T) at level l = m + 1
 template <int D>
-__global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, int m, unsigned emask)
+__global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, LGrid lg_, unsigned emask)
 {
+    LSETUP;
     (void)sc;
     const int li = m - g.J0;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
     const int ny = g.ny[li];
-    GRID_STRIDE(s, nL, nL + nI)
+    LGRID_STRIDE(s, nL, nL + nI)
     {
         const int plin = t.cells[li][s];
         if (!fl.keep[li][plin])
@@ -450,12 +481,13 @@ __global__ void k_grade(Geo g, Flags fl, int m)
 
 // ---------------------------------------------------------------- K4 kinds, fallback, ghosts, compaction
 template <int D>
-__global__ void k_kinds(Geo g, Flags fl, int m)
+__global__ void k_kinds(Geo g, Flags fl, LGrid lg_)
 {
+    LSETUP;
     const int li = m - g.J0;
     const int ny = g.ny[li], nyp = li > 0 ? g.ny[li - 1] : 1;
     const long long n = (long long)g.nx[li] * ny;
-    GRID_STRIDE(i, 0, n)
+    LGRID_STRIDE(i, 0, n)
     {
         int x, y;
         lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
@@ -570,12 +602,14 @@ __global__ void __launch_bounds__(256) k_band(Geo g, Flags fl, Aux aux)
 // 2D: separable dilation, pass 1 ORs R-membership over y +-2 into tmp, pass 2
 // ORs tmp over x +-2 (10 byte reads per cell instead of 25).
 template <int D>
-__global__ void k_ghost_rows(Geo g, Flags fl, int m, uint8_t* tmp)
+__global__ void k_ghost_rows(Geo g, Flags fl, LGrid lg_)
 {
+    LSETUP;
     const int li = m - g.J0;
+    uint8_t* tmp = fl.keep[li];
     const int nx = g.nx[li], ny = g.ny[li];
     const long long n = (long long)nx * ny;
-    GRID_STRIDE(i, 0, n)
+    LGRID_STRIDE(i, 0, n)
     {
         int x, y;
         lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
@@ -597,12 +631,14 @@ __global__ void k_ghost_rows(Geo g, Flags fl, int m, uint8_t* tmp)
 }
 
 template <int D>
-__global__ void k_ghost(Geo g, Flags fl, int m, const uint8_t* tmp)
+__global__ void k_ghost(Geo g, Flags fl, LGrid lg_)
 {
+    LSETUP;
     const int li = m - g.J0;
+    const uint8_t* tmp = fl.keep[li];
     const int nx = g.nx[li], ny = g.ny[li];
     const long long n = (long long)nx * ny;
-    GRID_STRIDE(i, 0, n)
+    LGRID_STRIDE(i, 0, n)
     {
         if (fl.kind[li][i] != 0)
             continue;
@@ -641,15 +677,16 @@ union V16 {
     uint8_t b[16];
 };
 
-__global__ void k_kinds_v(Geo g, Flags fl, int m)
+__global__ void k_kinds_v(Geo g, Flags fl, LGrid lg_)
 {
+    LSETUP;
     const int li = m - g.J0;
     const int ny = g.ny[li], nyp = li > 0 ? g.ny[li - 1] : 1;
     const long long nch = (long long)g.nx[li] * ny / 16;
     const uint8_t* rn = fl.rn[li];
     const uint8_t* rnp = li > 0 ? fl.rn[li - 1] : nullptr;
     const bool top = m == g.J0, fin = m == g.J1;
-    CHUNK_STRIDE(c, nch)
+    LGRID_STRIDE(c, 0, nch)
     {
         const int lin0 = (int)(c * 16);
         const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
@@ -672,7 +709,8 @@ __global__ void k_kinds_v(Geo g, Flags fl, int m)
 // fallback flags: chunks without a plain leaf are skipped with one load
 template <int D>
 __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int m, int li, int gap, long long i, int x,
-                                              int y, const int4& ub, const int2& pi, Aux& aux, int ib_in = -1)
+                                              int y, const int4& ub, const int2& pi, Aux& aux, int ib_in = -1,
+                                              const int4* sdep = nullptr, const unsigned short* spm = nullptr)
 {
     (void)pi;
     const int nx = g.nx[li], ny = g.ny[li];
@@ -711,9 +749,9 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     for (int pair = 0; pair < 2 * g.q; ++pair)
     {
         const int key = gap * 2 * g.q + pair;
-        const int4 db = aux.tdep[key];
+        const int4 db = sdep ? sdep[pair] : aux.tdep[key];
         const bool dom = !((!g.per0 && (x + db.x < 0 || x + db.y >= nx)) || (D == 2 && !g.per1 && (y + db.z < 0 || y + db.w >= ny)));
-        const bool ok = dom && !(ib & aux.pmask[key]);
+        const bool ok = dom && !(ib & (spm ? spm[pair] : aux.pmask[key]));
         if (!ok)
             mask |= 1u << pair;
         if (!dom)
@@ -745,15 +783,16 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
 }
 
 template <int D>
-__global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
+__global__ void k_fallback(Geo g, Flags fl, LGrid lg_, Aux aux)
 {
+    LSETUP;
     const int li = m - g.J0;
     const int gap = g.J1 - m;
     const int ny = g.ny[li];
     const long long n = (long long)g.nx[li] * ny;
     const int4 ub = aux.udep[gap];
     const int2 pi = aux.upidx[gap];
-    GRID_STRIDE(i, 0, n)
+    LGRID_STRIDE(i, 0, n)
     {
         if (fl.kind[li][i] != K_LEAF)
             continue;
@@ -763,15 +802,24 @@ __global__ void k_fallback(Geo g, Flags fl, int m, Aux aux)
     }
 }
 
-__global__ void k_fallback_v(Geo g, Flags fl, int m, Aux aux)
+__global__ void k_fallback_v(Geo g, Flags fl, LGrid lg_, Aux aux)
 {
+    LSETUP;
+    __shared__ int4 sdep[2 * kQ];
+    __shared__ unsigned short spm[2 * kQ];
     const int li = m - g.J0;
     const int gap = g.J1 - m;
+    for (int t = threadIdx.x; t < 2 * g.q; t += blockDim.x)
+    {
+        sdep[t] = aux.tdep[gap * 2 * g.q + t];
+        spm[t] = aux.pmask[gap * 2 * g.q + t];
+    }
+    __syncthreads();
     const int ny = g.ny[li];
     const long long nch = (long long)g.nx[li] * ny / 16;
     const int4 ub = aux.udep[gap];
     const int2 pi = aux.upidx[gap];
-    CHUNK_STRIDE(c, nch)
+    LGRID_STRIDE(c, 0, nch)
     {
         V16 k;
         k.v = reinterpret_cast<const uint4*>(fl.kind[li])[c];
@@ -808,19 +856,21 @@ __global__ void k_fallback_v(Geo g, Flags fl, int m, Aux aux)
 #pragma unroll
                 for (int o = 0; o < 9; ++o)
                     ib |= (w[o / 3][j + (o % 3)] ? 1 : 0) << o;
-                fallback_cell<2>(g, fl, m, li, gap, lin0 + j, x, y0 + j, ub, pi, aux, ib);
+                fallback_cell<2>(g, fl, m, li, gap, lin0 + j, x, y0 + j, ub, pi, aux, ib, sdep, spm);
             }
     }
 }
 
 // ghost rows: tmp = OR of R membership over y +- 2 (same row)
-__global__ void k_ghost_rows_v(Geo g, Flags fl, int m, uint8_t* tmp)
+__global__ void k_ghost_rows_v(Geo g, Flags fl, LGrid lg_)
 {
+    LSETUP;
     const int li = m - g.J0;
+    uint8_t* tmp = fl.keep[li];
     const int ny = g.ny[li];
     const long long nch = (long long)g.nx[li] * ny / 16;
     const uint8_t* kind = fl.kind[li];
-    CHUNK_STRIDE(c, nch)
+    LGRID_STRIDE(c, 0, nch)
     {
         const int lin0 = (int)(c * 16);
         const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
@@ -850,13 +900,15 @@ __global__ void k_ghost_rows_v(Geo g, Flags fl, int m, uint8_t* tmp)
 }
 
 // ghosts: empty cells with an R cell within +-2 rows of tmp
-__global__ void k_ghost_v(Geo g, Flags fl, int m, const uint8_t* tmp)
+__global__ void k_ghost_v(Geo g, Flags fl, LGrid lg_)
 {
+    LSETUP;
     const int li = m - g.J0;
+    const uint8_t* tmp = fl.keep[li];
     const int nx = g.nx[li], ny = g.ny[li];
     const long long nch = (long long)nx * ny / 16;
     const int cpr = ny / 16; // chunks per row
-    CHUNK_STRIDE(c, nch)
+    LGRID_STRIDE(c, 0, nch)
     {
         V16 k;
         k.v = reinterpret_cast<const uint4*>(fl.kind[li])[c];
@@ -1059,6 +1111,147 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* ki
         }
         else if (i < n && map)
             map[i] = -1;
+    }
+}
+
+// multi-level compaction: block range per level = that level's tiles (count,
+// scatter) or one block per level (scan)
+__global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(Geo g, Flags fl, TileP tp, LGrid lg_)
+{
+    LSETUP;
+    (void)lvg_;
+    const int li = m - g.J0;
+    const long long n = g.cap[li];
+    const uint8_t* kind = fl.kind[li];
+    __shared__ int red[3][kTileThreads / 32];
+    const long long base = (long long)lvb_ * kTile + (long long)threadIdx.x * 16;
+    uint8_t b[16];
+    load16(kind, base, n, b);
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+    {
+        c[0] += b[j] & K_LEAF ? 1 : 0;
+        c[1] += b[j] & K_INT ? 1 : 0;
+        c[2] += b[j] & K_VIRT ? 1 : 0;
+    }
+    for (int k = 0; k < 3; ++k)
+    {
+        int v = c[k];
+        for (int o = 16; o > 0; o >>= 1)
+            v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0)
+            red[k][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3)
+    {
+        int v = 0;
+        for (int w = 0; w < kTileThreads / 32; ++w)
+            v += red[threadIdx.x][w];
+        tp.t[li][(long long)lvb_ * 3 + threadIdx.x] = v;
+    }
+}
+
+__global__ void k_tile_scan_ml(Geo g, TileP tp, Tree tn, LGrid lg_)
+{
+    LSETUP;
+    (void)lvb_;
+    (void)lvg_;
+    const int li = m - g.J0;
+    const int ntiles = (int)((g.cap[li] + kTile - 1) / kTile);
+    int* tile_counts = tp.t[li];
+    int* cnt = tn.cnt + li * 4;
+    __shared__ int part[3][1024];
+    const int T = blockDim.x;
+    const int per = (ntiles + T - 1) / T;
+    const int b = threadIdx.x * per, e = min(ntiles, b + per);
+    int loc[3] = {0, 0, 0};
+    for (int t = b; t < e; ++t)
+        for (int k = 0; k < 3; ++k)
+            loc[k] += tile_counts[t * 3 + k];
+    for (int k = 0; k < 3; ++k)
+        part[k][threadIdx.x] = loc[k];
+    __syncthreads();
+    if (threadIdx.x < 3)
+    {
+        int run = 0;
+        for (int i = 0; i < T; ++i)
+        {
+            const int v = part[threadIdx.x][i];
+            part[threadIdx.x][i] = run;
+            run += v;
+        }
+        cnt[threadIdx.x] = run;
+    }
+    __syncthreads();
+    int run[3] = {part[0][threadIdx.x], part[1][threadIdx.x], part[2][threadIdx.x]};
+    for (int t = b; t < e; ++t)
+        for (int k = 0; k < 3; ++k)
+        {
+            const int v = tile_counts[t * 3 + k];
+            tile_counts[t * 3 + k] = run[k];
+            run[k] += v;
+        }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags fl, TileP tp, Tree tn, LGrid lg_)
+{
+    LSETUP;
+    (void)lvg_;
+    const int li = m - g.J0;
+    const long long n = g.cap[li];
+    const uint8_t* kind = fl.kind[li];
+    const int* tile_offsets = tp.t[li];
+    const int* cnt = tn.cnt + li * 4;
+    int32_t* cells = tn.cells[li];
+    constexpr int NW = kTileThreads / 32;
+    __shared__ int wsum[3][NW];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long long base = (long long)lvb_ * kTile + (long long)threadIdx.x * 16;
+    uint8_t b[16];
+    load16(kind, base, n, b);
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+    {
+        c[0] += b[j] & K_LEAF ? 1 : 0;
+        c[1] += b[j] & K_INT ? 1 : 0;
+        c[2] += b[j] & K_VIRT ? 1 : 0;
+    }
+    int pre[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        int v = c[k];
+        for (int o = 1; o < 32; o <<= 1)
+        {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
+        }
+        pre[k] = v - c[k];
+        if (lane == 31)
+            wsum[k][wid] = v;
+    }
+    __syncthreads();
+    const int catbase[3] = {0, cnt[0], cnt[0] + cnt[1]};
+    int pos[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        int wpre = 0;
+        for (int w = 0; w < wid; ++w)
+            wpre += wsum[k][w];
+        pos[k] = catbase[k] + tile_offsets[(long long)lvb_ * 3 + k] + wpre + pre[k];
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+    {
+        const long long i = base + j;
+        const int ct = cat_of(b[j]);
+        if (i < n && ct < 3)
+            cells[pos[ct]++] = (int)i;
     }
 }
 
@@ -1673,8 +1866,9 @@ __device__ __forceinline__ void gen_stream(int gap, const double* Fin, long long
 // populations from K8 (already in F0).  BS = block size of the block-diagonal M.
 template <int D, int Q, int BS, int EQ, bool GEN>
 __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F0, Fld F1, Flags fl,
-                                                           const SchemeDev* scg, int m, Aux aux)
+                                                           const SchemeDev* scg, LGrid lg_, Aux aux)
 {
+    LSETUP;
     constexpr int kMaxE = 2 * Q * 25;
     constexpr int kU = D == 1 ? 5 : 25; // distinct table offsets at one gap (5^D box)
     constexpr int kT = 256;
@@ -1734,7 +1928,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
     double* Fout = F0.f[li];
     const int per0 = g.per0, per1 = g.per1;
     int* myslot = &sSlot[0][threadIdx.x];
-    GRID_STRIDE(s, 0, nL)
+    LGRID_STRIDE(s, 0, nL)
     {
         const int lin = tn.cells[li][s];
         const uint8_t kd = fl.kind[li][lin];
@@ -2208,21 +2402,6 @@ int grid_for(mrlbm_ctx* c, long long n, int threads = 256)
 
 void kmark(mrlbm_ctx* c, const char* name, int level);
 
-template <int D>
-void launch_compaction(mrlbm_ctx* c, int v, int m)
-{
-    c->kcount += 3;
-    const int li = m - c->J0;
-    const long long n = c->geo.cap[li];
-    const int nt = static_cast<int>(c->ntiles[li]);
-    k_tile_count<<<nt, kTileThreads, 0, c->stream>>>(c->kind2[v][li], n, c->tiles[li]);
-    kmark(c, "k_tile_count", m);
-    k_tile_scan<<<1, 1024, 0, c->stream>>>(c->tiles[li], nt, c->cnt[v] + li * 4);
-    kmark(c, "k_tile_scan", m);
-    k_tile_scatter<<<nt, kTileThreads, 0, c->stream>>>(c->kind2[v][li], n, c->tiles[li], c->cnt[v] + li * 4, nullptr,
-                                                       c->cells[v][li]);
-    kmark(c, "k_tile_scatter", m);
-}
 
 void kmark(mrlbm_ctx* c, const char* name, int level)
 {
@@ -2238,6 +2417,45 @@ void kmark(mrlbm_ctx* c, const char* name, int level)
     cudaEventRecord(c->kev[c->kn], c->stream);
     c->klabel[c->kn] = {name, level};
     ++c->kn;
+}
+
+// block ranges of a multi-level launch over levels [m0, m1]
+template <class Blocks>
+LGrid make_lgrid(mrlbm_ctx* c, int m0, int m1, Blocks&& blocks, int* total)
+{
+    LGrid lg{};
+    lg.m0 = m0;
+    lg.nl = m1 - m0 + 1;
+    lg.start[0] = 0;
+    for (int i = 0; i < lg.nl; ++i)
+        lg.start[i + 1] = lg.start[i] + static_cast<int>(blocks(m0 + i - c->J0));
+    *total = lg.start[lg.nl];
+    return lg;
+}
+
+TileP tiles_of(mrlbm_ctx* c)
+{
+    TileP t{};
+    for (int i = 0; i < c->nlev; ++i)
+        t.t[i] = c->tiles[i];
+    return t;
+}
+
+// compaction of every level of tree version v: tile counts, per-level scans, scatter
+void launch_compaction_all(mrlbm_ctx* c, const Geo& g, Flags fl, Tree tv)
+{
+    TileP tp = tiles_of(c);
+    int nb = 0;
+    LGrid lt = make_lgrid(c, c->J0, c->J1, [&](int li) { return c->ntiles[li]; }, &nb);
+    k_tile_count_ml<<<nb, kTileThreads, 0, c->stream>>>(g, fl, tp, lt);
+    kmark(c, "k_tile_count", -1);
+    int ns = 0;
+    LGrid ls = make_lgrid(c, c->J0, c->J1, [&](int) { return 1; }, &ns);
+    k_tile_scan_ml<<<ns, 1024, 0, c->stream>>>(g, tp, tv, ls);
+    kmark(c, "k_tile_scan", -1);
+    k_tile_scatter_ml<<<nb, kTileThreads, 0, c->stream>>>(g, fl, tp, tv, lt);
+    kmark(c, "k_tile_scatter", -1);
+    c->kcount += 3;
 }
 
 void phase_mark(mrlbm_ctx* c, int k)
@@ -2272,56 +2490,86 @@ void enqueue_step(mrlbm_ctx* c)
         { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
     phase_mark(c, 1);
     // K2 details + flags
-    for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_details<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, fl, c->sch, m, aux);  kmark(c, "k_details", m); }
+    int nb = 0;
+    {
+        LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
+        c->kcount++;
+        k_details<D, Q><<<nb, T, 0, s>>>(g, to, Sf, fl, c->sch, lg, aux);
+        kmark(c, "k_details", -1);
+    }
     phase_mark(c, 2);
     // K3 closure, enlargement, grading
     for (int m = c->J1 - 1; m > c->J0; --m)
         { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);  kmark(c, "k_closure", m); }
-    for (int m = c->J0; m < c->J1; ++m)
-        { c->kcount++; k_enlarge<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, c->sch, m, c->emask);  kmark(c, "k_enlarge", m); }
+    {
+        LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
+        c->kcount++;
+        k_enlarge<D><<<nb, T, 0, s>>>(g, to, fl, c->sch, lg, c->emask);
+        kmark(c, "k_enlarge", -1);
+    }
     for (int m = c->J1 - 1; m > c->J0; --m)
         { c->kcount++; k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);  kmark(c, "k_grade", m); }
     phase_mark(c, 3);
     // K4 kinds, fallback flags, reconstruction bands, ghosts, compaction
     auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
-    for (int m = c->J0; m <= c->J1; ++m)
+    // levels [J0, mv) use the scalar dense kernels, [mv, J1] the 16-cell vector ones
+    int mv = c->J1 + 1;
+    for (int m = c->J1; m >= c->J0 && vec_ok(m); --m)
+        mv = m;
+    auto blocks_s = [&](int li) { return grid_for(c, g.cap[li], T); };
+    auto blocks_v = [&](int li) { return grid_for(c, g.cap[li] / 16, T); };
+    if (mv > c->J0)
     {
+        LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
         c->kcount++;
-        if (vec_ok(m))
-            k_kinds_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m);
-        else
-            k_kinds<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
-        kmark(c, "k_kinds", m);
+        k_kinds<D><<<nb, T, 0, s>>>(g, fl, lg);
+        kmark(c, "k_kinds", -1);
     }
-    for (int m = c->J0; m <= c->J1; ++m)
+    if (mv <= c->J1)
     {
+        LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
         c->kcount++;
-        if (vec_ok(m))
-            k_fallback_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m, aux);
-        else
-            k_fallback<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, aux);
-        kmark(c, "k_fallback", m);
+        k_kinds_v<<<nb, T, 0, s>>>(g, fl, lg);
+        kmark(c, "k_kinds_v", -1);
+    }
+    if (mv > c->J0)
+    {
+        LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
+        c->kcount++;
+        k_fallback<D><<<nb, T, 0, s>>>(g, fl, lg, aux);
+        kmark(c, "k_fallback", -1);
+    }
+    if (mv <= c->J1)
+    {
+        LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
+        c->kcount++;
+        k_fallback_v<<<nb, T, 0, s>>>(g, fl, lg, aux);
+        kmark(c, "k_fallback_v", -1);
     }
     { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);  kmark(c, "k_band", -1); }
-    for (int m = c->J0; m <= c->J1; ++m)
+    if (mv > c->J0)
     {
-        uint8_t* tmp = c->keep[m - c->J0];
-        if (vec_ok(m))
-        {
-            c->kcount += 2;
-            k_ghost_rows_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m, tmp);
-            kmark(c, "k_ghost_rows_v", m);
-            k_ghost_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m, tmp);
-            kmark(c, "k_ghost_v", m);
-            continue;
-        }
+        LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
         if (D == 2)
-            { c->kcount++; k_ghost_rows<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, tmp);  kmark(c, "k_ghost_rows", m); }
-        { c->kcount++; k_ghost<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m, tmp);  kmark(c, "k_ghost", m); }
+        {
+            c->kcount++;
+            k_ghost_rows<D><<<nb, T, 0, s>>>(g, fl, lg);
+            kmark(c, "k_ghost_rows", -1);
+        }
+        c->kcount++;
+        k_ghost<D><<<nb, T, 0, s>>>(g, fl, lg);
+        kmark(c, "k_ghost", -1);
     }
-    for (int m = c->J0; m <= c->J1; ++m)
-        launch_compaction<D>(c, n, m);
+    if (mv <= c->J1)
+    {
+        LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
+        c->kcount += 2;
+        k_ghost_rows_v<<<nb, T, 0, s>>>(g, fl, lg);
+        kmark(c, "k_ghost_rows_v", -1);
+        k_ghost_v<<<nb, T, 0, s>>>(g, fl, lg);
+        kmark(c, "k_ghost_v", -1);
+    }
+    launch_compaction_all(c, g, fl, tn);
     phase_mark(c, 4);
     // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
     for (int m = c->J0; m <= c->J1; ++m)
@@ -2334,8 +2582,12 @@ void enqueue_step(mrlbm_ctx* c)
     // K7/K8 stream + collide (+ obstacle) on every new leaf
     { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
     { c->kcount++; k_stream_fb1<D, Q, EQ, GEN><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
-    for (int m = c->J0; m <= c->J1; ++m)
-        { c->kcount++; k_stream_collide<D, Q, BS, EQ, GEN><<<grid_for(c, g.cap[m - c->J0], 256), 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, m, aux);  kmark(c, "k_stream_collide", m); }
+    {
+        LGrid lg = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
+        c->kcount++;
+        k_stream_collide<D, Q, BS, EQ, GEN><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux);
+        kmark(c, "k_stream_collide", -1);
+    }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
     phase_mark(c, 6);
     c->kernels_per_step = c->kcount;
@@ -2731,18 +2983,14 @@ int mrlbm_commit(mrlbm_ctx* ctx)
             else
                 k_closure_dense<2><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
         }
-        for (int m = ctx->J0; m <= ctx->J1; ++m)
         {
+            int nbk = 0;
+            LGrid lg = make_lgrid(ctx, ctx->J0, ctx->J1, [&](int li) { return grid_for(ctx, g.cap[li]); }, &nbk);
             if (ctx->D == 1)
-            {
-                k_kinds<1><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
-                launch_compaction<1>(ctx, v, m);
-            }
+                k_kinds<1><<<nbk, 256, 0, ctx->stream>>>(g, fl, lg);
             else
-            {
-                k_kinds<2><<<grid_for(ctx, g.cap[m - ctx->J0]), 256, 0, ctx->stream>>>(g, fl, m);
-                launch_compaction<2>(ctx, v, m);
-            }
+                k_kinds<2><<<nbk, 256, 0, ctx->stream>>>(g, fl, lg);
+            launch_compaction_all(ctx, g, fl, tree_of(ctx, v));
         }
         for (int li = 0; li < ctx->nlev; ++li)
         {
