@@ -236,6 +236,27 @@ struct TileP {
     int* t[kL];
 };
 
+// zero the per-step keep / rn flags of every level (16 bytes per thread)
+__global__ void k_zero_flags(Geo g, Flags fl, LGrid lg_, int* fbc)
+{
+    LSETUP;
+    const int li = m - g.J0;
+    const long long n16 = g.cap[li] / 16, n = g.cap[li];
+    if (blockIdx.x == 0 && threadIdx.x < 2)
+        fbc[threadIdx.x] = 0;
+    LGRID_STRIDE(i, 0, n16)
+    {
+        reinterpret_cast<uint4*>(fl.keep[li])[i] = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(fl.rn[li])[i] = make_uint4(0, 0, 0, 0);
+    }
+    if (lvb_ == 0)
+        for (long long i = n16 * 16 + threadIdx.x; i < n; i += blockDim.x)
+        {
+            fl.keep[li][i] = 0;
+            fl.rn[li][i] = 0;
+        }
+}
+
 // ---------------------------------------------------------------- K1 / K6 project
 // internal value = (sum of the 2^D children in children order) / 2^D   (prediction.hpp:51-60)
 template <int D, int Q>
@@ -2478,19 +2499,19 @@ void enqueue_step(mrlbm_ctx* c)
     const int T = 256;
     c->kcount = 0;
     c->kn = 0;
-    for (int li = 0; li < c->nlev; ++li)
+    int nb = 0;
     {
-        cudaMemsetAsync(c->keep[li], 0, g.cap[li], s);
-        cudaMemsetAsync(c->rn[li], 0, g.cap[li], s);
+        LGrid lz = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 16 + 1, T); }, &nb);
+        c->kcount++;
+        k_zero_flags<<<nb, T, 0, s>>>(g, fl, lz, c->fbc);
+        kmark(c, "k_zero_flags", -1);
     }
-    cudaMemsetAsync(c->fbc, 0, 2 * sizeof(int), s);
     phase_mark(c, 0);
     // K1 projection of the old tree (bottom-up)
     for (int m = c->J1 - 1; m >= c->J0; --m)
         { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
     phase_mark(c, 1);
     // K2 details + flags
-    int nb = 0;
     {
         LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
         c->kcount++;
