@@ -143,6 +143,22 @@ int mrlbm_synchronize(mrlbm_ctx* ctx);
 const char* mrlbm_last_error(const mrlbm_ctx* ctx);
 void mrlbm_destroy(mrlbm_ctx* ctx);
 
+/* ---- diagnostics (the reference has no implementation) ---- */
+/* cells of the finest level (the full finest grid), n = prod(base_cells) * 2^(d (j_max - j_min)) */
+int mrlbm_finest_count(const mrlbm_ctx* ctx, int64_t* n);
+/* Zero-detail reconstruction f^^ of the current state on the full finest grid
+   (§4.4): f[h*n + lin], lin lexicographic (axis 0 slow).
+   f == NULL keeps it on the device only. */
+int mrlbm_reconstruct_finest(mrlbm_ctx* ctx, double* f);
+/* Additional error E[m] = sum |m^^ - m_ref| / sum |m_ref| over the finest grid
+   (SPEC.md:450-458), m = sum_h row[h] f^h, both contexts
+   reconstructed on their devices (the reference is typically an epsilon = 0 run
+   on the full finest mesh, the uniform solver of SPEC.md:326-334).  A zero
+   reference moment (sum < 1e-300) reports the absolute error.
+   sums (optional, 2 doubles) = {sum |m^^ - m_ref|, sum |m_ref|}. */
+int mrlbm_additional_error(mrlbm_ctx* adaptive, mrlbm_ctx* reference, const double* row, double* E,
+                           double* sums);
+
 /* Flattened reconstruction table:
    sum over the E (side=0) or A (side=1) finest cells of a leaf at gap g of the
    zero-detail reconstruction == sum_i w_i f(l, k + off_i).  Lexicographic

@@ -1243,6 +1243,32 @@ class Oracle {
     }
 
     std::int64_t internal_count(int m) const { return lev[m - J0].ii.size(); }
+
+    // f^^ of the current state on the full finest grid: internal
+    // values re-projected from the current leaves (the next step's project_internal
+    // computes the same), then rec() per finest cell; out = SoA q x n, lexicographic.
+    void reconstruct_finest(double* out)
+    {
+        project_internal();
+        Memo memo;
+        const Idx n = extent(J1);
+        std::int64_t total = 1;
+        for (int i = 0; i < D; ++i)
+            total *= n[i];
+        for (std::int64_t lin = 0; lin < total; ++lin)
+        {
+            Idx c{};
+            std::int64_t r = lin;
+            for (int i = D - 1; i >= 0; --i)
+            {
+                c[i] = r % n[i];
+                r /= n[i];
+            }
+            const double* v = rec(J1, c, memo);
+            for (int h = 0; h < q; ++h)
+                out[h * total + lin] = v[h];
+        }
+    }
 };
 
 struct Handle {
@@ -1355,6 +1381,12 @@ int oracle_read_leaves(void* p, int level, int32_t* idx, double* f)
 {
     auto* h = static_cast<Handle*>(p);
     return ORACLE_DISPATCH(h, read(level, idx, f));
+}
+
+int oracle_reconstruct_finest(void* p, double* f)
+{
+    auto* h = static_cast<Handle*>(p);
+    return ORACLE_DISPATCH(h, reconstruct_finest(f));
 }
 
 int64_t oracle_fallback_leaves(void* p)

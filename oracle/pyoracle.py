@@ -46,6 +46,7 @@ def oracle_lib():
         L.oracle_internal_count.argtypes = [vp, C.c_int, P(C.c_int64)]
         L.oracle_read_leaves.argtypes = [vp, C.c_int, vp, vp]
         L.oracle_fallback_leaves.argtypes = [vp]
+        L.oracle_reconstruct_finest.argtypes = [vp, vp]
         L.oracle_fallback_leaves.restype = C.c_int64
         L.oracle_last_error.argtypes = [vp]
         L.oracle_last_error.restype = C.c_char_p
@@ -90,6 +91,9 @@ class Oracle:
     def __init__(self, scheme, cfg):
         self.L = oracle_lib()
         self.d, self.q = scheme.d, scheme.q
+        self.n_finest = 1
+        for i in range(scheme.d):
+            self.n_finest *= int(cfg.base_cells[i]) << (cfg.j_max - cfg.j_min)
         h = C.c_void_p()
         st = self.L.oracle_create(C.byref(scheme), C.byref(cfg), C.byref(h))
         if st != 0:
@@ -138,6 +142,12 @@ class Oracle:
             self._check(self.L.oracle_read_leaves(self.h, int(level), idx.ctypes.data_as(C.c_void_p),
                                                   f.ctypes.data_as(C.c_void_p)))
         return idx, f
+
+    def reconstruct_finest(self):
+        """f^^ on the full finest grid, (q, n) lexicographic (oracle rec())."""
+        f = np.zeros((self.q, self.n_finest), dtype=np.float64)
+        self._check(self.L.oracle_reconstruct_finest(self.h, f.ctypes.data_as(C.c_void_p)))
+        return f
 
     def close(self):
         if getattr(self, "h", None):

@@ -36,6 +36,9 @@ def lib():
         "mrlbm_synchronize": (C.c_int, [vp]),
         "mrlbm_last_error": (C.c_char_p, [vp]),
         "mrlbm_destroy": (None, [vp]),
+        "mrlbm_finest_count": (C.c_int, [vp, P(C.c_int64)]),
+        "mrlbm_reconstruct_finest": (C.c_int, [vp, vp]),
+        "mrlbm_additional_error": (C.c_int, [vp, vp, vp, P(C.c_double), vp]),
         "mrlbm_stream_table": (C.c_int, [C.c_int, C.c_int, P(C.c_int32), C.c_int, C.c_int, vp, vp, P(C.c_int)]),
         "mrlbm_build_config": (C.c_int, [C.c_int, C.c_int, C.c_double, P(SchemeSpec), P(RunConfig)]),
         "mrlbm_config_steps": (C.c_int64, [C.c_int, P(RunConfig)]),

@@ -2260,6 +2260,113 @@ __global__ void k_gather_leaves(const int32_t* cells, int n, int q, const double
     }
 }
 
+// ---------------------------------------------------------------- diagnostics
+// Internal values of the current tree = projection of its leaves (the values K1 of the
+// next step recomputes identically), runtime q.  Slots [nL, nL + nI) of level m.
+template <int D>
+__global__ void k_recon_project(Geo g, Tree t, Fld F, int m, int q)
+{
+    const int li = m - g.J0;
+    const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
+    const int ny = g.ny[li], ny1 = g.ny[li + 1];
+    const long long cap = g.cap[li], cap1 = g.cap[li + 1];
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        const int plin = t.cells[li][s];
+        int px, py;
+        lin2xy<D>(plin, ny, px, py);
+        for (int h = 0; h < q; ++h)
+        {
+            const double* src = F.f[li + 1] + (long long)h * cap1;
+            double acc = 0.0;
+            for (int c = 0; c < (1 << D); ++c)
+            {
+                const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+                acc = __dadd_rn(acc, src[xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)]);
+            }
+            F.f[li][(long long)h * cap + plin] = __ddiv_rn(acc, (double)(1 << D));
+        }
+    }
+}
+
+// Zero-detail reconstruction f^^ of every cell of level m: the
+// complete-tree value where the cell is in R(Lambda), else the prediction from the
+// (complete) reconstruction of level m-1 with the clamp / wrap stencil rule (D.8).
+// Level J0 lies entirely in R.  Same recursion as the oracle's rec().
+template <int D>
+__global__ void k_recon_level(Geo g, Tree t, Fld S, Fld R, int m, int q)
+{
+    const int li = m - g.J0;
+    const long long cap = g.cap[li];
+    const int ny = g.ny[li];
+    GRID_STRIDE(i, 0, cap)
+    {
+        const int lin = (int)i;
+        if (t.kind[li][lin] & (K_LEAF | K_INT))
+        {
+            for (int h = 0; h < q; ++h)
+                R.f[li][(long long)h * cap + lin] = S.f[li][(long long)h * cap + lin];
+            continue;
+        }
+        int x, y;
+        lin2xy<D>(lin, ny, x, y);
+        const int px = x >> 1, py = D == 1 ? 0 : (y >> 1);
+        int st[D == 1 ? 3 : 9];
+        for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
+        {
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            st[o] = mr_lin<D>(g, m - 1, px + ox, py + oy);
+        }
+        const long long capp = g.cap[li - 1];
+        for (int h = 0; h < q; ++h)
+        {
+            const double* P = R.f[li - 1] + (long long)h * capp;
+            double sv[D == 1 ? 3 : 9];
+            for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
+                sv[o] = P[st[o]];
+            R.f[li][(long long)h * cap + lin] = mr_predict<D>(sv, x & 1, D == 1 ? 0 : (y & 1));
+        }
+    }
+}
+
+// E[m] partial sums: per block, sum |m_a - m_b| and sum |m_b| with
+// m = sum_h row[h] f^h (h ascending); fixed thread -> cell map and a fixed tree
+// reduction, so the result is deterministic for a given grid.
+__global__ void __launch_bounds__(256) k_moment_err(const double* A, const double* B, long long cap, int q,
+                                                    const double* row, long long n, double* part)
+{
+    __shared__ double s0[256], s1[256];
+    double e = 0.0, r = 0.0;
+    GRID_STRIDE(i, 0, n)
+    {
+        double ma = 0.0, mb = 0.0;
+        for (int h = 0; h < q; ++h)
+        {
+            ma = __dadd_rn(ma, __dmul_rn(row[h], A[(long long)h * cap + i]));
+            mb = __dadd_rn(mb, __dmul_rn(row[h], B[(long long)h * cap + i]));
+        }
+        e = __dadd_rn(e, fabs(__dsub_rn(ma, mb)));
+        r = __dadd_rn(r, fabs(mb));
+    }
+    s0[threadIdx.x] = e;
+    s1[threadIdx.x] = r;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1)
+    {
+        if ((int)threadIdx.x < w)
+        {
+            s0[threadIdx.x] = __dadd_rn(s0[threadIdx.x], s0[threadIdx.x + w]);
+            s1[threadIdx.x] = __dadd_rn(s1[threadIdx.x], s1[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+    {
+        part[2 * blockIdx.x] = s0[0];
+        part[2 * blockIdx.x + 1] = s1[0];
+    }
+}
+
 } // namespace mrlbm_b200
 
 using namespace mrlbm_b200;
@@ -3178,6 +3285,109 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
         CU(cudaMemcpyAsync(f, stage, sizeof(double) * ctx->q * n, cudaMemcpyDeviceToHost, ctx->stream));
     }
     CU(cudaStreamSynchronize(ctx->stream));
+    return MRLBM_OK;
+}
+
+int mrlbm_finest_count(const mrlbm_ctx* ctx, int64_t* n)
+{
+    if (!ctx || !n)
+        return MRLBM_ERR_CONFIG;
+    *n = ctx->geo.cap[ctx->nlev - 1];
+    return MRLBM_OK;
+}
+
+} // extern "C"
+
+namespace {
+
+// f^^ of the current state on every cell of every level, into the non-state buffer
+// F[1 - curf] (free between steps; the next step writes before it reads there)
+int recon_device(mrlbm_ctx* ctx)
+{
+    if (!ctx->committed)
+        return set_err(ctx, MRLBM_ERR_STATE, "reconstruct before commit");
+    const Geo& g = ctx->geo;
+    Tree t = tree_of(ctx, ctx->cur);
+    Fld S = fld_of(ctx, ctx->curf), R = fld_of(ctx, 1 - ctx->curf);
+    cudaStream_t s = ctx->stream;
+    for (int m = ctx->J1 - 1; m >= ctx->J0; --m)
+    {
+        const int nb = grid_for(ctx, g.cap[m - ctx->J0]);
+        if (ctx->D == 1)
+            k_recon_project<1><<<nb, 256, 0, s>>>(g, t, S, m, ctx->q);
+        else
+            k_recon_project<2><<<nb, 256, 0, s>>>(g, t, S, m, ctx->q);
+    }
+    for (int m = ctx->J0; m <= ctx->J1; ++m)
+    {
+        const int nb = grid_for(ctx, g.cap[m - ctx->J0]);
+        if (ctx->D == 1)
+            k_recon_level<1><<<nb, 256, 0, s>>>(g, t, S, R, m, ctx->q);
+        else
+            k_recon_level<2><<<nb, 256, 0, s>>>(g, t, S, R, m, ctx->q);
+    }
+    CU(cudaGetLastError());
+    return MRLBM_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int mrlbm_reconstruct_finest(mrlbm_ctx* ctx, double* f)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    if (int st = recon_device(ctx); st != MRLBM_OK)
+        return st;
+    if (f)
+    {
+        const int li = ctx->nlev - 1;
+        CU(cudaMemcpyAsync(f, ctx->F[1 - ctx->curf][li], sizeof(double) * ctx->q * ctx->geo.cap[li],
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MRLBM_OK;
+}
+
+int mrlbm_additional_error(mrlbm_ctx* ctx, mrlbm_ctx* ref, const double* row, double* E, double* sums)
+{
+    if (!ctx || !ref || !row || !E)
+        return MRLBM_ERR_CONFIG;
+    const int li = ctx->nlev - 1, lr = ref->nlev - 1;
+    if (ctx->D != ref->D || ctx->q != ref->q || ctx->J1 != ref->J1 || ctx->geo.nx[li] != ref->geo.nx[lr] ||
+        ctx->geo.ny[li] != ref->geo.ny[lr])
+        return set_err(ctx, MRLBM_ERR_CONFIG, "additional_error: finest grids differ");
+    if (int st = recon_device(ref); st != MRLBM_OK)
+        return set_err(ctx, st, std::string("reference: ") + ref->err_msg);
+    if (cudaError_t e = cudaStreamSynchronize(ref->stream); e != cudaSuccess)
+        return set_err(ctx, MRLBM_ERR_CUDA, std::string("reference stream: ") + cudaGetErrorString(e));
+    if (int st = recon_device(ctx); st != MRLBM_OK)
+        return st;
+    const long long n = ctx->geo.cap[li];
+    const int nb = grid_for(ctx, n);
+    double* dev = nullptr;
+    CU(cudaMallocAsync(&dev, sizeof(double) * (ctx->q + 2 * nb), ctx->stream));
+    CU(cudaMemcpyAsync(dev, row, sizeof(double) * ctx->q, cudaMemcpyHostToDevice, ctx->stream));
+    k_moment_err<<<nb, 256, 0, ctx->stream>>>(ctx->F[1 - ctx->curf][li], ref->F[1 - ref->curf][lr], n, ctx->q, dev,
+                                               n, dev + ctx->q);
+    std::vector<double> part(2 * nb);
+    CU(cudaMemcpyAsync(part.data(), dev + ctx->q, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaFreeAsync(dev, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    double num = 0.0, den = 0.0;
+    for (int b = 0; b < nb; ++b)
+    {
+        num += part[2 * b];
+        den += part[2 * b + 1];
+    }
+    if (sums)
+    {
+        sums[0] = num;
+        sums[1] = den;
+    }
+    // zero reference moment: report the absolute error
+    *E = den < 1e-300 ? num : num / den;
     return MRLBM_OK;
 }
 

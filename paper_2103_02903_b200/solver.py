@@ -82,6 +82,29 @@ class Solver:
                                                  f.ctypes.data_as(C.c_void_p)))
         return n
 
+    def finest_count(self):
+        n = C.c_int64(0)
+        self._check(self.L.mrlbm_finest_count(self.h, C.byref(n)))
+        return n.value
+
+    def reconstruct_finest(self):
+        """Zero-detail reconstruction f^^ of the current state on the full finest grid,
+        (q, n) float64, lexicographic (SPEC.md:208-216)."""
+        f = np.zeros((self.q, self.finest_count()), dtype=np.float64)
+        self._check(self.L.mrlbm_reconstruct_finest(self.h, f.ctypes.data_as(C.c_void_p)))
+        return f
+
+    def additional_error(self, reference, row):
+        """E[m] against `reference` (a Solver on the same finest grid, typically epsilon=0),
+        m = sum_h row[h] f^h.  Returns (E, sum|diff|, sum|m_ref|)."""
+        row = np.ascontiguousarray(row, dtype=np.float64)
+        assert row.shape == (self.q,)
+        e = C.c_double(0.0)
+        sums = np.zeros(2, dtype=np.float64)
+        self._check(self.L.mrlbm_additional_error(self.h, reference.h, row.ctypes.data_as(C.c_void_p), C.byref(e),
+                                                  sums.ctypes.data_as(C.c_void_p)))
+        return e.value, float(sums[0]), float(sums[1])
+
     def set_profiling(self, on=True):
         self._check(self.L.mrlbm_set_profiling(self.h, int(bool(on))))
 

@@ -33,6 +33,17 @@ def main():
             data[f"f{lv}"] = f
         np.savez_compressed(os.path.join(out, f"oracle_c{cid}_J{J}_s{steps}.npz"), **data)
         print("wrote", cid, J, steps)
+    # snapshot golden file: config 1, J=6, 5 steps, written by the product's writer
+    from paper_2103_02903_b200.snapshot import write_snapshot
+    sc, rc = build_config(1, 6)
+    o = pyoracle.Oracle(sc, rc)
+    o.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(1, sc, rc))
+    o.commit()
+    o.step(5)
+    o.scheme, o.cfg = sc, rc
+    p = write_snapshot(o, 5, out)
+    os.replace(p, os.path.join(out, "cells_c1_J6_s5.csv"))
+    print("wrote snapshot golden")
 
 
 if __name__ == "__main__":

@@ -1,0 +1,135 @@
+"""zero-detail reconstruction f^^ on the full finest grid and
+the additional error E[m] against the uniform (epsilon = 0) run (SPEC.md:208-216,
+326-334, 450-458).
+
+CPU tests pin the oracle's reconstruction against an independent numpy
+implementation (tests/recon_ref.py); GPU tests compare the product's
+mrlbm_reconstruct_finest / mrlbm_additional_error with the oracle.
+"""
+import numpy as np
+import pytest
+
+from paper_2103_02903_b200 import build_config, finest_cells, initial_finest
+
+from recon_ref import reconstruct, additional_error
+
+SEED = 2103_02903
+
+
+def _oracle(cid, J, eps=-1.0, steps=0, f0=None):
+    from oracle import pyoracle
+    sc, rc = build_config(cid, J, eps)
+    o = pyoracle.Oracle(sc, rc)
+    idx = finest_cells(sc, rc)
+    o.load_leaves(rc.j_max, idx, initial_finest(cid, sc, rc, SEED) if f0 is None else f0)
+    o.commit()
+    if steps:
+        o.step(steps)
+    return sc, rc, o
+
+
+def _leaves(o, rc):
+    return {m: o.read_leaves(m) for m in range(rc.j_min, rc.j_max + 1)}
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def test_oracle_reconstruct_full_mesh_is_identity():
+    sc, rc, o = _oracle(1, 8)
+    idx, f = o.read_leaves(rc.j_max)
+    assert idx.shape[0] == o.n_finest
+    assert np.array_equal(_bits(o.reconstruct_finest()), _bits(f))
+
+
+def test_oracle_reconstruct_constant_field():
+    sc, rc = build_config(5, 6)
+    f0 = initial_finest(5, sc, rc, SEED)
+    const = np.repeat(f0[:, :1], f0.shape[1], axis=1)
+    sc, rc, o = _oracle(5, 6, f0=const)
+    # no stream step: adapt alone (one step would stream); reconstruct the loaded mesh
+    r = o.reconstruct_finest()
+    assert np.array_equal(r, const)
+
+
+@pytest.mark.parametrize("cid,J,steps", [(1, 9, 40), (4, 6, 6), (5, 6, 8), (2, 7, 20)])
+def test_oracle_reconstruct_matches_numpy(cid, J, steps):
+    sc, rc, o = _oracle(cid, J, steps=steps)
+    lv = _leaves(o, rc)
+    nleaves = sum(v[0].shape[0] for v in lv.values())
+    assert nleaves < o.n_finest, "mesh should be adapted for this check to mean something"
+    ref = reconstruct(rc, sc.d, sc.q, lv)
+    got = o.reconstruct_finest()
+    assert np.array_equal(_bits(got), _bits(ref))
+    # the oracle keeps stepping identically after a reconstruction (it re-projects internals only)
+    o.step(1)
+
+
+def test_oracle_additional_error_eps0_is_zero():
+    sc, rc, a = _oracle(1, 8, eps=0.0, steps=16)
+    _, _, b = _oracle(1, 8, eps=0.0, steps=16)
+    E, num, den = additional_error(a.reconstruct_finest(), b.reconstruct_finest(), [1.0, 1.0])
+    assert E == 0.0 and num == 0.0 and den > 0.0
+
+
+# ------------------------------------------------------------------ GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid,J,steps", [(1, 10, 100), (2, 8, 30), (4, 7, 10), (5, 8, 20)])
+def test_gpu_reconstruct_matches_oracle(cid, J, steps):
+    from parity_util import make_pair, compare
+    sc, rc, gpu, ora = make_pair(cid, J)
+    gpu.step(steps)
+    ora.step(steps)
+    g = gpu.reconstruct_finest()
+    o = ora.reconstruct_finest()
+    assert g.shape == o.shape == (sc.q, ora.n_finest)
+    assert np.array_equal(_bits(g), _bits(o)), float(np.max(np.abs(g - o)))
+    # stepping on after a reconstruction stays bit-identical (the scratch buffer is free between steps)
+    gpu.step(3)
+    ora.step(3)
+    worst, bitwise, _ = compare(gpu, ora, rc, f"C{cid} after reconstruct")
+    assert bitwise, worst
+
+
+@pytest.mark.gpu
+def test_gpu_additional_error_vs_oracle():
+    from paper_2103_02903_b200 import Solver
+    from parity_util import make_pair
+    sc, rc, gpu, ora = make_pair(1, 10)
+    sc0, rc0, gref, oref = make_pair(1, 10, eps=0.0)
+    for s in (gpu, ora, gref, oref):
+        s.step(256)
+    row = [1.0, 1.0]  # conserved moment u = f0 + f1
+    E, num, den = gpu.additional_error(gref, row)
+    Eo, numo, deno = additional_error(ora.reconstruct_finest(), oref.reconstruct_finest(), row)
+    assert E > 0.0
+    assert abs(E - Eo) <= 1e-12 * Eo
+    assert abs(num - numo) <= 1e-12 * numo and abs(den - deno) <= 1e-12 * deno
+    # identical states -> exactly zero
+    E0, n0, _ = gref.additional_error(gref, row)
+    assert E0 == 0.0 and n0 == 0.0
+    # mismatched grids are rejected (status 2 -> ValueError)
+    sc2, rc2 = build_config(1, 9)
+    other = Solver(sc2, rc2)
+    other.load_leaves(rc2.j_max, finest_cells(sc2, rc2), initial_finest(1, sc2, rc2, SEED))
+    other.commit()
+    with pytest.raises(ValueError):
+        gpu.additional_error(other, row)
+
+
+@pytest.mark.gpu
+def test_gpu_additional_error_decreases_with_epsilon():
+    """PAPER.md:1170-1180 bound E <= C(T) eps: the measured E[u] of config 1 at J=10
+    after 1024 steps shrinks monotonically over eps = 1e-2 .. 1e-4."""
+    from parity_util import make_pair
+    _, _, gref, _ = make_pair(1, 10, eps=0.0)
+    gref.step(1024)
+    Es = []
+    for eps in (1e-2, 1e-3, 1e-4):
+        _, _, g, _ = make_pair(1, 10, eps=eps)
+        g.step(1024)
+        Es.append(g.additional_error(gref, [1.0, 1.0])[0])
+    assert Es[0] > Es[1] > Es[2] > 0.0
+    slope = np.polyfit(np.log10([1e-2, 1e-3, 1e-4]), np.log10(Es), 1)[0]
+    assert 0.2 < slope < 1.5, slope
