@@ -10,9 +10,24 @@ for every gap >= 2, asserted below up to gap 14) the generated function
     from the runtime tables in shared memory,
 so the arithmetic is identical to the generic table loop (and to the oracle).
 
+Gap classes 0 and 1 take their weights as compile-time constants (exact dyadics,
+rounded to nearest like csrc/host_configs.cpp; gen_w_* arrays let mrlbm_create
+verify them against the runtime tables).  At gap 0 every weight and the scale
+2^{d(l-J)} are exactly 1, so the multiplications by them are dropped (x * 1 == x
+bit for bit).
+
+The collision m = M f and f* = M^-1 m' is unrolled over the zero / +1 / -1 /
+general pattern of the scheme's matrices (collide_patterns.json, written by
+tools/collide_patterns.py): zero terms are skipped, +-1 terms become a plain
+add / subtract (acc + 1*x == acc + x, acc + (-1)*x == acc - x exactly, and acc
+starts at +0 so skipping +-0 products never changes it).  General entries are
+read from the kernel-parameter copy of the matrices.  mrlbm_create checks the
+runtime matrices against the pattern (gen_pat_*) before enabling this path.
+
 Run: python paper_2103_02903_b200/csrc/gen_stream.py  (rewrites stream_gen.cuh)
 """
 import itertools
+import json
 import os
 from fractions import Fraction
 
@@ -55,6 +70,35 @@ def table_offsets(d, g, eta, side):
     return [k for k, v in sorted(cur.items()) if v != 0]
 
 
+def table_weights_exact(d, g, eta, side):
+    n = 2 ** g
+    inb = lambda x: all(0 <= xi < n for xi in x)  # noqa: E731
+    cur = {}
+    for x in itertools.product(range(-1, n + 1), repeat=d):
+        xe = tuple(xi + e for xi, e in zip(x, eta))
+        if (inb(xe) and not inb(x)) if side == 0 else (inb(x) and not inb(xe)):
+            cur[x] = Fraction(1)
+    for _ in range(g):
+        nxt = {}
+        for c, w in cur.items():
+            p = tuple(ci >> 1 for ci in c)
+            dl = tuple(ci - 2 * pi for ci, pi in zip(c, p))
+            for o, wo in pred_w(d, dl).items():
+                k = tuple(pi + oi for pi, oi in zip(p, o))
+                nxt[k] = nxt.get(k, 0) + w * wo
+        cur = nxt
+    return [float(v) for k, v in sorted(cur.items()) if v != 0]
+
+
+def table_weights(d, g, etas):
+    """All weights of one gap in table order (population, side, lexicographic offset)."""
+    out = []
+    for eta in etas:
+        for side in (0, 1):
+            out += table_weights_exact(d, g, eta, side)
+    return out
+
+
 D2Q4 = [(1, 0), (0, 1), (-1, 0), (0, -1)]
 SETS = {
     # name: (d, q, eta list, equilibrium enum)
@@ -88,12 +132,14 @@ def gen_class(name, d, q, etas, gclass, out):
         ox = o[0]
         oy = o[1] if d == 2 else 0
         xs = f"x + ({ox})" if ox else "x"
+        # 32-bit linear indices (a level holds < 2^31 cells): half the registers of 64-bit ones
         if d == 1:
-            out.append(f"    const long long sl{i} = gen_wrap({xs}, nx, per0);")
+            out.append(f"    const int sl{i} = gen_wrap({xs}, nx, per0);")
         else:
             ys = f"y + ({oy})" if oy else "y"
-            out.append(f"    const long long sl{i} = (long long)gen_wrap({xs}, nx, per0) * ny + gen_wrap({ys}, ny, per1);")
+            out.append(f"    const int sl{i} = gen_wrap({xs}, nx, per0) * ny + gen_wrap({ys}, ny, per1);")
     widx = 0
+    wts = table_weights(d, g, etas) if gclass < 2 else None
     for h in range(q):
         used = sorted({oid[o] for side in (0, 1) for o in tabs[(h, side)]})
         out.append("    {")
@@ -106,13 +152,25 @@ def gen_class(name, d, q, etas, gclass, out):
             nm = "sE" if side == 0 else "sA"
             out.append(f"        double {nm} = 0.0;")
             for o in tabs[(h, side)]:
-                out.append(f"        {nm} = __dadd_rn({nm}, __dmul_rn(sW[{widx}], v{oid[o]}));")
+                if gclass == 0:
+                    assert wts[widx] == 1.0
+                    out.append(f"        {nm} = __dadd_rn({nm}, v{oid[o]});")
+                elif gclass == 1:
+                    out.append(f"        {nm} = __dadd_rn({nm}, __dmul_rn({wts[widx].hex()}, v{oid[o]}));")
+                else:
+                    out.append(f"        {nm} = __dadd_rn({nm}, __dmul_rn(sW[{widx}], v{oid[o]}));")
                 widx += 1
             sums.append(nm)
-        out.append(f"        f[{h}] = __dadd_rn(fs, __dmul_rn(scale, __dsub_rn(sE, sA)));")
+        if gclass == 0:
+            out.append(f"        f[{h}] = __dadd_rn(fs, __dsub_rn(sE, sA));")
+        else:
+            out.append(f"        f[{h}] = __dadd_rn(fs, __dmul_rn(scale, __dsub_rn(sE, sA)));")
         out.append("    }")
     out.append("}")
     out.append("")
+    if gclass < 2:
+        out.append(f"static const double gen_w_{name}_g{gclass}[{len(wts)}] = {{{', '.join(w.hex() for w in wts)}}};")
+        out.append("")
     return widx
 
 
@@ -199,6 +257,48 @@ def gen_fb1(name, d, q, etas, out):
     return widx
 
 
+def gen_matvec(fn, name, q, bs, pat, arr, src, dst, out):
+    """dst[i] = sum_c A[i][b0 + c] * src[b0 + c] over the pattern, DenseMatrix::multiply order."""
+    out.append(f"template <class CC>")
+    out.append(f"__device__ __forceinline__ void {fn}_{name}(const CC& cc, const double (&{src})[{q}], double (&{dst})[{q}])")
+    out.append("{")
+    for i in range(q):
+        b0 = (i // bs) * bs
+        terms = []
+        for c, ch in enumerate(pat[i]):
+            j = b0 + c
+            if ch == "0":
+                continue
+            if ch == "+":
+                terms.append(("add", f"{src}[{j}]"))
+            elif ch == "-":
+                terms.append(("sub", f"{src}[{j}]"))
+            else:
+                terms.append(("add", f"__dmul_rn(cc.{arr}[{i * bs + c}], {src}[{j}])"))
+        if not terms:
+            out.append(f"    {dst}[{i}] = 0.0;")
+            continue
+        expr = "0.0"
+        for op, t in terms:
+            expr = f"__d{op}_rn({expr}, {t})"
+        out.append(f"    {dst}[{i}] = {expr};")
+    out.append("}")
+    out.append("")
+
+
+def gen_collide(out):
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "collide_patterns.json")
+    pats = json.load(open(path))
+    for name in SETS:
+        p = pats[name]
+        q, bs = p["q"], p["bs"]
+        gen_matvec("gen_mf", name, q, bs, p["M"], "M", "f", "m", out)
+        gen_matvec("gen_minv", name, q, bs, p["Minv"], "Mi", "m", "f", out)
+        out.append(f'static const char gen_pat_{name}_M[] = "{"".join(p["M"])}";')
+        out.append(f'static const char gen_pat_{name}_Minv[] = "{"".join(p["Minv"])}";')
+        out.append("")
+
+
 def main():
     out = ["// GENERATED by gen_stream.py -- do not edit.",
            "// Unrolled flattened-table stream sums for the built-in velocity sets (K7 fast path).",
@@ -214,6 +314,7 @@ def main():
             gen_class(name, d, q, etas, gc, out)
     for name, (d, q, etas) in SETS.items():
         gen_fb1(name, d, q, etas, out)
+    gen_collide(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "stream_gen.cuh")
     open(path, "w").write("\n".join(out) + "\n")
     print("wrote", path, len(out), "lines")

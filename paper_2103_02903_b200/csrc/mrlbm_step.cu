@@ -1463,7 +1463,7 @@ __device__ __forceinline__ void equilibrium_t(const double* P, double lambda, co
 // -> boundary rule by direct evaluation
 template <int D>
 __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const Fld& S, const SchemeDev* sc, int x,
-                                            int y, int h, int leaf_li, long long leaf_lin, Aux& aux)
+                                            int y, int h, int leaf_li, long long leaf_lin, const Aux& aux)
 {
     const int lj = g.J1 - g.J0;
     const int nx = g.nx[lj], ny = g.ny[lj];
@@ -1538,7 +1538,7 @@ __device__ __forceinline__ bool in_box(int x, int y, int bx0, int bx1, int by0, 
 // full rows where the row leaves B, else the single end column.
 template <int D>
 __device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int h, int side, int bx0,
-                          int bx1, int by0, int by1, int leaf_li, long long leaf_lin, Aux& aux)
+                          int bx1, int by0, int by1, int leaf_li, long long leaf_lin, const Aux& aux)
 {
     const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
     double s = 0.0;
@@ -1847,18 +1847,24 @@ __global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld 
 }
 
 // generated unrolled table sums (stream_gen.cuh) for the built-in velocity sets
-template <int EQ, int Q>
+// GC: gap class compiled in (0: gap 0 only, 1: gaps >= 1 only, -1: any)
+template <int EQ, int Q, int GC>
 __device__ __forceinline__ void gen_stream(int gap, const double* Fin, long long cap, int x, int y, int nx, int ny,
                                            int per0, int per1, long long s, const double* sW, double scale,
                                            double (&f)[Q])
 {
 #define GEN_CALL(N)                                                                                                    \
-    if (gap == 0)                                                                                                      \
+    if constexpr (GC == 0)                                                                                             \
         gen_stream_EQ##N##_g0(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
-    else if (gap == 1)                                                                                                 \
-        gen_stream_EQ##N##_g1(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                               \
     else                                                                                                               \
-        gen_stream_EQ##N##_g2(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);
+    {                                                                                                                  \
+        if (GC < 0 && gap == 0)                                                                                        \
+            gen_stream_EQ##N##_g0(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                           \
+        else if (gap == 1)                                                                                             \
+            gen_stream_EQ##N##_g1(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                           \
+        else                                                                                                           \
+            gen_stream_EQ##N##_g2(Fin, cap, x, y, nx, ny, per0, per1, s, sW, scale, f);                           \
+    }
     if constexpr (EQ == 1 && Q == 2)
     {
         GEN_CALL(1)
@@ -1882,12 +1888,56 @@ __device__ __forceinline__ void gen_stream(int gap, const double* Fin, long long
 #undef GEN_CALL
 }
 
+// the scheme's matrices as a kernel parameter (constant bank): block-diagonal compact
+// layout [i * BS + c] = M[i][(i / BS) * BS + c]
+template <int Q, int BS>
+struct CollC {
+    double M[Q * BS], Mi[Q * BS];
+};
+
+// generated pattern-unrolled m = M f and f = M^-1 m (stream_gen.cuh, gen_stream.py)
+template <int EQ, int Q, class CC>
+__device__ __forceinline__ void gen_collide_mv(const CC& cc, bool inverse, const double (&x)[Q], double (&y)[Q])
+{
+#define GEN_MV(N)                                                                                                      \
+    if (inverse)                                                                                                       \
+        gen_minv_EQ##N(cc, x, y);                                                                                      \
+    else                                                                                                               \
+        gen_mf_EQ##N(cc, x, y);
+    if constexpr (EQ == 1 && Q == 2)
+    {
+        GEN_MV(1)
+    }
+    else if constexpr (EQ == 2 && Q == 9)
+    {
+        GEN_MV(2)
+    }
+    else if constexpr (EQ == 3 && Q == 4)
+    {
+        GEN_MV(3)
+    }
+    else if constexpr (EQ == 4 && Q == 16)
+    {
+        GEN_MV(4)
+    }
+    else if constexpr (EQ == 5 && Q == 9)
+    {
+        GEN_MV(5)
+    }
+#undef GEN_MV
+}
+
 // K7: table-path stream + collision +
 // obstacle blend, one thread per leaf.  Fallback leaves take their post-stream
 // populations from K8 (already in F0).  BS = block size of the block-diagonal M.
-template <int D, int Q, int BS, int EQ, bool GEN>
-__global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F0, Fld F1, Flags fl,
-                                                           const SchemeDev* scg, LGrid lg_, Aux aux)
+// MODE 0 streams the table-path leaves only (no calls, no stack: the hot kernel);
+// MODE 1 the fallback leaves (values from K8 / k_stream_fb1, or the boundary rim).
+template <int D, int Q, int BS, int EQ, bool GEN, int MODE, int GC>
+__global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
+    k_stream_collide(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld F0,
+                     const __grid_constant__ Fld F1, const __grid_constant__ Flags fl, const SchemeDev* scg,
+                     const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux,
+                     const __grid_constant__ CollC<Q, BS> cc)
 {
     LSETUP;
     constexpr int kMaxE = 2 * Q * 25;
@@ -1953,10 +2003,11 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
     {
         const int lin = tn.cells[li][s];
         const uint8_t kd = fl.kind[li][lin];
-        const bool fb = (kd & K_FB) != 0;
-        const bool fbc = (kd & K_FBC) != 0;
+        if (((kd & K_FB) != 0) != (MODE == 1))
+            continue;
+        constexpr bool fb = MODE == 1;
         double f[Q];
-        if (fb && !fbc && gap >= kDeepGap)
+        if (fb && gap >= kDeepGap)
         {
             // deep-gap fallback leaf: post-stream populations from K8
 #pragma unroll
@@ -1967,7 +2018,7 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
         {
             int x, y;
             lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-            gen_stream<EQ, Q>(gap, Fin, cap, x, y, nx, ny, per0, per1, lin, sW, scale, f);
+            gen_stream<EQ, Q, GC>(gap, Fin, cap, x, y, nx, ny, per0, per1, lin, sW, scale, f);
         }
         else
         {
@@ -2077,29 +2128,39 @@ __global__ void __launch_bounds__(256, 3) k_stream_collide(Geo g, Tree tn, Fld F
         // collide: m = M f (block diagonal, DenseMatrix::multiply order),
         // m' = (1-s) m + s m^eq, f* = M^-1 m'
         double mo[Q], meq[Q];
-#pragma unroll
-        for (int i = 0; i < Q; ++i)
+        if constexpr (GEN)
+            gen_collide_mv<EQ, Q>(cc, false, f, mo);
+        else
         {
-            const int b0 = (i / BS) * BS;
-            double acc = 0.0;
 #pragma unroll
-            for (int j = 0; j < BS; ++j)
-                acc = __dadd_rn(acc, __dmul_rn(sM[i * BS + j], f[b0 + j]));
-            mo[i] = acc;
+            for (int i = 0; i < Q; ++i)
+            {
+                const int b0 = (i / BS) * BS;
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < BS; ++j)
+                    acc = __dadd_rn(acc, __dmul_rn(sM[i * BS + j], f[b0 + j]));
+                mo[i] = acc;
+            }
         }
         equilibrium_t<EQ, Q>(sP, scg->lambda, mo, meq);
 #pragma unroll
         for (int i = 0; i < Q; ++i)
             mo[i] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, sS[i]), mo[i]), __dmul_rn(sS[i], meq[i]));
-#pragma unroll
-        for (int i = 0; i < Q; ++i)
+        if constexpr (GEN)
+            gen_collide_mv<EQ, Q>(cc, true, mo, f);
+        else
         {
-            const int b0 = (i / BS) * BS;
-            double acc = 0.0;
 #pragma unroll
-            for (int j = 0; j < BS; ++j)
-                acc = __dadd_rn(acc, __dmul_rn(sMi[i * BS + j], mo[b0 + j]));
-            f[i] = acc;
+            for (int i = 0; i < Q; ++i)
+            {
+                const int b0 = (i / BS) * BS;
+                double acc = 0.0;
+#pragma unroll
+                for (int j = 0; j < BS; ++j)
+                    acc = __dadd_rn(acc, __dmul_rn(sMi[i * BS + j], mo[b0 + j]));
+                f[i] = acc;
+            }
         }
         if constexpr (EQ == MRLBM_EQ_NS_D2Q9 && D == 2)
         {
@@ -2417,7 +2478,8 @@ struct mrlbm_ctx {
     bool committed = false;
     bool profiling = false;
     bool use_graph = true;
-    bool use_gen = false; // generated stream path (built-in velocity sets)
+    bool use_gen = false; // generated stream / collision path (built-in velocity sets)
+    bool gen_ok = false;  // the generated code's constants match this scheme
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
     // load staging (device): per level, coordinates -> linear indices; the values are
@@ -2713,8 +2775,38 @@ void enqueue_step(mrlbm_ctx* c)
     {
         LGrid lg = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
         c->kcount++;
-        k_stream_collide<D, Q, BS, EQ, GEN><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux);
-        kmark(c, "k_stream_collide", -1);
+        CollC<Q, BS> cc;
+        for (int i = 0; i < Q; ++i)
+            for (int j = 0; j < BS; ++j)
+            {
+                const int col = (i / BS) * BS + j;
+                cc.M[i * BS + j] = c->sc.M[i * Q + col];
+                cc.Mi[i * BS + j] = c->sc.Minv[i * Q + col];
+            }
+        if constexpr (GEN)
+        {
+            // the generated path in two register budgets: the finest level (gap 0) alone,
+            // then every coarser level (gap classes 1 and >= 2)
+            LGrid l0 = make_lgrid(c, c->J1, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
+            k_stream_collide<D, Q, BS, EQ, GEN, 0, 0><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
+            kmark(c, "k_stream_collide", c->J1);
+            if (c->J1 > c->J0)
+            {
+                LGrid l1 = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
+                c->kcount++;
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
+                kmark(c, "k_stream_collide", -1);
+            }
+        }
+        else
+        {
+            k_stream_collide<D, Q, BS, EQ, GEN, 0, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
+            kmark(c, "k_stream_collide", -1);
+        }
+        LGrid lf = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 8, 256); }, &nb);
+        c->kcount++;
+        k_stream_collide<D, Q, BS, EQ, GEN, 1, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
+        kmark(c, "k_stream_collide_fb", -1);
     }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
     phase_mark(c, 6);
@@ -2722,6 +2814,67 @@ void enqueue_step(mrlbm_ctx* c)
 }
 
 using StepFn = void (*)(mrlbm_ctx*);
+
+// The generated code's compile-time constants hold for this scheme: the gap-0 / gap-1
+// table weights (table order) and the zero / +-1 pattern of M and M^-1.
+bool gen_constants_match(const mrlbm_scheme_spec* sc, int nlev, const std::vector<int2>& idx,
+                         const std::vector<double>& w)
+{
+    const double* gw[2] = {nullptr, nullptr};
+    int gn[2] = {0, 0};
+    const char* pat[2] = {nullptr, nullptr};
+#define GEN_CASE(N)                                                                                                    \
+    case N:                                                                                                            \
+        gw[0] = gen_w_EQ##N##_g0;                                                                                      \
+        gn[0] = static_cast<int>(sizeof(gen_w_EQ##N##_g0) / sizeof(double));                                           \
+        gw[1] = gen_w_EQ##N##_g1;                                                                                      \
+        gn[1] = static_cast<int>(sizeof(gen_w_EQ##N##_g1) / sizeof(double));                                           \
+        pat[0] = gen_pat_EQ##N##_M;                                                                                    \
+        pat[1] = gen_pat_EQ##N##_Minv;                                                                                 \
+        break;
+    switch (sc->equilibrium)
+    {
+        GEN_CASE(1)
+        GEN_CASE(2)
+        GEN_CASE(3)
+        GEN_CASE(4)
+        GEN_CASE(5)
+    default:
+        return false;
+    }
+#undef GEN_CASE
+    const int q = sc->q, bs = q / sc->nblocks;
+    for (int gp = 0; gp < 2 && gp < nlev; ++gp)
+    {
+        const int b = idx[gp * 2 * q].x;
+        const int2 last = idx[gp * 2 * q + 2 * q - 1];
+        if (last.x + last.y - b != gn[gp])
+            return false;
+        for (int e = 0; e < gn[gp]; ++e)
+            if (w[b + e] != gw[gp][e])
+                return false;
+    }
+    for (int k = 0; k < 2; ++k)
+    {
+        const double* A = k == 0 ? sc->M : sc->Minv;
+        if (static_cast<int>(std::strlen(pat[k])) != q * bs)
+            return false;
+        for (int i = 0; i < q; ++i)
+            for (int c = 0; c < bs; ++c)
+            {
+                const double v = A[i * q + (i / bs) * bs + c];
+                const char ch = pat[k][i * bs + c];
+                if ((ch == '0' && v != 0.0) || (ch == '+' && v != 1.0) || (ch == '-' && v != -1.0))
+                    return false;
+            }
+        // block-diagonal: nothing outside the blocks
+        for (int i = 0; i < q; ++i)
+            for (int j = 0; j < q; ++j)
+                if (j / bs != i / bs && A[i * q + j] != 0.0)
+                    return false;
+    }
+    return true;
+}
 
 // the generated stream path applies when the velocities are exactly the built-in
 // set of the equilibrium kind (the order csrc/host_configs.cpp uses)
@@ -3015,6 +3168,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             return MRLBM_ERR_CUDA;
         for (auto& e : ctx->ev)
             CU(cudaEventCreate(&e));
+        ctx->gen_ok = gen_constants_match(sc, ctx->nlev, idx, w);
         return MRLBM_OK;
     }();
     if (st != MRLBM_OK)
@@ -3024,7 +3178,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         fprintf(stderr, "mrlbm_create: %s\n", msg.c_str());
         return st;
     }
-    ctx->use_gen = builtin_velocities(sc) && std::getenv("MRLBM_NO_GEN") == nullptr;
+    ctx->use_gen = builtin_velocities(sc) && ctx->gen_ok && std::getenv("MRLBM_NO_GEN") == nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
         const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;
