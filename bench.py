@@ -292,6 +292,8 @@ def bench_product(args):
 
     if rank == 0:
         leaves_last = [int(st.leaves[i]) for i in range(st.levels)]
+        internal_last = [int(st.internal[i]) for i in range(st.levels)]
+        virtual_last = [int(st.virtual_cells[i]) for i in range(st.levels)]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -302,6 +304,8 @@ def bench_product(args):
                        "parallelism": "replicas" if world > 1 else "single-gpu",
                        "l2": f"flushed between timed steps (256 MiB write); state {state_bytes / 1e6:.0f} MB",
                        "leaves_per_level_last_step": leaves_last,
+                       "internal_per_level_last_step": internal_last,
+                       "virtual_per_level_last_step": virtual_last,
                        "fallback_leaves_last_step": int(st.fallback_leaves)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -187,29 +187,31 @@ def rim_cells_g1(d, eta, side):
     return out
 
 
-def gen_fb1(name, d, q, etas, out):
-    """Gap-1 fallback leaves: table sums + details of the rim cells that are finest
-    leaves (Decision D.13b), per (population, side) selected by the masks."""
+def gen_fb1h(name, d, q, etas, out):
+    """Gap-1 fallback leaves, one population (one warp per population in k_fb1,
+    selected by a warp-uniform switch on h): table sums + details of the rim cells
+    that are finest leaves (Decision D.13b), per side selected by the masks; box =
+    5^d level-l linear indices, rim = 4^d finest linear indices of leaves (-1: not a
+    leaf); dmask pairs are left to the caller."""
     tabs = {(h, side): table_offsets(d, 1, eta, side) for h, eta in enumerate(etas) for side in (0, 1)}
-    nbox = 5 ** d
     bidx = (lambda o: o[0] + 2) if d == 1 else (lambda o: (o[0] + 2) * 5 + (o[1] + 2))
-    out.append(f"// {name}: gap-1 fallback leaves (table + detail correction), box = 5^d level-l slots,")
-    out.append("// rim = 4^d finest linear indices of leaves (-1: not a leaf); dmask pairs are left to the caller.")
-    out.append(f"__device__ __forceinline__ void gen_fb1_{name}(const double* __restrict__ Fin, long long cap, "
+    out.append(f"__device__ __forceinline__ void gen_fb1h_{name}(int h, const double* __restrict__ Fin, long long cap, "
                f"const double* __restrict__ Fj, long long capj, const int* box, const int* rim, int bstride, "
-               f"unsigned mask, unsigned dmask, const double* sW, double (&sE)[{q}], double (&sA)[{q}])")
+               f"unsigned mask, unsigned dmask, const double* sW, double& sE, double& sA)")
     out.append("{")
+    out.append("    switch (h)")
+    out.append("    {")
     widx = 0
-    nr = 4 ** d
     for h, eta in enumerate(etas):
         needed_box = set()
         for side in (0, 1):
             for o in tabs[(h, side)]:
                 needed_box.add(bidx(o))
+        out.append(f"    case {h}:")
         out.append("    {")
         out.append(f"        const double* Fh = Fin + {h}LL * cap;")
         out.append(f"        const double* Fjh = Fj + {h}LL * capj;")
-        out.append("        (void)Fjh;")
+        out.append("        (void)Fjh; (void)Fh;")
         for b in sorted(needed_box):
             out.append(f"        const double v{b} = Fh[box[{b} * bstride]];")
         for side in (0, 1):
@@ -235,26 +237,27 @@ def gen_fb1(name, d, q, etas, out):
                 for c in rims:
                     r = c[0] if d == 1 else c[0] * 4 + c[1]
                     p = tuple((ci + 1) // 2 - 1 for ci in c)
-                    par = tuple((ci + 1) & 1 for ci in c)  # child parity of the rim cell
+                    par = tuple((ci + 1) & 1 for ci in c)
                     out.append("                {")
                     out.append(f"                    const int sj = rim[{r} * bstride];")
                     out.append("                    if (sj >= 0)")
                     out.append("                    {")
-                    sv = []
-                    for st in itertools.product((-1, 0, 1), repeat=d):
-                        sv.append(f"v{bidx(tuple(pi + si for pi, si in zip(p, st)))}")
+                    sv = [f"v{bidx(tuple(pi + si for pi, si in zip(p, st)))}" for st in itertools.product((-1, 0, 1), repeat=d)]
                     out.append(f"                        const double sv[{len(sv)}] = {{{', '.join(sv)}}};")
                     dy = par[1] if d == 2 else 0
                     out.append(f"                        acc = __dadd_rn(acc, __dsub_rn(Fjh[sj], mr_predict<{d}>(sv, {par[0]}, {dy})));")
                     out.append("                    }")
                     out.append("                }")
                 out.append("            }")
-            out.append(f"            {nm}[{h}] = acc;")
+            out.append(f"            {nm} = acc;")
             out.append("        }")
+        out.append("        break;")
         out.append("    }")
+    out.append("    default:")
+    out.append("        break;")
+    out.append("    }")
     out.append("}")
     out.append("")
-    return widx
 
 
 def gen_matvec(fn, name, q, bs, pat, arr, src, dst, out):
@@ -286,6 +289,32 @@ def gen_matvec(fn, name, q, bs, pat, arr, src, dst, out):
     out.append("")
 
 
+def gen_matrow(fn, name, q, bs, pat, arr, out):
+    """Row i of the same product (warp-uniform switch), for the row-per-warp collision of k_fb1."""
+    out.append("template <class CC>")
+    out.append(f"__device__ __forceinline__ double {fn}_row_{name}(const CC& cc, int i, const double (&x)[{q}])")
+    out.append("{")
+    out.append("    switch (i)")
+    out.append("    {")
+    for i in range(q):
+        b0 = (i // bs) * bs
+        expr = None
+        for c, ch in enumerate(pat[i]):
+            j = b0 + c
+            if ch == "0":
+                continue
+            t = f"x[{j}]" if ch in "+-" else f"__dmul_rn(cc.{arr}[{i * bs + c}], x[{j}])"
+            op = "sub" if ch == "-" else "add"
+            expr = f"__d{op}_rn({expr or '0.0'}, {t})"
+        out.append(f"    case {i}:")
+        out.append(f"        return {expr or '0.0'};")
+    out.append("    default:")
+    out.append("        return 0.0;")
+    out.append("    }")
+    out.append("}")
+    out.append("")
+
+
 def gen_collide(out):
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "collide_patterns.json")
     pats = json.load(open(path))
@@ -294,6 +323,8 @@ def gen_collide(out):
         q, bs = p["q"], p["bs"]
         gen_matvec("gen_mf", name, q, bs, p["M"], "M", "f", "m", out)
         gen_matvec("gen_minv", name, q, bs, p["Minv"], "Mi", "m", "f", out)
+        gen_matrow("gen_mf", name, q, bs, p["M"], "M", out)
+        gen_matrow("gen_minv", name, q, bs, p["Minv"], "Mi", out)
         out.append(f'static const char gen_pat_{name}_M[] = "{"".join(p["M"])}";')
         out.append(f'static const char gen_pat_{name}_Minv[] = "{"".join(p["Minv"])}";')
         out.append("")
@@ -313,7 +344,7 @@ def main():
         for gc in (0, 1, 2):
             gen_class(name, d, q, etas, gc, out)
     for name, (d, q, etas) in SETS.items():
-        gen_fb1(name, d, q, etas, out)
+        gen_fb1h(name, d, q, etas, out)
     gen_collide(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "stream_gen.cuh")
     open(path, "w").write("\n".join(out) + "\n")

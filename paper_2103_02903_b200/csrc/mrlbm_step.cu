@@ -795,7 +795,7 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     }
     else
     {
-        // gap 0 / 1 fallback leaves are found by slot scans (K7 / k_stream_fb1);
+        // gap 0 / 1 fallback leaves are found by slot scans (K7 / k_fb1);
         // count them for the statistics with one atomic per warp
         const unsigned am = __activemask();
         if ((threadIdx.x & 31) == __ffs(am) - 1)
@@ -1594,7 +1594,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
         const int it = (int)(t / q), h = (int)(t % q);
         const int2 e = aux.fb_list[it];
         if (g.J1 - e.x < 2)
-            continue; // gap 1: k_stream_fb1
+            continue; // gap 1: k_fb1
         const unsigned mask = aux.fb_mask[it];
         const unsigned dmask = aux.fb_dmask[it];
         const int m = e.x, li = m - g.J0;
@@ -1672,178 +1672,35 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
     }
 }
 
-// Gap-1 fallback leaves, one thread per leaf.  The leaf's 5^D level-l slots and
-// the 4^D finest-level cells around its 2^D children are looked up once into shared
-// memory; then every (population, side) pair is summed from the cache: the
-// flattened table when exact, the table plus the details of the leaf rim cells
-// when only finer neighbours break it (Decision D.13b), else the boundary rim
-// (rim_sum).  Writes post-stream populations into F0; K7 collides them.
-template <int EQ, int Q>
-__device__ __forceinline__ void gen_fb1(const double* Fin, long long cap, const double* Fj, long long capj, const int* box,
-                                        const int* rim, int bstride, unsigned mask, unsigned dmask,
-                                        const double* sW, double (&sE)[Q], double (&sA)[Q])
+// config 5 volume-fraction blend: the fraction alpha
+// of the cell (level m, index x, y) inside the disc, from ns x ns sub-samples; 0 when
+// the cell's box misses the disc's bounding box.
+__device__ __forceinline__ double obstacle_alpha(const SchemeDev* scg, int m, int x, int y)
 {
-    if constexpr (EQ == 1 && Q == 2)
-        gen_fb1_EQ1(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
-    else if constexpr (EQ == 2 && Q == 9)
-        gen_fb1_EQ2(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
-    else if constexpr (EQ == 3 && Q == 4)
-        gen_fb1_EQ3(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
-    else if constexpr (EQ == 4 && Q == 16)
-        gen_fb1_EQ4(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
-    else if constexpr (EQ == 5 && Q == 9)
-        gen_fb1_EQ5(Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
-}
-
-template <int D, int Q, int EQ, bool GEN>
-__global__ void __launch_bounds__(128) k_stream_fb1(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* sc, Aux aux)
-{
-    constexpr int kB = D == 1 ? 5 : 25;   // level-l box
-    constexpr int kR = D == 1 ? 4 : 16;   // finest-level 4^D box around the children
-    constexpr int kT = 128;
-    constexpr int kMaxE = 2 * Q * 25;
-    __shared__ int sBox[kB][kT];
-    __shared__ int sRim[kR][kT];
-    __shared__ double sW[kMaxE];
-    if (GEN && g.J1 - 1 >= g.J0)
+    const double dx = ldexp(1.0, -m);
+    const double ox = scg->origin[0], oy = scg->origin[1];
+    const double cx = scg->obs_c[0], cy = scg->obs_c[1], r = scg->obs_r;
+    const double x0 = __dadd_rn(ox, __dmul_rn((double)x, dx));
+    const double y0 = __dadd_rn(oy, __dmul_rn((double)y, dx));
+    const double x1 = __dadd_rn(x0, dx), y1 = __dadd_rn(y0, dx);
+    if (x1 < __dsub_rn(cx, r) || x0 > __dadd_rn(cx, r) || y1 < __dsub_rn(cy, r) || y0 > __dadd_rn(cy, r))
+        return 0.0;
+    const int ns = scg->obs_ns;
+    const double r2 = __dmul_rn(r, r);
+    int cnt = 0;
+    for (int a = 0; a < ns; ++a)
     {
-        // gap-1 table weights in table order
-        const int base = aux.tidx[1 * 2 * Q].x;
-        const int2 last = aux.tidx[1 * 2 * Q + 2 * Q - 1];
-        const int ne = min(last.x + last.y - base, kMaxE);
-        for (int e = threadIdx.x; e < ne; e += blockDim.x)
-            sW[e] = aux.tw[base + e];
-        __syncthreads();
-    }
-    const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
-    const int q = g.q;
-    const int m = g.J1 - 1, li = m - g.J0, lj = li + 1;
-    if (li < 0)
-        return;
-    const int nx = g.nx[li], ny = g.ny[li], nxj = g.nx[lj], nyj = g.ny[lj];
-    const long long cap = g.cap[li], capj = g.cap[lj];
-    const double scale = ldexp(1.0, D * (m - g.J1));
-    const int gap = 1;
-    (void)nfb;
-    const int nL = tn.cnt[li * 4 + 0];
-    // leaf-slot order (lexicographic) keeps neighbouring threads on neighbouring cells
-    GRID_STRIDE(sl_, 0, nL)
-    {
-        const int lin = tn.cells[li][sl_];
-        if ((fl.kind[li][lin] & K_FB) == 0)
-            continue;
-        const unsigned mask = fl.fbm[li][lin], dmask = fl.fbd[li][lin];
-        const long long slot = lin; // dense storage
-        int x, y;
-        lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-        for (int b = 0; b < kB; ++b)
+        const double sx = __dadd_rn(ox, __dmul_rn(__dadd_rn((double)x, __ddiv_rn((double)a + 0.5, (double)ns)), dx));
+        const double ddx = __dsub_rn(sx, cx);
+        const double rx = __dmul_rn(ddx, ddx);
+        for (int b = 0; b < ns; ++b)
         {
-            const int ox = D == 1 ? b - 2 : b / 5 - 2, oy = D == 1 ? 0 : b % 5 - 2;
-            int xx = x + ox, yy = y + oy;
-            bool in = true;
-            if (g.per0)
-                xx = mr_coord(xx, nx, 1);
-            else
-                in = xx >= 0 && xx < nx;
-            if (D == 2)
-            {
-                if (g.per1)
-                    yy = mr_coord(yy, ny, 1);
-                else
-                    in = in && yy >= 0 && yy < ny;
-            }
-            // linear index, clamped for out-of-domain stencil cells (MR boundary rule, D.8)
-            sBox[b][threadIdx.x] = in ? xy2lin<D>(xx, yy, ny) : mr_lin<D>(g, m, x + ox, y + oy);
-        }
-        for (int r = 0; r < kR; ++r)
-        {
-            const int rx = 2 * x - 1 + (D == 1 ? r : r / 4), ry = D == 1 ? 0 : 2 * y - 1 + r % 4;
-            bool in = (g.per0 || (rx >= 0 && rx < nxj)) && (D == 1 || g.per1 || (ry >= 0 && ry < nyj));
-            const int rl = in ? mr_lin<D>(g, g.J1, rx, ry) : -1;
-            sRim[r][threadIdx.x] = (rl >= 0 && (tn.kind[lj][rl] & K_LEAF)) ? rl : -1; // finest leaves only
-        }
-        if constexpr (GEN)
-        {
-            double sE[Q], sA[Q];
-            gen_fb1<EQ, Q>(F1.f[li], cap, F1.f[lj], capj, &sBox[0][threadIdx.x], &sRim[0][threadIdx.x], kT, mask,
-                           dmask, sW, sE, sA);
-            if (dmask)
-                for (int h = 0; h < Q; ++h)
-                    for (int side = 0; side < 2; ++side)
-                        if ((dmask >> (2 * h + side)) & 1u)
-                        {
-                            const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
-                            (side ? sA[h] : sE[h]) = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, slot, aux);
-                        }
-#pragma unroll
-            for (int h = 0; h < Q; ++h)
-            {
-                const long long o = (long long)h * cap + slot;
-                F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sE[h], sA[h])));
-            }
-            continue;
-        }
-        for (int h = 0; h < q; ++h)
-        {
-            const double* Fh = F1.f[li] + (long long)h * cap;
-            const double* Fj = F1.f[lj] + (long long)h * capj;
-            const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
-            double sum[2];
-            for (int side = 0; side < 2; ++side)
-            {
-                const int pair = 2 * h + side;
-                const bool ok = !((mask >> pair) & 1u);
-                const bool dom_bad = (dmask >> pair) & 1u;
-                double acc = 0.0;
-                if (!dom_bad)
-                {
-                    const int2 ti = aux.tidx[(gap * q + h) * 2 + side];
-                    for (int k = ti.x; k < ti.x + ti.y; ++k)
-                    {
-                        const int2 o = aux.toff[k];
-                        const int b = D == 1 ? o.x + 2 : (o.x + 2) * 5 + (o.y + 2);
-                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], Fh[sBox[b][threadIdx.x]]));
-                    }
-                    if (!ok)
-                    {
-                        // Decision D.13b: + details of the rim cells that are finest leaves
-                        for (int r = 0; r < kR; ++r)
-                        {
-                            const int dx = D == 1 ? r : r / 4, dy = D == 1 ? 0 : r % 4;
-                            const int xr = 2 * x - 1 + dx, yr = D == 1 ? 0 : 2 * y - 1 + dy;
-                            const bool inb = dx >= 1 && dx <= 2 && (D == 1 || (dy >= 1 && dy <= 2));
-                            const bool ine = (dx + ex) >= 1 && (dx + ex) <= 2 && (D == 1 || ((dy + ey) >= 1 && (dy + ey) <= 2));
-                            if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
-                                continue;
-                            const int sj = sRim[r][threadIdx.x];
-                            if (sj < 0)
-                                continue;
-                            const int xc = mr_coord(xr, nxj, g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
-                            // parent offset from the leaf: ((xc >> 1) - x) in {-1, 0, 1} modulo wrap
-                            const int pdx = (dx + 1) / 2 - 1, pdy = D == 1 ? 0 : (dy + 1) / 2 - 1;
-                            constexpr int NS = D == 1 ? 3 : 9;
-                            double sv[NS];
-                            for (int o = 0; o < NS; ++o)
-                            {
-                                const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-                                const int b = D == 1 ? pdx + ox + 2 : (pdx + ox + 2) * 5 + (pdy + oy + 2);
-                                sv[o] = Fh[sBox[b][threadIdx.x]];
-                            }
-                            acc = __dadd_rn(acc, __dsub_rn(Fj[sj], mr_predict<D>(sv, xc & 1, yc & 1)));
-                        }
-                    }
-                }
-                else
-                {
-                    const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
-                    acc = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, slot, aux);
-                }
-                sum[side] = acc;
-            }
-            const long long o = (long long)h * cap + slot;
-            F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+            const double sy = __dadd_rn(oy, __dmul_rn(__dadd_rn((double)y, __ddiv_rn((double)b + 0.5, (double)ns)), dx));
+            const double ddy = __dsub_rn(sy, cy);
+            cnt += __dadd_rn(rx, __dmul_rn(ddy, ddy)) < r2;
         }
     }
+    return cnt > 0 ? __ddiv_rn((double)cnt, (double)(ns * ns)) : 0.0;
 }
 
 // generated unrolled table sums (stream_gen.cuh) for the built-in velocity sets
@@ -1927,11 +1784,361 @@ __device__ __forceinline__ void gen_collide_mv(const CC& cc, bool inverse, const
 #undef GEN_MV
 }
 
+// per-population gap-1 fallback sums (stream_gen.cuh gen_fb1h_*)
+template <int EQ, int Q>
+__device__ __forceinline__ void gen_fb1h(int h, const double* Fin, long long cap, const double* Fj, long long capj,
+                                         const int* box, const int* rim, int bstride, unsigned mask, unsigned dmask,
+                                         const double* sW, double& sE, double& sA)
+{
+    if constexpr (EQ == 1 && Q == 2)
+        gen_fb1h_EQ1(h, Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 2 && Q == 9)
+        gen_fb1h_EQ2(h, Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 3 && Q == 4)
+        gen_fb1h_EQ3(h, Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 4 && Q == 16)
+        gen_fb1h_EQ4(h, Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
+    else if constexpr (EQ == 5 && Q == 9)
+        gen_fb1h_EQ5(h, Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
+}
+
+// row i of the generated pattern-unrolled M f / M^-1 m
+template <int EQ, int Q, class CC>
+__device__ __forceinline__ double gen_collide_row(const CC& cc, bool inverse, int i, const double (&x)[Q])
+{
+#define GEN_ROW(N) return inverse ? gen_minv_row_EQ##N(cc, i, x) : gen_mf_row_EQ##N(cc, i, x);
+    if constexpr (EQ == 1 && Q == 2)
+    {
+        GEN_ROW(1)
+    }
+    else if constexpr (EQ == 2 && Q == 9)
+    {
+        GEN_ROW(2)
+    }
+    else if constexpr (EQ == 3 && Q == 4)
+    {
+        GEN_ROW(3)
+    }
+    else if constexpr (EQ == 4 && Q == 16)
+    {
+        GEN_ROW(4)
+    }
+    else
+    {
+        GEN_ROW(5)
+    }
+#undef GEN_ROW
+}
+
+// Gap-1 fallback leaves (level J-1, Decision D.13b): stream AND collide, Q warps per
+// block.  Blocks take chunks of the level's leaf slots (lexicographic) interleaved, so
+// the resident blocks sweep the level together and the box rows they share stay in L2.
+// Each block compacts the chunk's fallback leaves into a shared queue in slot order and
+// processes them in batches of 32 consecutive fallback leaves:
+//   A. all threads: the leaf's 5^D level-l box and the 4^D finest-level cells around its
+//      children (linear indices; -1 for rim cells that are not finest leaves);
+//   B. warp h, lane k: population h of leaf k -- the flattened table where exact, plus
+//      the details of the rim leaves where only finer neighbours break it, or the
+//      boundary rim (rim_sum) where the dependencies leave the domain;
+//   C. the collision row by row: warp i computes m_i = row i of M f, warp 0 the
+//      equilibrium / relaxation (and the obstacle fraction) per leaf, warp i then
+//      f*_i = row i of M^-1 m' (+ blend), written to F0.
+// Every value uses the same operations in the same order as K7, so the result is
+// identical; the leaves' loads are spread over Q warps instead of one thread.
+template <int D, int Q, int BS, int EQ, bool GEN>
+__global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+                                                const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
+                                                const __grid_constant__ Flags fl, const SchemeDev* scg,
+                                                const __grid_constant__ Aux aux,
+                                                const __grid_constant__ CollC<Q, BS> cc)
+{
+    constexpr int kB = D == 1 ? 5 : 25; // level-l box
+    constexpr int kR = D == 1 ? 4 : 16; // finest-level 4^D box around the children
+    constexpr int NT = 32 * Q;
+    constexpr int kMaxE = 2 * Q * 25;
+    __shared__ int sBox[kB][32];
+    __shared__ int sRim[kR][32];
+    __shared__ int sLin[32], sBad[32];
+    __shared__ unsigned sMask[32], sDmask[32];
+    __shared__ double sF[Q][32], sMo[Q][32], sAlpha[32];
+    __shared__ double sW[kMaxE], sM[Q * BS], sMi[Q * BS], sS[Q], sP[8], sFeq[Q];
+    __shared__ int sQ[NT + 32];
+    __shared__ int sCnt[Q];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int m = g.J1 - 1, li = m - g.J0, lj = li + 1;
+    if (li < 0)
+        return;
+    {
+        // gap-1 table weights in table order, scheme constants
+        const int base = aux.tidx[1 * 2 * Q].x;
+        const int2 last = aux.tidx[1 * 2 * Q + 2 * Q - 1];
+        const int ne = min(last.x + last.y - base, kMaxE);
+        for (int e = tid; e < ne; e += NT)
+            sW[e] = aux.tw[base + e];
+        for (int i = tid; i < Q * BS; i += NT)
+        {
+            sM[i] = cc.M[i];
+            sMi[i] = cc.Mi[i];
+        }
+        for (int i = tid; i < Q; i += NT)
+        {
+            sS[i] = scg->s[i];
+            sFeq[i] = scg->obs_feq[i];
+        }
+        if (tid < 8)
+            sP[tid] = scg->eqp[tid];
+    }
+    __syncthreads();
+    const int q = g.q;
+    const int nL = tn.cnt[li * 4 + 0];
+    const int nx = g.nx[li], ny = g.ny[li], nxj = g.nx[lj], nyj = g.ny[lj];
+    const long long cap = g.cap[li], capj = g.cap[lj];
+    const double scale = ldexp(1.0, D * (m - g.J1));
+    const long long nchunk = (nL + NT - 1) / NT;
+    int qn = 0;
+    long long ch = blockIdx.x;
+    while (ch < nchunk || qn > 0)
+    {
+        if (ch < nchunk && qn < 32)
+        {
+            // append this chunk's fallback leaves to the queue, in slot order
+            const long long sl = ch * NT + tid;
+            int lin = -1;
+            bool isfb = false;
+            if (sl < nL)
+            {
+                lin = tn.cells[li][sl];
+                isfb = (fl.kind[li][lin] & K_FB) != 0;
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, isfb);
+            if (lane == 0)
+                sCnt[wid] = __popc(bal);
+            __syncthreads();
+            int off = qn, tot = qn;
+            for (int w = 0; w < Q; ++w)
+            {
+                const int cw = sCnt[w];
+                off += w < wid ? cw : 0;
+                tot += cw;
+            }
+            if (isfb)
+                sQ[off + __popc(bal & ((1u << lane) - 1u))] = lin;
+            qn = tot;
+            ch += gridDim.x;
+            __syncthreads();
+            if (qn < 32 && ch < nchunk)
+                continue;
+        }
+        const int nb = min(qn, 32);
+        // A: box and rim indices of the batch
+        for (int t = tid; t < 32 * (kB + kR); t += NT)
+        {
+            const int k = t & 31, e = t >> 5;
+            if (k >= nb)
+                continue;
+            int x, y;
+            lin2xy_l<D>(sQ[k], ny, g.lny[li], x, y);
+            if (e < kB)
+            {
+                const int ox = D == 1 ? e - 2 : e / 5 - 2, oy = D == 1 ? 0 : e % 5 - 2;
+                int xx = x + ox, yy = y + oy;
+                bool in = true;
+                if (g.per0)
+                    xx = mr_coord(xx, nx, 1);
+                else
+                    in = xx >= 0 && xx < nx;
+                if (D == 2)
+                {
+                    if (g.per1)
+                        yy = mr_coord(yy, ny, 1);
+                    else
+                        in = in && yy >= 0 && yy < ny;
+                }
+                // clamped for out-of-domain stencil cells (MR boundary rule, D.8)
+                sBox[e][k] = in ? xy2lin<D>(xx, yy, ny) : mr_lin<D>(g, m, x + ox, y + oy);
+            }
+            else
+            {
+                const int r = e - kB;
+                const int rx = 2 * x - 1 + (D == 1 ? r : r / 4), ry = D == 1 ? 0 : 2 * y - 1 + r % 4;
+                const bool in = (g.per0 || (rx >= 0 && rx < nxj)) && (D == 1 || g.per1 || (ry >= 0 && ry < nyj));
+                const int rl = in ? mr_lin<D>(g, g.J1, rx, ry) : -1;
+                sRim[r][k] = (rl >= 0 && (tn.kind[lj][rl] & K_LEAF)) ? rl : -1; // finest leaves only
+            }
+        }
+        if (tid < nb)
+        {
+            const int lin = sQ[tid];
+            sLin[tid] = lin;
+            sMask[tid] = fl.fbm[li][lin];
+            sDmask[tid] = fl.fbd[li][lin];
+            sBad[tid] = 0;
+        }
+        __syncthreads();
+        // B: stream, warp = population
+        if (lane < nb && wid < Q)
+        {
+            const int h = wid, k = lane;
+            const int lin = sLin[k];
+            const unsigned mask = sMask[k], dmask = sDmask[k];
+            double sum[2] = {0.0, 0.0};
+            if constexpr (GEN)
+                gen_fb1h<EQ, Q>(h, F1.f[li], cap, F1.f[lj], capj, &sBox[0][k], &sRim[0][k], 32, mask, dmask, sW, sum[0],
+                                sum[1]);
+            else
+            {
+                const double* Fh = F1.f[li] + (long long)h * cap;
+                const double* Fj = F1.f[lj] + (long long)h * capj;
+                const int ex = scg->eta[h][0], ey = D == 1 ? 0 : scg->eta[h][1];
+                int x, y;
+                lin2xy_l<D>(lin, ny, g.lny[li], x, y);
+                for (int side = 0; side < 2; ++side)
+                {
+                    const int pair = 2 * h + side;
+                    if ((dmask >> pair) & 1u)
+                        continue;
+                    double acc = 0.0;
+                    const int2 ti = aux.tidx[(1 * q + h) * 2 + side];
+                    for (int e = ti.x; e < ti.x + ti.y; ++e)
+                    {
+                        const int2 o = aux.toff[e];
+                        const int bb = D == 1 ? o.x + 2 : (o.x + 2) * 5 + (o.y + 2);
+                        acc = __dadd_rn(acc, __dmul_rn(aux.tw[e], Fh[sBox[bb][k]]));
+                    }
+                    if ((mask >> pair) & 1u)
+                    {
+                        // Decision D.13b: + details of the rim cells that are finest leaves
+                        for (int r = 0; r < kR; ++r)
+                        {
+                            const int dx = D == 1 ? r : r / 4, dy = D == 1 ? 0 : r % 4;
+                            const int xr = 2 * x - 1 + dx, yr = D == 1 ? 0 : 2 * y - 1 + dy;
+                            const bool inb = dx >= 1 && dx <= 2 && (D == 1 || (dy >= 1 && dy <= 2));
+                            const bool ine = (dx + ex) >= 1 && (dx + ex) <= 2 &&
+                                             (D == 1 || ((dy + ey) >= 1 && (dy + ey) <= 2));
+                            if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
+                                continue;
+                            const int sj = sRim[r][k];
+                            if (sj < 0)
+                                continue;
+                            const int xc = mr_coord(xr, nxj, g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
+                            const int pdx = (dx + 1) / 2 - 1, pdy = D == 1 ? 0 : (dy + 1) / 2 - 1;
+                            constexpr int NS = D == 1 ? 3 : 9;
+                            double sv[NS];
+                            for (int o = 0; o < NS; ++o)
+                            {
+                                const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+                                const int bb = D == 1 ? pdx + ox + 2 : (pdx + ox + 2) * 5 + (pdy + oy + 2);
+                                sv[o] = Fh[sBox[bb][k]];
+                            }
+                            acc = __dadd_rn(acc, __dsub_rn(Fj[sj], mr_predict<D>(sv, xc & 1, yc & 1)));
+                        }
+                    }
+                    sum[side] = acc;
+                }
+            }
+            if (dmask)
+            {
+                int x, y;
+                lin2xy_l<D>(lin, ny, g.lny[li], x, y);
+                for (int side = 0; side < 2; ++side)
+                    if ((dmask >> (2 * h + side)) & 1u)
+                    {
+                        const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
+                        sum[side] = rim_sum<D>(g, tn, F1, scg, h, side, bx0, bx1, by0, by1, li, lin, aux);
+                    }
+            }
+            sF[h][k] = __dadd_rn(F1.f[li][(long long)h * cap + lin], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+        }
+        __syncthreads();
+        // C1: m_i = row i of M f
+        if (lane < nb && wid < Q)
+        {
+            const int i = wid, k = lane;
+            double f[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j)
+                f[j] = sF[j][k];
+            double acc = 0.0;
+            if constexpr (GEN)
+                acc = gen_collide_row<EQ, Q>(cc, false, i, f);
+            else
+            {
+                const int b0 = (i / BS) * BS;
+#pragma unroll
+                for (int j = 0; j < BS; ++j)
+                    acc = __dadd_rn(acc, __dmul_rn(sM[i * BS + j], f[b0 + j]));
+            }
+            sMo[i][k] = acc;
+        }
+        __syncthreads();
+        // C2: equilibrium and relaxation per leaf; obstacle fraction
+        if (wid == 0 && lane < nb)
+        {
+            const int k = lane;
+            double mo[Q], meq[Q];
+#pragma unroll
+            for (int i = 0; i < Q; ++i)
+                mo[i] = sMo[i][k];
+            equilibrium_t<EQ, Q>(sP, scg->lambda, mo, meq);
+#pragma unroll
+            for (int i = 0; i < Q; ++i)
+                sMo[i][k] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, sS[i]), mo[i]), __dmul_rn(sS[i], meq[i]));
+            double alpha = 0.0;
+            if constexpr (EQ == MRLBM_EQ_NS_D2Q9 && D == 2)
+            {
+                if (scg->obstacle == 1)
+                {
+                    int x, y;
+                    lin2xy_l<D>(sLin[k], ny, g.lny[li], x, y);
+                    alpha = obstacle_alpha(scg, m, x, y);
+                }
+            }
+            sAlpha[k] = alpha;
+        }
+        __syncthreads();
+        // C3: f*_i = row i of M^-1 m', blend, store
+        if (lane < nb && wid < Q)
+        {
+            const int i = wid, k = lane;
+            double mo[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j)
+                mo[j] = sMo[j][k];
+            double fi = 0.0;
+            if constexpr (GEN)
+                fi = gen_collide_row<EQ, Q>(cc, true, i, mo);
+            else
+            {
+                const int b0 = (i / BS) * BS;
+#pragma unroll
+                for (int j = 0; j < BS; ++j)
+                    fi = __dadd_rn(fi, __dmul_rn(sMi[i * BS + j], mo[b0 + j]));
+            }
+            const double alpha = sAlpha[k];
+            if (alpha > 0.0)
+                fi = __dadd_rn(__dmul_rn(alpha, sFeq[i]), __dmul_rn(__dsub_rn(1.0, alpha), fi));
+            if (!isfinite(fi))
+                sBad[k] = 1;
+            F0.f[li][(long long)i * cap + sLin[k]] = fi;
+        }
+        // shift the queue
+        const int rest = qn - nb;
+        const int carry = tid < rest ? sQ[32 + tid] : 0;
+        __syncthreads();
+        if (tid < rest)
+            sQ[tid] = carry;
+        if (tid < nb && sBad[tid])
+            flag_err(aux.err, 1);
+        qn = rest;
+        __syncthreads();
+    }
+}
+
 // K7: table-path stream + collision +
 // obstacle blend, one thread per leaf.  Fallback leaves take their post-stream
 // populations from K8 (already in F0).  BS = block size of the block-diagonal M.
 // MODE 0 streams the table-path leaves only (no calls, no stack: the hot kernel);
-// MODE 1 the fallback leaves (values from K8 / k_stream_fb1, or the boundary rim).
+// MODE 1 the fallback leaves at gap 0 (boundary rim) and gap >= 2 (values from K8).
 template <int D, int Q, int BS, int EQ, bool GEN, int MODE, int GC>
 __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     k_stream_collide(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld F0,
@@ -2006,6 +2213,8 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
         if (((kd & K_FB) != 0) != (MODE == 1))
             continue;
         constexpr bool fb = MODE == 1;
+        if (fb && gap == 1)
+            continue; // streamed and collided by k_fb1
         double f[Q];
         if (fb && gap >= kDeepGap)
         {
@@ -2166,41 +2375,14 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
         {
             if (scg->obstacle == 1)
             {
-                // config 5 volume-fraction blend
                 int x, y;
                 lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-                const double dx = ldexp(1.0, -m);
-                const double ox = scg->origin[0], oy = scg->origin[1];
-                const double cx = scg->obs_c[0], cy = scg->obs_c[1], r = scg->obs_r;
-                const double x0 = __dadd_rn(ox, __dmul_rn((double)x, dx));
-                const double y0 = __dadd_rn(oy, __dmul_rn((double)y, dx));
-                const double x1 = __dadd_rn(x0, dx), y1 = __dadd_rn(y0, dx);
-                const bool cand = !(x1 < __dsub_rn(cx, r) || x0 > __dadd_rn(cx, r) || y1 < __dsub_rn(cy, r) ||
-                                    y0 > __dadd_rn(cy, r));
-                if (cand)
+                const double alpha = obstacle_alpha(scg, m, x, y);
+                if (alpha > 0.0)
                 {
-                    const int ns = scg->obs_ns;
-                    const double r2 = __dmul_rn(r, r);
-                    int cnt = 0;
-                    for (int a = 0; a < ns; ++a)
-                    {
-                        const double sx = __dadd_rn(ox, __dmul_rn(__dadd_rn((double)x, __ddiv_rn((double)a + 0.5, (double)ns)), dx));
-                        const double ddx = __dsub_rn(sx, cx);
-                        const double rx = __dmul_rn(ddx, ddx);
-                        for (int b = 0; b < ns; ++b)
-                        {
-                            const double sy = __dadd_rn(oy, __dmul_rn(__dadd_rn((double)y, __ddiv_rn((double)b + 0.5, (double)ns)), dx));
-                            const double ddy = __dsub_rn(sy, cy);
-                            cnt += __dadd_rn(rx, __dmul_rn(ddy, ddy)) < r2;
-                        }
-                    }
-                    if (cnt > 0)
-                    {
-                        const double alpha = __ddiv_rn((double)cnt, (double)(ns * ns));
 #pragma unroll
-                        for (int h = 0; h < Q; ++h)
-                            f[h] = __dadd_rn(__dmul_rn(alpha, sFeq[h]), __dmul_rn(__dsub_rn(1.0, alpha), f[h]));
-                    }
+                    for (int h = 0; h < Q; ++h)
+                        f[h] = __dadd_rn(__dmul_rn(alpha, sFeq[h]), __dmul_rn(__dsub_rn(1.0, alpha), f[h]));
                 }
             }
         }
@@ -2771,18 +2953,23 @@ void enqueue_step(mrlbm_ctx* c)
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
     { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
-    { c->kcount++; k_stream_fb1<D, Q, EQ, GEN><<<c->grid_cap * 2, 128, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fb1", -1); }
+    CollC<Q, BS> cc;
+    for (int i = 0; i < Q; ++i)
+        for (int j = 0; j < BS; ++j)
+        {
+            const int col = (i / BS) * BS + j;
+            cc.M[i * BS + j] = c->sc.M[i * Q + col];
+            cc.Mi[i * BS + j] = c->sc.Minv[i * Q + col];
+        }
+    if (c->J1 > c->J0)
+    {
+        c->kcount++;
+        k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+        kmark(c, "k_fb1", -1);
+    }
     {
         LGrid lg = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
         c->kcount++;
-        CollC<Q, BS> cc;
-        for (int i = 0; i < Q; ++i)
-            for (int j = 0; j < BS; ++j)
-            {
-                const int col = (i / BS) * BS + j;
-                cc.M[i * BS + j] = c->sc.M[i * Q + col];
-                cc.Mi[i * BS + j] = c->sc.Minv[i * Q + col];
-            }
         if constexpr (GEN)
         {
             // the generated path in two register budgets: the finest level (gap 0) alone,
