@@ -619,9 +619,17 @@ __global__ void __launch_bounds__(256) k_band(Geo g, Flags fl, Aux aux)
     }
 }
 
-// ghost layer: cells not in R within Chebyshev distance 2 of an R cell.
-// 2D: separable dilation, pass 1 ORs R-membership over y +-2 into tmp, pass 2
-// ORs tmp over x +-2 (10 byte reads per cell instead of 25).
+// ghost layer: cells not in R within Chebyshev distance gd of an R cell, gd = 2 below
+// the finest level (the 5^d table boxes and the predictions of the next level's ghosts
+// reach that far), gd = 1 at the finest level (only the gap-0 stream reads its ghosts:
+// the 3^d neighbours; any other finest-level value is predicted on the fly, rim_value).
+// 2D: separable dilation, pass 1 ORs R-membership over y +-gd into tmp, pass 2
+// ORs tmp over x +-gd (10 byte reads per cell instead of 25).
+__device__ __forceinline__ int ghost_dist(const Geo& g, int m)
+{
+    return m == g.J1 ? 1 : 2;
+}
+
 template <int D>
 __global__ void k_ghost_rows(Geo g, Flags fl, LGrid lg_)
 {
@@ -635,9 +643,12 @@ __global__ void k_ghost_rows(Geo g, Flags fl, LGrid lg_)
         int x, y;
         lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
         uint8_t r = 0;
+        const int gd = ghost_dist(g, m);
 #pragma unroll
         for (int oy = -2; oy <= 2; ++oy)
         {
+            if (oy < -gd || oy > gd)
+                continue;
             int yy = y + oy;
             if (yy < 0 || yy >= ny)
             {
@@ -666,9 +677,12 @@ __global__ void k_ghost(Geo g, Flags fl, LGrid lg_)
         int x, y;
         lin2xy_l<D>((int)i, ny, g.lny[li], x, y);
         bool near = false;
+        const int gd = ghost_dist(g, m);
 #pragma unroll
         for (int ox = -2; ox <= 2; ++ox)
         {
+            if (ox < -gd || ox > gd)
+                continue;
             int xx = x + ox;
             if (xx < 0 || xx >= nx)
             {
@@ -913,9 +927,18 @@ __global__ void k_ghost_rows_v(Geo g, Flags fl, LGrid lg_)
             w[j] = vl;
             w[18 + j] = vr;
         }
+        if (ghost_dist(g, m) == 1)
+        {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            o.b[j] = w[j] | w[j + 1] | w[j + 2] | w[j + 3] | w[j + 4];
+            for (int j = 0; j < 16; ++j)
+                o.b[j] = w[j + 1] | w[j + 2] | w[j + 3];
+        }
+        else
+        {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                o.b[j] = w[j] | w[j + 1] | w[j + 2] | w[j + 3] | w[j + 4];
+        }
         reinterpret_cast<uint4*>(tmp)[c] = o.v;
     }
 }
@@ -942,9 +965,12 @@ __global__ void k_ghost_v(Geo g, Flags fl, LGrid lg_)
         const int x = (int)(c / cpr), cy = (int)(c - (long long)x * cpr);
         V16 acc;
         acc.v = make_uint4(0, 0, 0, 0);
+        const int gd = ghost_dist(g, m);
 #pragma unroll
         for (int ox = -2; ox <= 2; ++ox)
         {
+            if (ox < -gd || ox > gd)
+                continue;
             int xx = x + ox;
             if (xx < 0 || xx >= nx)
             {
