@@ -53,6 +53,7 @@ struct Geo {
 struct Tree {
     uint8_t* kind[kL];  // dense per cell: K_LEAF / K_INT / K_VIRT (+ K_FB) of this tree version
     int32_t* cells[kL]; // slot -> linear index: leaves | internal | virtual, each lexicographic
+    uint8_t* skind[kL]; // slot -> kind of that cell (read with cells[], no dependent gather)
     int* cnt;           // [nlev][4] = nL, nI, nV, -
 };
 
@@ -1292,13 +1293,18 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
             wpre += wsum[k][w];
         pos[k] = catbase[k] + tile_offsets[(long long)lvb_ * 3 + k] + wpre + pre[k];
     }
+    uint8_t* skind = tn.skind[li];
 #pragma unroll
     for (int j = 0; j < 16; ++j)
     {
         const long long i = base + j;
         const int ct = cat_of(b[j]);
         if (i < n && ct < 3)
-            cells[pos[ct]++] = (int)i;
+        {
+            const int sl = pos[ct]++;
+            cells[sl] = (int)i;
+            skind[sl] = b[j];
+        }
     }
 }
 
@@ -1934,7 +1940,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
             if (sl < nL)
             {
                 lin = tn.cells[li][sl];
-                isfb = (fl.kind[li][lin] & K_FB) != 0;
+                isfb = (tn.skind[li][sl] & K_FB) != 0;
             }
             const unsigned bal = __ballot_sync(0xffffffffu, isfb);
             if (lane == 0)
@@ -2232,10 +2238,21 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     double* Fout = F0.f[li];
     const int per0 = g.per0, per1 = g.per1;
     int* myslot = &sSlot[0][threadIdx.x];
-    LGRID_STRIDE(s, 0, nL)
+    // grid-stride over the leaf slots with the next slot's (index, kind) loaded one
+    // iteration ahead, so the value gathers never wait on the slot list
+    const long long sstep = (long long)lvg_ * blockDim.x;
+    long long s = (long long)lvb_ * blockDim.x + threadIdx.x;
+    int lin_next = s < nL ? tn.cells[li][s] : 0;
+    uint8_t kd_next = s < nL ? tn.skind[li][s] : 0;
+    for (; s < nL; s += sstep)
     {
-        const int lin = tn.cells[li][s];
-        const uint8_t kd = fl.kind[li][lin];
+        const int lin = lin_next;
+        const uint8_t kd = kd_next;
+        if (s + sstep < nL)
+        {
+            lin_next = tn.cells[li][s + sstep];
+            kd_next = tn.skind[li][s + sstep];
+        }
         if (((kd & K_FB) != 0) != (MODE == 1))
             continue;
         constexpr bool fb = MODE == 1;
@@ -2648,6 +2665,7 @@ struct mrlbm_ctx {
     Geo geo{};
     cudaStream_t stream = nullptr;
     int32_t* cells[2][kL]{};
+    uint8_t* skind[2][kL]{}; // per tree version: kinds in slot order
     uint8_t* kind2[2][kL]{}; // per tree version: dense cell kinds
     int* cnt[2]{};
     uint8_t* rn[kL]{};
@@ -2733,6 +2751,7 @@ Tree tree_of(mrlbm_ctx* c, int v)
     {
         t.kind[i] = c->kind2[v][i];
         t.cells[i] = c->cells[v][i];
+        t.skind[i] = c->skind[v][i];
     }
     t.cnt = c->cnt[v];
     return t;
@@ -3220,6 +3239,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             for (int v = 0; v < 2; ++v)
             {
                 CU(cudaMalloc(&ctx->cells[v][li], sizeof(int32_t) * n));
+                CU(cudaMalloc(&ctx->skind[v][li], n));
                 CU(cudaMalloc(&ctx->kind2[v][li], n));
                 CU(cudaMemset(ctx->kind2[v][li], 0, n));
                 CU(cudaMalloc(&ctx->F[v][li], sizeof(double) * n * ctx->q));
@@ -3824,6 +3844,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         {
             cudaFree(ctx->kind2[v][li]);
             cudaFree(ctx->cells[v][li]);
+            cudaFree(ctx->skind[v][li]);
             cudaFree(ctx->F[v][li]);
         }
     }
