@@ -485,19 +485,23 @@ __global__ void k_grade(Geo g, Flags fl, int m)
             continue;
         int px, py;
         lin2xy_l<D>((int)i, ny, g.lny[li], px, py);
-        for (int ox = -1; ox <= 1; ++ox)
-            for (int oy = (D == 1 ? 0 : -1); oy <= (D == 1 ? 0 : 1); ++oy)
+        // the parents of the 3^D box: the distinct values of (px +- 1) >> 1 per axis
+        // (px >> 1 is always one of them; an out-of-domain neighbour adds nothing)
+        auto par = [](int c, int o, int n, int per) {
+            int v = c + o;
+            if (v < 0 || v >= n)
             {
-                int x = px + ox, y = py + oy;
-                if (!g.per0 && (x < 0 || x >= nx))
-                    continue;
-                if (D == 2 && !g.per1 && (y < 0 || y >= ny))
-                    continue;
-                x = mr_coord(x, nx, 1);
-                if (D == 2)
-                    y = mr_coord(y, ny, 1);
-                fl.rn[li - 1][xy2lin<D>(x >> 1, y >> 1, nyp)] = 1;
+                if (!per)
+                    return c >> 1;
+                v = mr_coord(v, n, 1);
             }
+            return v >> 1;
+        };
+        const int ax0 = par(px, -1, nx, g.per0), ax1 = par(px, 1, nx, g.per0);
+        const int ay0 = D == 2 ? par(py, -1, ny, g.per1) : 0, ay1 = D == 2 ? par(py, 1, ny, g.per1) : 0;
+        for (int a = 0; a < (ax1 != ax0 ? 2 : 1); ++a)
+            for (int b = 0; b < (ay1 != ay0 ? 2 : 1); ++b)
+                fl.rn[li - 1][xy2lin<D>(a ? ax1 : ax0, b ? ay1 : ay0, nyp)] = 1;
     }
 }
 
@@ -1037,21 +1041,35 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count(const uint8_t* kind
     const long long base = (long long)blockIdx.x * kTile + (long long)threadIdx.x * 16;
     uint8_t b[16];
     load16(kind, base, n, b);
+    // the kinds are exclusive bits: count them four bytes at a time
     int c[3] = {0, 0, 0};
+    {
+        unsigned wv[4];
+        memcpy(wv, b, 16);
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-    {
-        c[0] += b[j] & K_LEAF ? 1 : 0;
-        c[1] += b[j] & K_INT ? 1 : 0;
-        c[2] += b[j] & K_VIRT ? 1 : 0;
+        for (int k = 0; k < 4; ++k)
+        {
+            c[0] += __popc(wv[k] & 0x01010101u * K_LEAF);
+            c[1] += __popc(wv[k] & 0x01010101u * K_INT);
+            c[2] += __popc(wv[k] & 0x01010101u * K_VIRT);
+        }
     }
-    for (int k = 0; k < 3; ++k)
+    if (__any_sync(0xffffffffu, (c[0] | c[1] | c[2]) != 0))
     {
-        int v = c[k];
-        for (int o = 16; o > 0; o >>= 1)
-            v += __shfl_down_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0)
-            red[k][threadIdx.x >> 5] = v;
+        for (int k = 0; k < 3; ++k)
+        {
+            int v = c[k];
+            for (int o = 16; o > 0; o >>= 1)
+                v += __shfl_down_sync(0xffffffffu, v, o);
+            if ((threadIdx.x & 31) == 0)
+                red[k][threadIdx.x >> 5] = v;
+        }
+    }
+    else if ((threadIdx.x & 31) == 0)
+    {
+        red[0][threadIdx.x >> 5] = 0;
+        red[1][threadIdx.x >> 5] = 0;
+        red[2][threadIdx.x >> 5] = 0;
     }
     __syncthreads();
     if (threadIdx.x < 3)
@@ -1175,21 +1193,35 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(Geo g, Flags fl,
     const long long base = (long long)lvb_ * kTile + (long long)threadIdx.x * 16;
     uint8_t b[16];
     load16(kind, base, n, b);
+    // the kinds are exclusive bits: count them four bytes at a time
     int c[3] = {0, 0, 0};
+    {
+        unsigned wv[4];
+        memcpy(wv, b, 16);
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-    {
-        c[0] += b[j] & K_LEAF ? 1 : 0;
-        c[1] += b[j] & K_INT ? 1 : 0;
-        c[2] += b[j] & K_VIRT ? 1 : 0;
+        for (int k = 0; k < 4; ++k)
+        {
+            c[0] += __popc(wv[k] & 0x01010101u * K_LEAF);
+            c[1] += __popc(wv[k] & 0x01010101u * K_INT);
+            c[2] += __popc(wv[k] & 0x01010101u * K_VIRT);
+        }
     }
-    for (int k = 0; k < 3; ++k)
+    if (__any_sync(0xffffffffu, (c[0] | c[1] | c[2]) != 0))
     {
-        int v = c[k];
-        for (int o = 16; o > 0; o >>= 1)
-            v += __shfl_down_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0)
-            red[k][threadIdx.x >> 5] = v;
+        for (int k = 0; k < 3; ++k)
+        {
+            int v = c[k];
+            for (int o = 16; o > 0; o >>= 1)
+                v += __shfl_down_sync(0xffffffffu, v, o);
+            if ((threadIdx.x & 31) == 0)
+                red[k][threadIdx.x >> 5] = v;
+        }
+    }
+    else if ((threadIdx.x & 31) == 0)
+    {
+        red[0][threadIdx.x >> 5] = 0;
+        red[1][threadIdx.x >> 5] = 0;
+        red[2][threadIdx.x >> 5] = 0;
     }
     __syncthreads();
     if (threadIdx.x < 3)
@@ -1256,6 +1288,18 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
     constexpr int NW = kTileThreads / 32;
     __shared__ int wsum[3][NW];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    {
+        // empty tile (exclusive offsets equal to the next tile's / the level totals): done
+        const int ntl = (int)((n + kTile - 1) / kTile);
+        bool empty = true;
+        for (int k = 0; k < 3; ++k)
+        {
+            const int nxt = lvb_ + 1 < ntl ? tile_offsets[(long long)(lvb_ + 1) * 3 + k] : cnt[k];
+            empty = empty && nxt == tile_offsets[(long long)lvb_ * 3 + k];
+        }
+        if (empty)
+            return;
+    }
     const long long base = (long long)lvb_ * kTile + (long long)threadIdx.x * 16;
     uint8_t b[16];
     load16(kind, base, n, b);
@@ -1611,24 +1655,82 @@ __device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const Sch
     return s;
 }
 
-// K8: stream of the fallback leaves, one thread per (leaf, population).  Each side
-// uses the flattened table when it is exact for this leaf, else the recursive
-// reconstruction (materialised virtual cells at the finest level + boundary rule).
-// Writes post-stream populations into F0 at the leaf's slot; K7 collides them.
+// The i-th finest-level cell of the E (side 0) or A (side 1) rim of the box
+// [bx0, bx1) x [by0, by1) for velocity (ex, ey), in rim_sum's loop order: at most one
+// x of the range contributes a whole column (the first or the last), the others one
+// cell each when ey != 0.  Returns the count with i < 0.
+template <int D>
+__device__ __forceinline__ int rim_cell(int side, int ex, int ey, int bx0, int bx1, int by0, int by1, int i, int& x,
+                                        int& y)
+{
+    const int nx = bx1 - bx0;
+    const int colLen = D == 2 ? by1 - by0 : 1;
+    const bool single = D == 2 && ey != 0;
+    // column position: 0 none, 1 first x of the range, 2 last
+    const int colpos = ex == 0 ? 0 : (side == 0 ? (ex > 0 ? 1 : 2) : (ex > 0 ? 2 : 1));
+    const int xs = side == 0 ? bx0 - ex : bx0;
+    const int ycol = side == 0 ? by0 - ey : by0;
+    const int ysgl = side == 0 ? (ey > 0 ? by0 - 1 : by1) : (ey > 0 ? by1 - 1 : by0);
+    const int nsg = single ? nx - (colpos ? 1 : 0) : 0;
+    if (i < 0)
+        return (colpos ? colLen : 0) + nsg;
+    if (colpos == 1)
+    {
+        if (i < colLen)
+        {
+            x = xs;
+            y = D == 2 ? ycol + i : 0;
+        }
+        else
+        {
+            x = xs + 1 + (i - colLen);
+            y = ysgl;
+        }
+    }
+    else if (colpos == 2)
+    {
+        if (i < nsg)
+        {
+            x = xs + i;
+            y = ysgl;
+        }
+        else
+        {
+            x = xs + nx - 1;
+            y = D == 2 ? ycol + (i - nsg) : 0;
+        }
+    }
+    else
+    {
+        x = xs + i;
+        y = ysgl;
+    }
+    return 0;
+}
+
+// K8: stream of the deep-gap (gap >= 2) fallback leaves, one warp per (leaf,
+// population).  Each side uses the flattened table when it is exact for this leaf,
+// else the recursive reconstruction of the finest-level rim (materialised band cells
+// or on-the-fly predictions, plus the boundary rule).  The lanes load the table
+// operands / evaluate the rim cells in parallel; the sums are then accumulated in
+// table / rim order through shuffles, so the arithmetic is rim_sum's.  Writes
+// post-stream populations into F0; K7 collides them.
 template <int D>
 __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* sc,
                                                          Aux aux)
 {
     const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
     const int q = g.q;
-    GRID_STRIDE(t, 0, (long long)nfb * q)
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long t = gw; t < (long long)nfb * q; t += nw)
     {
         const int it = (int)(t / q), h = (int)(t % q);
         const int2 e = aux.fb_list[it];
         if (g.J1 - e.x < 2)
             continue; // gap 1: k_fb1
         const unsigned mask = aux.fb_mask[it];
-        const unsigned dmask = aux.fb_dmask[it];
         const int m = e.x, li = m - g.J0;
         const long long slot = e.y; // dense storage: values live at the linear index
         const int ny = g.ny[li];
@@ -1636,71 +1738,60 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
         int x, y;
         lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
         const int gap = g.J1 - m;
+        const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
         double sums[2];
         for (int side = 0; side < 2; ++side)
         {
-            const int key = (gap * q + h) * 2 + side;
-            (void)key;
-            const bool ok = ((mask >> (2 * h + side)) & 1u) == 0;
             double acc = 0.0;
-            const bool corr = !ok && gap == 1 && !((dmask >> (2 * h + side)) & 1u);
-            if (ok || corr)
+            if (((mask >> (2 * h + side)) & 1u) == 0)
             {
-                const int2 ti = aux.tidx[key];
-                for (int k = ti.x; k < ti.x + ti.y; ++k)
+                // flattened table (<= 25 entries): one operand per lane, summed in order
+                const int2 ti = aux.tidx[(gap * q + h) * 2 + side];
+                for (int b0 = 0; b0 < ti.y; b0 += 32)
                 {
-                    const int2 o = aux.toff[k];
-                    const int sl = mr_lin<D>(g, m, x + o.x, y + o.y);
-                    if (!tn.kind[li][sl])
+                    double v = 0.0;
+                    if (b0 + lane < ti.y)
                     {
-                        flag_err(aux.err, 0);
-                        continue;
+                        const int k = ti.x + b0 + lane;
+                        const int2 o = aux.toff[k];
+                        const int sl = mr_lin<D>(g, m, x + o.x, y + o.y);
+                        if (!tn.kind[li][sl])
+                            flag_err(aux.err, 0);
+                        v = __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + sl]);
                     }
-                    acc = __dadd_rn(acc, __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + sl]));
+                    const int nv = min(32, ti.y - b0);
+                    for (int j = 0; j < nv; ++j)
+                        acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, j));
                 }
             }
-            if (corr)
-            {
-                // Decision D.13b: add the details of the rim cells that are leaves
-                const int lj = li + 1;
-                const int nyj = g.ny[lj];
-                const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
-                const int bx0 = 2 * x, bx1 = bx0 + 2, by0 = D == 1 ? 0 : 2 * y, by1 = D == 1 ? 1 : by0 + 2;
-                for (int xr = bx0 - 1; xr <= bx1; ++xr)
-                    for (int yr = (D == 1 ? 0 : by0 - 1); yr <= (D == 1 ? 0 : by1); ++yr)
-                    {
-                        const bool inb = in_box<D>(xr, yr, bx0, bx1, by0, by1);
-                        const bool ine = in_box<D>(xr + ex, yr + ey, bx0, bx1, by0, by1);
-                        if (!(side == 0 ? (ine && !inb) : (inb && !ine)))
-                            continue;
-                        const int xc = mr_coord(xr, g.nx[lj], g.per0), yc = D == 2 ? mr_coord(yr, nyj, g.per1) : 0;
-                        const int sj = xy2lin<D>(xc, yc, nyj);
-                        if (!(tn.kind[lj][sj] & K_LEAF))
-                            continue;
-                        constexpr int NS = D == 1 ? 3 : 9;
-                        double sv[NS];
-                        for (int o = 0; o < NS; ++o)
-                        {
-                            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-                            const int ps = mr_lin<D>(g, m, (xc >> 1) + ox, (yc >> 1) + oy);
-                            sv[o] = F1.f[li][(long long)h * cap + ps];
-                        }
-                        acc = __dadd_rn(acc, __dsub_rn(F1.f[lj][(long long)h * g.cap[lj] + sj],
-                                                       mr_predict<D>(sv, xc & 1, yc & 1)));
-                    }
-            }
-            if (!ok && !corr)
+            else if (ex != 0 || ey != 0)
             {
                 const int side_n = 1 << gap;
                 const int bx0 = x * side_n, bx1 = bx0 + side_n;
                 const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
-                acc = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, slot, aux);
+                int xr = 0, yr = 0;
+                const int n = rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, -1, xr, yr);
+                for (int b0 = 0; b0 < n; b0 += 32)
+                {
+                    double v = 0.0;
+                    if (b0 + lane < n)
+                    {
+                        rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, b0 + lane, xr, yr);
+                        v = rim_value<D>(g, tn, F1, sc, xr, yr, h, li, slot, aux);
+                    }
+                    const int nv = min(32, n - b0);
+                    for (int j = 0; j < nv; ++j)
+                        acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, v, j));
+                }
             }
             sums[side] = acc;
         }
-        const double scale = ldexp(1.0, D * (m - g.J1));
-        const long long o = (long long)h * cap + slot;
-        F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+        if (lane == 0)
+        {
+            const double scale = ldexp(1.0, D * (m - g.J1));
+            const long long o = (long long)h * cap + slot;
+            F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+        }
     }
 }
 
@@ -2925,7 +3016,11 @@ void enqueue_step(mrlbm_ctx* c)
         kmark(c, "k_enlarge", -1);
     }
     for (int m = c->J1 - 1; m > c->J0; --m)
-        { c->kcount++; k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);  kmark(c, "k_grade", m); }
+    {
+        c->kcount++;
+        k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+        kmark(c, "k_grade", m);
+    }
     phase_mark(c, 3);
     // K4 kinds, fallback flags, reconstruction bands, ghosts, compaction
     auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
