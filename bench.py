@@ -108,9 +108,10 @@ def snapshot(s, rc):
     return out
 
 
-def run_cpu_sample(steps=2, jmax=9, threads=None):
+def run_cpu_sample(min_seconds=10.0, max_steps=40, jmax=10, threads=None):
     """CPU oracle (the reference path restated on the reference headers) on a
-    bounded sample: config 5 at J_bar = jmax from its initial datum."""
+    bounded sample: config 5 at J_bar = jmax from its initial datum, stepping
+    until min_seconds of step time (at least 2 steps, at most max_steps)."""
     from oracle import pyoracle
     from paper_2103_02903_b200 import build_config, finest_cells, initial_finest
     cores = threads or os.cpu_count() or 1
@@ -119,12 +120,13 @@ def run_cpu_sample(steps=2, jmax=9, threads=None):
     o = pyoracle.Oracle(sc, rc)
     o.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
     o.commit()
-    upd, secs = 0, 0.0
-    for _ in range(steps):
+    upd, secs, steps = 0, 0.0, 0
+    while steps < max_steps and (steps < 2 or secs < min_seconds):
         t = time.perf_counter()
         o.step(1)
         secs += time.perf_counter() - t
         upd += sum(o.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1))
+        steps += 1
     o.close()
     return {"value": upd / secs, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"config 5 (D2Q9 cylinder) at J_bar={jmax} ({(8 << (jmax - 2)) * (4 << (jmax - 2))} finest cells), "
@@ -288,7 +290,7 @@ def bench_product(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = run_cpu_sample(steps=2, jmax=9)
+        cpu = run_cpu_sample()
 
     if rank == 0:
         leaves_last = [int(st.leaves[i]) for i in range(st.levels)]

@@ -158,6 +158,30 @@ __device__ __forceinline__ int xy2lin(int x, int y, int ny)
     return D == 1 ? x : x * ny + y;
 }
 
+// the 2^D children of cell (px, py) in children order (dx, dy) = (c >> 1, c & 1): two
+// 16-byte loads (2D) / one (1D) -- the sibling pairs along the last axis are adjacent
+// and 16-byte aligned (even index, even level sizes)
+template <int D>
+__device__ __forceinline__ void load_children(const double* __restrict__ src, int px, int py, int ny1,
+                                              double (&ch)[1 << D])
+{
+    if (D == 1)
+    {
+        const double2 a = *reinterpret_cast<const double2*>(src + 2 * px);
+        ch[0] = a.x;
+        ch[1] = a.y;
+    }
+    else
+    {
+        const double2 a = *reinterpret_cast<const double2*>(src + (long long)(2 * px) * ny1 + 2 * py);
+        const double2 b = *reinterpret_cast<const double2*>(src + (long long)(2 * px + 1) * ny1 + 2 * py);
+        ch[0] = a.x;
+        ch[1] = a.y;
+        ch[D == 1 ? 1 : 2] = b.x;
+        ch[D == 1 ? 1 : 3] = b.y;
+    }
+}
+
 // stencil lookup with the MR boundary rule (clamp / wrap), Decision D.8
 template <int D>
 __device__ __forceinline__ int mr_lin(const Geo& g, int m, int x, int y)
@@ -282,10 +306,12 @@ __global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Au
 #pragma unroll
         for (int h = 0; h < Q; ++h)
         {
-            const double* src = F.f[li + 1] + (long long)h * cap1;
+            double ch[1 << D];
+            load_children<D>(F.f[li + 1] + (long long)h * cap1, px, py, ny1, ch);
             double acc = 0.0;
+#pragma unroll
             for (int c = 0; c < (1 << D); ++c)
-                acc = __dadd_rn(acc, src[cs[c]]);
+                acc = __dadd_rn(acc, ch[c]);
             v[h] = __ddiv_rn(acc, (double)(1 << D));
         }
 #pragma unroll
@@ -328,10 +354,12 @@ __global__ void __launch_bounds__(256) k_project_new(Geo g, Tree to, Tree tn, Fl
 #pragma unroll
         for (int h = 0; h < Q; ++h)
         {
-            const double* src = F.f[li + 1] + (long long)h * cap1;
+            double ch[1 << D];
+            load_children<D>(F.f[li + 1] + (long long)h * cap1, px, py, ny1, ch);
             double acc = 0.0;
+#pragma unroll
             for (int c = 0; c < (1 << D); ++c)
-                acc = __dadd_rn(acc, src[cs[c]]);
+                acc = __dadd_rn(acc, ch[c]);
             v[h] = __ddiv_rn(acc, (double)(1 << D));
         }
 #pragma unroll
@@ -391,10 +419,13 @@ __global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl,
             double sv[NS];
             for (int o = 0; o < NS; ++o)
                 sv[o] = fm[st[o]];
+            double ch[1 << D];
+            load_children<D>(f1, px, py, ny1, ch);
+#pragma unroll
             for (int c = 0; c < (1 << D); ++c)
             {
                 const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
-                const double d = __dsub_rn(f1[cs[c]], mr_predict<D>(sv, dx, dy));
+                const double d = __dsub_rn(ch[c], mr_predict<D>(sv, dx, dy));
                 const double ad = fabs(d);
                 if (ad > metric)
                     metric = ad;
