@@ -311,7 +311,7 @@ def bench_product(args):
                        "fallback_leaves_last_step": int(st.fallback_leaves)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "stream+collide phase (K7/K8, one launch per level) per step",
+                         "kernel": "stream+collide phase per step (K8, k_fb1, K7 x3)",
                          "algorithmic_bytes": stream_bytes, "peak_kind": peak_kind},
             "step_roofline": {"bytes_model_per_step": sp.bytes_model,
                               "achieved_gbs": sp.bytes_model / (ms_max / args.steps / 1e3) / 1e9,
