@@ -159,6 +159,28 @@ int mrlbm_reconstruct_finest(mrlbm_ctx* ctx, double* f);
 int mrlbm_additional_error(mrlbm_ctx* adaptive, mrlbm_ctx* reference, const double* row, double* E,
                            double* sums);
 
+/* ---- config-5 integral diagnostics ---- */
+/* Obstacle force tracking.  capacity_steps > 0 records, for each following step, the
+   force on the obstacle F = sum over leaves of alpha * q * |cell| / dt: the momentum the
+   obstacle blend removes per unit time (SPEC.md:476 design decision),
+   q = post-collision momentum moments (m_1, m_2), dt = 2^-J_bar / lambda.  Summed on the
+   device in a fixed order (deterministic).  0 turns it off.  Needs the D2Q9 obstacle
+   configuration (status 2 otherwise). */
+int mrlbm_set_force_tracking(mrlbm_ctx* ctx, int capacity_steps);
+/* per-step forces recorded since tracking was enabled: fx[i], fy[i] for i < min(n, cap);
+   n = steps recorded (status 5 when n exceeds the capacity given to set_force_tracking) */
+int mrlbm_force_history(mrlbm_ctx* ctx, double* fx, double* fy, int cap, int* n);
+/* C_D = 2 F_x / (rho0 u0^2 L), C_L = 2 F_y / (rho0 u0^2 L) */
+int mrlbm_drag_lift(double fx, double fy, double rho0, double u0, double L, double* cd, double* cl);
+/* Strouhal number St = L f / u0 of a lift series sampled every dt (PAPER.md:1380-1383,
+   SPEC.md:477-485): samples [skip, n) are detrended (least-squares line), Hann-windowed
+   and transformed by a direct DFT; f = the bin of the largest non-zero-frequency
+   power.  df (optional) = the frequency resolution 1 / ((n - skip) dt).  Status 3
+   ("no dominant peak") when the detrended series is flat or the peak power is below
+   4x the mean power of the other bins; status 2 for fewer than 8 samples. */
+int mrlbm_strouhal(const double* cl, int64_t n, int64_t skip, double dt, double u0, double L, double* st,
+                   double* df);
+
 /* Flattened reconstruction table:
    sum over the E (side=0) or A (side=1) finest cells of a leaf at gap g of the
    zero-detail reconstruction == sum_i w_i f(l, k + off_i).  Lexicographic

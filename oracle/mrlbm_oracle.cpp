@@ -393,6 +393,9 @@ class Oracle {
     std::int64_t fallback_last = 0;
     std::int64_t leaf_updates = 0;
     std::string err;
+    // obstacle force history: one (Fx, Fy) per step while tracking
+    bool track_force = false;
+    std::vector<double> force_hist;
 
     Oracle(const mrlbm_scheme_spec& s_, const mrlbm_run_config& r_) : sc(s_), rc(r_)
     {
@@ -1009,6 +1012,8 @@ class Oracle {
     {
         const Idx nfine = extent(J1);
         std::int64_t nfb = 0;
+        const bool trk = track_force && rc.obstacle == 1;
+        double force[2] = {0.0, 0.0};
         for (int l = J0; l <= J1; ++l)
         {
             Level& L = lev[l - J0];
@@ -1017,6 +1022,7 @@ class Oracle {
             std::vector<Idx> cells;
             L.leaves.for_each_cell([&](const Idx& c) { cells.push_back(c); });
             std::vector<double> out(cells.size() * q);
+            std::vector<double> fc(trk ? cells.size() * 2 : 0, 0.0);
             std::vector<char> fb(cells.size(), 0);
             OmpErr oe;
 #pragma omp parallel reduction(+ : nfb)
@@ -1126,7 +1132,11 @@ class Oracle {
                         mp[h] = (1.0 - sc.s[h]) * mm[h] + sc.s[h] * meq[h];
                     Minv.multiply(mp.data(), fs.data());
                     if (rc.obstacle == 1)
-                        obstacle_blend(l, k, fs.data());
+                    {
+                        const double alpha = obstacle_blend(l, k, fs.data());
+                        if (trk && alpha > 0.0)
+                            force_terms(l, alpha, mp.data(), &fc[2 * i]);
+                    }
                     for (int h = 0; h < q; ++h)
                     {
                         if (!std::isfinite(fs[h]))
@@ -1139,11 +1149,34 @@ class Oracle {
             // write after all leaves of this level have read their stencils: but
             // stencils also read other levels -> defer the swap until all levels done
             pending.push_back(std::move(out));
+            // obstacle force: level by level, leaves in CellIndex order
+            for (std::size_t i = 0; i < fc.size() / 2; ++i)
+            {
+                force[0] = force[0] + fc[2 * i];
+                force[1] = force[1] + fc[2 * i + 1];
+            }
         }
         for (int l = J0; l <= J1; ++l)
             lev[l - J0].lf = std::move(pending[l - J0]);
         pending.clear();
         fallback_last = nfb;
+        if (trk)
+        {
+            force_hist.push_back(force[0]);
+            force_hist.push_back(force[1]);
+        }
+    }
+
+    // Force on the obstacle (SPEC.md:468-476 design decision "force via momentum
+    // exchange of the obstacle blend"): the momentum the blend removes from a leaf per
+    // unit time, alpha * q * |cell| / dt with q = the post-collision momentum moments
+    // (conserved by the collision) and dt = dx_J / lambda (acoustic scaling).
+    void force_terms(int l, double alpha, const double* mp, double* out) const
+    {
+        const double area = std::ldexp(1.0, -D * l);
+        const double dt = std::ldexp(1.0, -J1) / sc.lambda;
+        for (int a = 0; a < 2; ++a)
+            out[a] = ((alpha * mp[1 + a]) * area) / dt;
     }
     std::vector<std::vector<double>> pending;
 
@@ -1187,7 +1220,7 @@ class Oracle {
 
     // config 5 obstacle: alpha by
     // sub-sampling, f <- alpha feq0 + (1 - alpha) f
-    void obstacle_blend(int l, const Idx& k, double* fs) const
+    double obstacle_blend(int l, const Idx& k, double* fs) const
     {
         const int ns = rc.obstacle_subsamples;
         const double dx = std::ldexp(1.0, -l);
@@ -1201,7 +1234,7 @@ class Oracle {
         // bounding-box rejection (exact in dyadics)
         for (int i = 0; i < D; ++i)
             if (x1[i] < rc.obstacle_center[i] - rc.obstacle_radius || x0[i] > rc.obstacle_center[i] + rc.obstacle_radius)
-                return;
+                return 0.0;
         int cnt = 0;
         for (int a = 0; a < ns; ++a)
             for (int b = 0; b < (D == 1 ? 1 : ns); ++b)
@@ -1216,10 +1249,11 @@ class Oracle {
                 cnt += rr < r2;
             }
         if (cnt == 0)
-            return;
+            return 0.0;
         const double alpha = static_cast<double>(cnt) / (D == 1 ? ns : ns * ns);
         for (int h = 0; h < q; ++h)
             fs[h] = alpha * rc.obstacle_feq[h] + (1.0 - alpha) * fs[h];
+        return alpha;
     }
 
     std::int64_t level_count(int m) const { return lev[m - J0].li.size(); }
@@ -1393,6 +1427,35 @@ int64_t oracle_fallback_leaves(void* p)
 {
     auto* h = static_cast<Handle*>(p);
     return h->o1 ? h->o1->fallback_last : h->o2->fallback_last;
+}
+
+int oracle_set_force_tracking(void* p, int on)
+{
+    auto* h = static_cast<Handle*>(p);
+    return guard(h, [&] {
+        if (h->o1)
+            throw std::invalid_argument("force tracking needs the 2D obstacle configuration");
+        if (h->o2->rc.obstacle != 1)
+            throw std::invalid_argument("force tracking needs an obstacle (run config obstacle = 1)");
+        h->o2->track_force = on != 0;
+        h->o2->force_hist.clear();
+    });
+}
+
+// per-step obstacle forces recorded since tracking was enabled: n = number of steps
+int oracle_force_history(void* p, double* fx, double* fy, int cap, int* n)
+{
+    auto* h = static_cast<Handle*>(p);
+    return guard(h, [&] {
+        const std::vector<double>& v = h->o2 ? h->o2->force_hist : std::vector<double>{};
+        const int k = static_cast<int>(v.size() / 2);
+        for (int i = 0; i < k && i < cap; ++i)
+        {
+            fx[i] = v[2 * i];
+            fy[i] = v[2 * i + 1];
+        }
+        *n = k;
+    });
 }
 
 const char* oracle_last_error(void* p)

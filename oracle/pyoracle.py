@@ -53,6 +53,8 @@ def oracle_lib():
         L.oracle_destroy.argtypes = [vp]
         L.oracle_destroy.restype = None
         L.oracle_set_threads.argtypes = [C.c_int]
+        L.oracle_set_force_tracking.argtypes = [vp, C.c_int]
+        L.oracle_force_history.argtypes = [vp, vp, vp, C.c_int, P(C.c_int)]
         L.oracle_stream_table.argtypes = [C.c_int, C.c_int, P(C.c_int32), C.c_int, C.c_int, vp, vp, P(C.c_int)]
         _orc = L
     return _orc
@@ -148,6 +150,18 @@ class Oracle:
         f = np.zeros((self.q, self.n_finest), dtype=np.float64)
         self._check(self.L.oracle_reconstruct_finest(self.h, f.ctypes.data_as(C.c_void_p)))
         return f
+
+    def set_force_tracking(self, on=True):
+        self._check(self.L.oracle_set_force_tracking(self.h, int(bool(on))))
+
+    def force_history(self):
+        n = C.c_int(0)
+        self._check(self.L.oracle_force_history(self.h, None, None, 0, C.byref(n)))
+        fx = np.zeros(n.value)
+        fy = np.zeros(n.value)
+        self._check(self.L.oracle_force_history(self.h, fx.ctypes.data_as(C.c_void_p), fy.ctypes.data_as(C.c_void_p),
+                                                n.value, C.byref(n)))
+        return fx, fy
 
     def close(self):
         if getattr(self, "h", None):

@@ -5,4 +5,4 @@ the C-ABI in include/mrlbm_gpu.h; this package is the thin host-side mirror.
 """
 from .abi import SchemeSpec, RunConfig, StepStats  # noqa: F401
 from .schemes import build_config, config_steps, finest_cells, initial_finest, stream_table, CONFIG_NAMES  # noqa: F401
-from .solver import Solver, MRLBMError  # noqa: F401
+from .solver import Solver, MRLBMError, drag_lift, strouhal  # noqa: F401

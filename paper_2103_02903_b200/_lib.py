@@ -43,6 +43,12 @@ def lib():
         "mrlbm_build_config": (C.c_int, [C.c_int, C.c_int, C.c_double, P(SchemeSpec), P(RunConfig)]),
         "mrlbm_config_steps": (C.c_int64, [C.c_int, P(RunConfig)]),
         "mrlbm_initial_finest": (C.c_int, [C.c_int, P(SchemeSpec), P(RunConfig), C.c_uint64, vp]),
+        "mrlbm_set_force_tracking": (C.c_int, [vp, C.c_int]),
+        "mrlbm_force_history": (C.c_int, [vp, vp, vp, C.c_int, P(C.c_int)]),
+        "mrlbm_drag_lift": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
+                                      P(C.c_double), P(C.c_double)]),
+        "mrlbm_strouhal": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                     P(C.c_double), P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -669,4 +669,81 @@ int mrlbm_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_co
     return MRLBM_OK;
 }
 
+// ---- config-5 integral diagnostics ----
+int mrlbm_drag_lift(double fx, double fy, double rho0, double u0, double L, double* cd, double* cl)
+{
+    const double den = rho0 * u0 * u0 * L;
+    if (!(den > 0.0) || !cd || !cl)
+        return MRLBM_ERR_CONFIG;
+    *cd = 2.0 * fx / den;
+    *cl = 2.0 * fy / den;
+    return MRLBM_OK;
+}
+
+int mrlbm_strouhal(const double* cl, int64_t n, int64_t skip, double dt, double u0, double L, double* st, double* df)
+{
+    if (!cl || !st || skip < 0 || !(dt > 0.0) || !(u0 != 0.0))
+        return MRLBM_ERR_CONFIG;
+    const int64_t N = n - skip;
+    if (N < 8)
+        return MRLBM_ERR_CONFIG;
+    const double* y = cl + skip;
+    // least-squares line a + b t (t = sample index), removed
+    double st_ = 0.0, sy = 0.0, stt = 0.0, sty = 0.0;
+    for (int64_t i = 0; i < N; ++i)
+    {
+        const double t = static_cast<double>(i);
+        st_ += t;
+        sy += y[i];
+        stt += t * t;
+        sty += t * y[i];
+    }
+    const double Nd = static_cast<double>(N);
+    const double b = (Nd * sty - st_ * sy) / (Nd * stt - st_ * st_);
+    const double a = (sy - b * st_) / Nd;
+    std::vector<double> w(N);
+    double amp = 0.0;
+    for (int64_t i = 0; i < N; ++i)
+    {
+        const double r = y[i] - (a + b * static_cast<double>(i));
+        const double hann = 0.5 - 0.5 * std::cos(2.0 * M_PI * static_cast<double>(i) / static_cast<double>(N - 1));
+        w[i] = r * hann;
+        amp = std::max(amp, std::fabs(r));
+    }
+    const double scale = std::max(std::fabs(a), std::fabs(b) * Nd);
+    if (!(amp > 1e-12 * scale) || amp == 0.0)
+        return MRLBM_ERR_NUMERIC; // flat after detrending: no shedding
+    // direct DFT power over bins 1 .. N/2
+    const int64_t K = N / 2;
+    std::vector<double> p(K + 1, 0.0);
+    for (int64_t k = 1; k <= K; ++k)
+    {
+        double re = 0.0, im = 0.0;
+        const double wk = 2.0 * M_PI * static_cast<double>(k) / Nd;
+        for (int64_t i = 0; i < N; ++i)
+        {
+            const double ph = wk * static_cast<double>(i);
+            re += w[i] * std::cos(ph);
+            im -= w[i] * std::sin(ph);
+        }
+        p[k] = re * re + im * im;
+    }
+    int64_t kmax = 1;
+    for (int64_t k = 2; k <= K; ++k)
+        if (p[k] > p[kmax])
+            kmax = k;
+    double rest = 0.0;
+    for (int64_t k = 1; k <= K; ++k)
+        if (k != kmax)
+            rest += p[k];
+    rest /= static_cast<double>(std::max<int64_t>(K - 1, 1));
+    if (!(p[kmax] > 4.0 * rest))
+        return MRLBM_ERR_NUMERIC; // no dominant peak
+    const double freq = static_cast<double>(kmax) / (Nd * dt);
+    *st = L * freq / u0;
+    if (df)
+        *df = 1.0 / (Nd * dt);
+    return MRLBM_OK;
+}
+
 } // extern "C"

@@ -103,6 +103,11 @@ struct Aux {
     const int2* eta;    // [h] logical velocities (x, y)
     const unsigned short* pmask; // [(g * q + h) * 2 + side] parents as bits of the 3^d box ((ox+1)*3+(oy+1))
     const unsigned short* umask; // [g] union over the pairs
+    // obstacle force tracking (null when off): per level, a dense box over the disc's
+    // bounding box holding each leaf's (Fx, Fy) term of the current step
+    double* frc;
+    long long frc_off[kL];
+    int frc_x0[kL], frc_y0[kL], frc_nx[kL], frc_ny[kL];
 };
 
 // ---------------------------------------------------------------- helpers
@@ -533,6 +538,81 @@ __global__ void k_grade(Geo g, Flags fl, int m)
         for (int a = 0; a < (ax1 != ax0 ? 2 : 1); ++a)
             for (int b = 0; b < (ay1 != ay0 ? 2 : 1); ++b)
                 fl.rn[li - 1][xy2lin<D>(a ? ax1 : ax0, b ? ay1 : ay0, nyp)] = 1;
+    }
+}
+
+// same, 16 cells of a row per thread (one 16-byte load; empty chunks cost one load)
+__global__ void k_grade_v(Geo g, Flags fl, int m)
+{
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li], nyp = g.ny[li - 1];
+    const long long nch = (long long)nx * ny / 16;
+    const uint8_t* rn = fl.rn[li];
+    uint8_t* rnp = fl.rn[li - 1];
+    GRID_STRIDE(c, 0, nch)
+    {
+        const uint4 v = reinterpret_cast<const uint4*>(rn)[c];
+        if ((v.x | v.y | v.z | v.w) == 0)
+            continue;
+        const int lin0 = (int)(c * 16);
+        const int px = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
+        // distinct parent rows of px-1..px+1 (clipped / wrapped)
+        int prow[3], npr = 0;
+        for (int o = -1; o <= 1; ++o)
+        {
+            int xv = px + o;
+            if (xv < 0 || xv >= nx)
+            {
+                if (!g.per0)
+                    continue;
+                xv = mr_coord(xv, nx, 1);
+            }
+            const int r = xv >> 1;
+            bool dup = false;
+            for (int k = 0; k < npr; ++k)
+                dup = dup || prow[k] == r;
+            if (!dup)
+                prow[npr++] = r;
+        }
+        // parent columns touched by the set cells' y-1..y+1: a bit mask over
+        // (y0 - 1) >> 1 .. (y0 + 16) >> 1 plus wrapped ends
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+        unsigned cols = 0; // bit j: parent column (y0 >> 1) - 1 + j, j in [0, 10)
+        bool wrapLo = false, wrapHi = false;
+        for (int j = 0; j < 16; ++j)
+        {
+            if (!b[j])
+                continue;
+            const int y = y0 + j;
+            for (int o = -1; o <= 1; ++o)
+            {
+                const int yv = y + o;
+                if (yv < 0)
+                {
+                    if (g.per1)
+                        wrapLo = true;
+                    continue;
+                }
+                if (yv >= ny)
+                {
+                    if (g.per1)
+                        wrapHi = true;
+                    continue;
+                }
+                cols |= 1u << ((yv >> 1) - (y0 >> 1) + 1);
+            }
+        }
+        for (int k = 0; k < npr; ++k)
+        {
+            uint8_t* row = rnp + (long long)prow[k] * nyp;
+            for (int j = 0; j < 10; ++j)
+                if ((cols >> j) & 1u)
+                    row[(y0 >> 1) - 1 + j] = 1;
+            if (wrapLo)
+                row[mr_coord(-1, ny, 1) >> 1] = 1;
+            if (wrapHi)
+                row[mr_coord(ny, ny, 1) >> 1] = 1;
+        }
     }
 }
 
@@ -1358,17 +1438,25 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
             wsum[k][wid] = v;
     }
     __syncthreads();
-    const int catbase[3] = {0, cnt[0], cnt[0] + cnt[1]};
-    int pos[3];
+    // the tile's slots are staged in shared memory (category-segmented, lexicographic
+    // within each category) and then written out with coalesced stores
+    __shared__ int sCells[kTile];
+    __shared__ uint8_t sKind[kTile];
+    int tot[3], pos[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
     {
-        int wpre = 0;
-        for (int w = 0; w < wid; ++w)
-            wpre += wsum[k][w];
-        pos[k] = catbase[k] + tile_offsets[(long long)lvb_ * 3 + k] + wpre + pre[k];
+        int wpre = 0, t = 0;
+        for (int w = 0; w < NW; ++w)
+        {
+            wpre += w < wid ? wsum[k][w] : 0;
+            t += wsum[k][w];
+        }
+        tot[k] = t;
+        pos[k] = wpre + pre[k];
     }
-    uint8_t* skind = tn.skind[li];
+    pos[1] += tot[0];
+    pos[2] += tot[0] + tot[1];
 #pragma unroll
     for (int j = 0; j < 16; ++j)
     {
@@ -1377,9 +1465,24 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
         if (i < n && ct < 3)
         {
             const int sl = pos[ct]++;
-            cells[sl] = (int)i;
-            skind[sl] = b[j];
+            sCells[sl] = (int)i;
+            sKind[sl] = b[j];
         }
+    }
+    __syncthreads();
+    const int catbase[3] = {0, cnt[0], cnt[0] + cnt[1]};
+    uint8_t* skind = tn.skind[li];
+    int lo = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        const long long gb = (long long)catbase[k] + tile_offsets[(long long)lvb_ * 3 + k] - lo;
+        for (int t = lo + threadIdx.x; t < lo + tot[k]; t += kTileThreads)
+        {
+            cells[gb + t] = sCells[t];
+            skind[gb + t] = sKind[t];
+        }
+        lo += tot[k];
     }
 }
 
@@ -1857,6 +1960,60 @@ __device__ __forceinline__ double obstacle_alpha(const SchemeDev* scg, int m, in
     return cnt > 0 ? __ddiv_rn((double)cnt, (double)(ns * ns)) : 0.0;
 }
 
+// obstacle force term of one leaf (oracle force_terms): the momentum the blend removes
+// per unit time, alpha * q * |cell| / dt, q = post-collision momentum moments mo[1..2]
+__device__ __forceinline__ void force_store(const Aux& aux, const Geo& g, const SchemeDev* scg, int m, int x, int y,
+                                         double alpha, double mx, double my)
+{
+    const int li = m - g.J0;
+    const int bx = x - aux.frc_x0[li], by = y - aux.frc_y0[li];
+    if (bx < 0 || by < 0 || bx >= aux.frc_nx[li] || by >= aux.frc_ny[li])
+    {
+        flag_err(aux.err, 2);
+        return;
+    }
+    const double area = ldexp(1.0, -2 * m);
+    const double dt = __ddiv_rn(ldexp(1.0, -g.J1), scg->lambda);
+    double* o = aux.frc + aux.frc_off[li] + 2LL * ((long long)bx * aux.frc_ny[li] + by);
+    o[0] = __ddiv_rn(__dmul_rn(__dmul_rn(alpha, mx), area), dt);
+    o[1] = __ddiv_rn(__dmul_rn(__dmul_rn(alpha, my), area), dt);
+}
+
+// deterministic sum of the force boxes (level by level, fixed strided partition and
+// tree): appends (Fx, Fy) of this step to the history; one block of 1024 threads
+__global__ void __launch_bounds__(1024) k_force_sum(const double* frc, long long n, double* hist, int* hn, int cap)
+{
+    __shared__ double s0[1024], s1[1024];
+    double a0 = 0.0, a1 = 0.0;
+    for (long long i = threadIdx.x; i < n; i += 1024)
+    {
+        a0 = __dadd_rn(a0, frc[2 * i]);
+        a1 = __dadd_rn(a1, frc[2 * i + 1]);
+    }
+    s0[threadIdx.x] = a0;
+    s1[threadIdx.x] = a1;
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1)
+    {
+        if ((int)threadIdx.x < w)
+        {
+            s0[threadIdx.x] = __dadd_rn(s0[threadIdx.x], s0[threadIdx.x + w]);
+            s1[threadIdx.x] = __dadd_rn(s1[threadIdx.x], s1[threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+    {
+        const int k = *hn;
+        if (k < cap)
+        {
+            hist[2 * k] = s0[0];
+            hist[2 * k + 1] = s1[0];
+        }
+        *hn = k + 1;
+    }
+}
+
 // generated unrolled table sums (stream_gen.cuh) for the built-in velocity sets
 // GC: gap class compiled in (0: gap 0 only, 1: gaps >= 1 only, -1: any)
 template <int EQ, int Q, int GC>
@@ -1999,7 +2156,7 @@ __device__ __forceinline__ double gen_collide_row(const CC& cc, bool inverse, in
 //      f*_i = row i of M^-1 m' (+ blend), written to F0.
 // Every value uses the same operations in the same order as K7, so the result is
 // identical; the leaves' loads are spread over Q warps instead of one thread.
-template <int D, int Q, int BS, int EQ, bool GEN>
+template <int D, int Q, int BS, int EQ, bool GEN, bool FRC = false>
 __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
                                                 const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
                                                 const __grid_constant__ Flags fl, const SchemeDev* scg,
@@ -2245,6 +2402,9 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                     int x, y;
                     lin2xy_l<D>(sLin[k], ny, g.lny[li], x, y);
                     alpha = obstacle_alpha(scg, m, x, y);
+                    if constexpr (FRC)
+                        if (alpha > 0.0)
+                            force_store(aux, g, scg, m, x, y, alpha, sMo[1][k], sMo[2][k]);
                 }
             }
             sAlpha[k] = alpha;
@@ -2293,7 +2453,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
 // populations from K8 (already in F0).  BS = block size of the block-diagonal M.
 // MODE 0 streams the table-path leaves only (no calls, no stack: the hot kernel);
 // MODE 1 the fallback leaves at gap 0 (boundary rim) and gap >= 2 (values from K8).
-template <int D, int Q, int BS, int EQ, bool GEN, int MODE, int GC>
+template <int D, int Q, int BS, int EQ, bool GEN, int MODE, int GC, bool FRC = false>
 __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     k_stream_collide(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld F0,
                      const __grid_constant__ Fld F1, const __grid_constant__ Flags fl, const SchemeDev* scg,
@@ -2545,6 +2705,8 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
                 const double alpha = obstacle_alpha(scg, m, x, y);
                 if (alpha > 0.0)
                 {
+                    if constexpr (FRC)
+                        force_store(aux, g, scg, m, x, y, alpha, mo[1], mo[2]);
 #pragma unroll
                     for (int h = 0; h < Q; ++h)
                         f[h] = __dadd_rn(__dmul_rn(alpha, sFeq[h]), __dmul_rn(__dsub_rn(1.0, alpha), f[h]));
@@ -2836,6 +2998,14 @@ struct mrlbm_ctx {
     int32_t* ld_lin[kL]{};
     long long ld_n[kL]{};
     int* ld_bad = nullptr;
+    // obstacle force tracking (mrlbm_set_force_tracking)
+    double* frc = nullptr;
+    long long frc_n = 0; // cells over all level boxes
+    long long frc_off[kL]{};
+    int frc_x0[kL]{}, frc_y0[kL]{}, frc_nx[kL]{}, frc_ny[kL]{};
+    double* fhist = nullptr;
+    int* fhn = nullptr;
+    int fcap = 0;
     cudaEvent_t ev[16]{};
     double phase_ms[MRLBM_PHASE_COUNT]{};
     std::string err_msg;
@@ -2926,6 +3096,15 @@ Aux aux_of(mrlbm_ctx* c)
     a.eta = c->etad;
     a.pmask = c->pmaskd;
     a.umask = c->umaskd;
+    a.frc = c->frc;
+    for (int i = 0; i < kL; ++i)
+    {
+        a.frc_off[i] = 2 * c->frc_off[i];
+        a.frc_x0[i] = c->frc_x0[i];
+        a.frc_y0[i] = c->frc_y0[i];
+        a.frc_nx[i] = c->frc_nx[i];
+        a.frc_ny[i] = c->frc_ny[i];
+    }
     return a;
 }
 
@@ -3018,6 +3197,8 @@ void enqueue_step(mrlbm_ctx* c)
     c->kcount = 0;
     c->kn = 0;
     int nb = 0;
+    if (c->frc)
+        cudaMemsetAsync(c->frc, 0, sizeof(double) * 2 * c->frc_n, s);
     {
         LGrid lz = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 16 + 1, T); }, &nb);
         c->kcount++;
@@ -3046,15 +3227,18 @@ void enqueue_step(mrlbm_ctx* c)
         k_enlarge<D><<<nb, T, 0, s>>>(g, to, fl, c->sch, lg, c->emask);
         kmark(c, "k_enlarge", -1);
     }
+    auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
     for (int m = c->J1 - 1; m > c->J0; --m)
     {
         c->kcount++;
-        k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
+        if (vec_ok(m))
+            k_grade_v<<<grid_for(c, g.cap[m - c->J0] / 16, T), T, 0, s>>>(g, fl, m);
+        else
+            k_grade<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, fl, m);
         kmark(c, "k_grade", m);
     }
     phase_mark(c, 3);
     // K4 kinds, fallback flags, reconstruction bands, ghosts, compaction
-    auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
     // levels [J0, mv) use the scalar dense kernels, [mv, J1] the 16-cell vector ones
     int mv = c->J1 + 1;
     for (int m = c->J1; m >= c->J0 && vec_ok(m); --m)
@@ -3132,10 +3316,17 @@ void enqueue_step(mrlbm_ctx* c)
             cc.M[i * BS + j] = c->sc.M[i * Q + col];
             cc.Mi[i * BS + j] = c->sc.Minv[i * Q + col];
         }
+    // force tracking (config 5 diagnostics) runs separately compiled variants, so the
+    // default kernels carry no extra code
+    constexpr bool kObs = EQ == MRLBM_EQ_NS_D2Q9 && D == 2;
+    const bool frc = kObs && c->frc != nullptr;
     if (c->J1 > c->J0)
     {
         c->kcount++;
-        k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+        if (frc)
+            k_fb1<D, Q, BS, EQ, GEN, kObs><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+        else
+            k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
         kmark(c, "k_fb1", -1);
     }
     {
@@ -3146,27 +3337,41 @@ void enqueue_step(mrlbm_ctx* c)
             // the generated path in two register budgets: the finest level (gap 0) alone,
             // then every coarser level (gap classes 1 and >= 2)
             LGrid l0 = make_lgrid(c, c->J1, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
-            k_stream_collide<D, Q, BS, EQ, GEN, 0, 0><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
+            if (frc)
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, 0, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
+            else
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, 0><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
             kmark(c, "k_stream_collide", c->J1);
             if (c->J1 > c->J0)
             {
                 LGrid l1 = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
                 c->kcount++;
-                k_stream_collide<D, Q, BS, EQ, GEN, 0, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
+                if (frc)
+                    k_stream_collide<D, Q, BS, EQ, GEN, 0, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
+                else
+                    k_stream_collide<D, Q, BS, EQ, GEN, 0, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
                 kmark(c, "k_stream_collide", -1);
             }
         }
         else
         {
-            k_stream_collide<D, Q, BS, EQ, GEN, 0, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
+            if (frc)
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
+            else
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
             kmark(c, "k_stream_collide", -1);
         }
         LGrid lf = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 8, 256); }, &nb);
         c->kcount++;
-        k_stream_collide<D, Q, BS, EQ, GEN, 1, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
+        if (frc)
+            k_stream_collide<D, Q, BS, EQ, GEN, 1, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
+        else
+            k_stream_collide<D, Q, BS, EQ, GEN, 1, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
         kmark(c, "k_stream_collide_fb", -1);
     }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
+    if (c->frc)
+        { c->kcount++; k_force_sum<<<1, 1024, 0, s>>>(c->frc, c->frc_n, c->fhist, c->fhn, c->fcap);  kmark(c, "k_force_sum", -1); }
     phase_mark(c, 6);
     c->kernels_per_step = c->kcount;
 }
@@ -3928,6 +4133,103 @@ int mrlbm_profile_text(mrlbm_ctx* ctx, char* buf, int cap, int reset)
     return MRLBM_OK;
 }
 
+static void drop_graphs(mrlbm_ctx* ctx)
+{
+    for (auto& gph : ctx->graph)
+        if (gph)
+        {
+            cudaGraphExecDestroy(gph);
+            gph = nullptr;
+        }
+}
+
+static void free_force(mrlbm_ctx* ctx)
+{
+    cudaFree(ctx->frc);
+    cudaFree(ctx->fhist);
+    cudaFree(ctx->fhn);
+    ctx->frc = nullptr;
+    ctx->fhist = nullptr;
+    ctx->fhn = nullptr;
+    ctx->frc_n = 0;
+    ctx->fcap = 0;
+}
+
+int mrlbm_set_force_tracking(mrlbm_ctx* ctx, int capacity_steps)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    if (capacity_steps < 0)
+        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking: negative capacity");
+    if (capacity_steps > 0 && !(ctx->rc.obstacle == 1 && ctx->D == 2 && ctx->sc.equilibrium == MRLBM_EQ_NS_D2Q9))
+        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking needs the D2Q9 obstacle configuration (obstacle = 1)");
+    CU(cudaStreamSynchronize(ctx->stream));
+    drop_graphs(ctx);
+    free_force(ctx);
+    if (capacity_steps == 0)
+        return MRLBM_OK;
+    // per level, the cells whose box can meet the disc's bounding box (obstacle_alpha's
+    // rejection test) plus one cell of margin, clipped to the level box
+    long long tot = 0;
+    for (int li = 0; li < ctx->nlev; ++li)
+    {
+        const int m = ctx->J0 + li;
+        const double dx = std::ldexp(1.0, -m);
+        int lo[2], n[2];
+        const int ext[2] = {ctx->geo.nx[li], ctx->geo.ny[li]};
+        for (int a = 0; a < 2; ++a)
+        {
+            const double c0 = ctx->rc.obstacle_center[a] - ctx->rc.obstacle_radius - ctx->rc.origin[a];
+            const double c1 = ctx->rc.obstacle_center[a] + ctx->rc.obstacle_radius - ctx->rc.origin[a];
+            int a0 = static_cast<int>(std::floor(c0 / dx)) - 2, a1 = static_cast<int>(std::floor(c1 / dx)) + 2;
+            a0 = std::max(a0, 0);
+            a1 = std::min(a1, ext[a] - 1);
+            lo[a] = a0;
+            n[a] = std::max(0, a1 - a0 + 1);
+        }
+        ctx->frc_x0[li] = lo[0];
+        ctx->frc_y0[li] = lo[1];
+        ctx->frc_nx[li] = n[0];
+        ctx->frc_ny[li] = n[1];
+        ctx->frc_off[li] = tot;
+        tot += static_cast<long long>(n[0]) * n[1];
+    }
+    ctx->frc_n = tot;
+    CU(cudaMalloc(&ctx->frc, sizeof(double) * 2 * std::max(tot, 1LL)));
+    CU(cudaMalloc(&ctx->fhist, sizeof(double) * 2 * capacity_steps));
+    CU(cudaMalloc(&ctx->fhn, sizeof(int)));
+    CU(cudaMemsetAsync(ctx->fhn, 0, sizeof(int), ctx->stream));
+    ctx->fcap = capacity_steps;
+    return MRLBM_OK;
+}
+
+int mrlbm_force_history(mrlbm_ctx* ctx, double* fx, double* fy, int cap, int* n)
+{
+    if (!ctx || !n)
+        return MRLBM_ERR_CONFIG;
+    if (!ctx->frc)
+        return set_err(ctx, MRLBM_ERR_STATE, "force history: tracking is off");
+    int k = 0;
+    CU(cudaMemcpyAsync(&k, ctx->fhn, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const int kk = std::min(std::min(k, ctx->fcap), cap);
+    std::vector<double> h(2 * static_cast<size_t>(std::max(kk, 0)));
+    if (kk > 0)
+    {
+        CU(cudaMemcpyAsync(h.data(), ctx->fhist, sizeof(double) * 2 * kk, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    for (int i = 0; i < kk; ++i)
+    {
+        fx[i] = h[2 * i];
+        fy[i] = h[2 * i + 1];
+    }
+    *n = k;
+    if (k > ctx->fcap)
+        return set_err(ctx, MRLBM_ERR_CAPACITY, "force history: more steps than the tracking capacity");
+    return MRLBM_OK;
+}
+
 int mrlbm_set_graph(mrlbm_ctx* ctx, int on)
 {
     if (!ctx)
@@ -3963,6 +4265,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     for (auto& gph : ctx->graph)
         if (gph)
             cudaGraphExecDestroy(gph);
+    free_force(ctx);
     for (int v = 0; v < 2; ++v)
     {
         cudaFree(ctx->cnt[v]);

@@ -26,6 +26,30 @@ def _raise(status, msg):
     raise MRLBMError(f"status {status}: {msg}")
 
 
+def drag_lift(fx, fy, rho0, u0, L):
+    """C_D, C_L = 2 F / (rho0 u0^2 L), through the C-ABI."""
+    lib = _lib.lib()
+    cd, cl = C.c_double(0.0), C.c_double(0.0)
+    st = lib.mrlbm_drag_lift(float(fx), float(fy), float(rho0), float(u0), float(L), C.byref(cd), C.byref(cl))
+    if st != 0:
+        _raise(st, "drag_lift: rho0 u0^2 L must be positive")
+    return cd.value, cl.value
+
+
+def strouhal(cl, dt, u0, L, skip=0):
+    """St = L f / u0 of the dominant shedding frequency of a lift series (PAPER.md:1380-1383;
+    SPEC.md:477-485).  Returns (St, frequency resolution).  Raises FloatingPointError
+    ("no dominant peak") for a flat spectrum."""
+    lib = _lib.lib()
+    y = np.ascontiguousarray(cl, dtype=np.float64)
+    st, df = C.c_double(0.0), C.c_double(0.0)
+    code = lib.mrlbm_strouhal(y.ctypes.data_as(C.c_void_p), y.size, int(skip), float(dt), float(u0), float(L),
+                              C.byref(st), C.byref(df))
+    if code != 0:
+        _raise(code, "strouhal: no dominant peak" if code == ERR_NUMERIC else "strouhal: need >= 8 samples, dt > 0")
+    return st.value, df.value
+
+
 class Solver:
     def __init__(self, scheme, cfg):
         self.L = _lib.lib()
@@ -104,6 +128,22 @@ class Solver:
         self._check(self.L.mrlbm_additional_error(self.h, reference.h, row.ctypes.data_as(C.c_void_p), C.byref(e),
                                                   sums.ctypes.data_as(C.c_void_p)))
         return e.value, float(sums[0]), float(sums[1])
+
+    def set_force_tracking(self, capacity_steps):
+        """Record the obstacle force (Fx, Fy) of each following step on the device
+        (config 5).  0 turns it off."""
+        self._check(self.L.mrlbm_set_force_tracking(self.h, int(capacity_steps)))
+
+    def force_history(self):
+        """(fx, fy) arrays of the per-step obstacle forces recorded since tracking began."""
+        n = C.c_int(0)
+        self._check(self.L.mrlbm_force_history(self.h, None, None, 0, C.byref(n)))
+        fx = np.zeros(n.value, dtype=np.float64)
+        fy = np.zeros(n.value, dtype=np.float64)
+        if n.value:
+            self._check(self.L.mrlbm_force_history(self.h, fx.ctypes.data_as(C.c_void_p),
+                                                   fy.ctypes.data_as(C.c_void_p), n.value, C.byref(n)))
+        return fx, fy
 
     def set_profiling(self, on=True):
         self._check(self.L.mrlbm_set_profiling(self.h, int(bool(on))))
