@@ -330,6 +330,93 @@ def gen_collide(out):
         out.append("")
 
 
+def gen_fb1t(name, d, q, etas, out):
+    """Gap-1 fallback leaves, one thread per leaf (k_fb1t): every population's
+    table sums + details of the rim cells that are finest leaves (Decision D.13b),
+    the same operands and order as gen_fb1h.  For leaves without domain-leaving
+    pairs (dmask == 0): box values are loaded at clamped / wrapped coordinates (the
+    pairs that use them are inside the domain), rim cells are tested for finest
+    leaves on the fly."""
+    tabs = {(h, side): table_offsets(d, 1, eta, side) for h, eta in enumerate(etas) for side in (0, 1)}
+    box = [o for o in itertools.product(range(-2, 3), repeat=d)]
+    bidx = (lambda o: o[0] + 2) if d == 1 else (lambda o: (o[0] + 2) * 5 + (o[1] + 2))
+    out.append(f"__device__ __forceinline__ void gen_fb1t_{name}(const double* __restrict__ Fin, long long cap, "
+               f"const double* __restrict__ Fj, long long capj, const uint8_t* __restrict__ kindj, "
+               f"int x, int y, int nx, int ny, int nxj, int nyj, int per0, int per1, unsigned mask, "
+               f"long long s, const double* sW, double scale, double (&f)[{q}])")
+    out.append("{")
+    out.append("    (void)y; (void)ny; (void)nyj; (void)per1; (void)capj; (void)Fj; (void)kindj; (void)nxj;")
+    used_all = set()
+    for h, eta in enumerate(etas):
+        for side in (0, 1):
+            for o in tabs[(h, side)]:
+                used_all.add(bidx(o))
+            for c in rim_cells_g1(d, eta, side):
+                p = tuple((ci + 1) // 2 - 1 for ci in c)
+                for st in itertools.product((-1, 0, 1), repeat=d):
+                    used_all.add(bidx(tuple(pi + si for pi, si in zip(p, st))))
+    for o in box:
+        b = bidx(o)
+        if b not in used_all:
+            continue
+        xs = f"x + ({o[0]})" if o[0] else "x"
+        if d == 1:
+            out.append(f"    const int b{b} = gen_clampw({xs}, nx, per0);")
+        else:
+            ys = f"y + ({o[1]})" if o[1] else "y"
+            out.append(f"    const int b{b} = gen_clampw({xs}, nx, per0) * ny + gen_clampw({ys}, ny, per1);")
+    widx = 0
+    for h, eta in enumerate(etas):
+        out.append("    {")
+        out.append(f"        const double* Fh = Fin + {h}LL * cap;")
+        out.append(f"        const double* Fjh = Fj + {h}LL * capj;")
+        out.append("        (void)Fjh;")
+        out.append("        const double fs = Fh[s];")
+        needed = sorted({bidx(o) for side in (0, 1) for o in tabs[(h, side)]})
+        for b in needed:
+            out.append(f"        const double v{b} = Fh[b{b}];")
+        for side in (0, 1):
+            nm = "sE" if side == 0 else "sA"
+            pair = 2 * h + side
+            out.append(f"        double {nm} = 0.0;")
+            for o in tabs[(h, side)]:
+                out.append(f"        {nm} = __dadd_rn({nm}, __dmul_rn(sW[{widx}], v{bidx(o)}));")
+                widx += 1
+            rims = rim_cells_g1(d, eta, side)
+            if rims:
+                out.append(f"        if ((mask >> {pair}) & 1u)")
+                out.append("        {")
+                extra = set()
+                for c in rims:
+                    p = tuple((ci + 1) // 2 - 1 for ci in c)
+                    for st in itertools.product((-1, 0, 1), repeat=d):
+                        extra.add(bidx(tuple(pi + si for pi, si in zip(p, st))))
+                for b in sorted(extra - set(needed)):
+                    out.append(f"            const double v{b} = Fh[b{b}];")
+                for c in rims:
+                    p = tuple((ci + 1) // 2 - 1 for ci in c)
+                    par = tuple((ci + 1) & 1 for ci in c)
+                    xs = f"2 * x + ({c[0] - 1})"
+                    if d == 1:
+                        out.append(f"            {{ const int jl = gen_wrap({xs}, nxj, per0);")
+                    else:
+                        ys = f"2 * y + ({c[1] - 1})"
+                        out.append(f"            {{ const int jl = gen_wrap({xs}, nxj, per0) * nyj + gen_wrap({ys}, nyj, per1);")
+                    out.append("              if (kindj[jl] & 1)")
+                    out.append("              {")
+                    sv = [f"v{bidx(tuple(pi + si for pi, si in zip(p, st)))}" for st in itertools.product((-1, 0, 1), repeat=d)]
+                    out.append(f"                const double sv[{len(sv)}] = {{{', '.join(sv)}}};")
+                    dy = par[1] if d == 2 else 0
+                    out.append(f"                {nm} = __dadd_rn({nm}, __dsub_rn(Fjh[jl], mr_predict<{d}>(sv, {par[0]}, {dy})));")
+                    out.append("              }")
+                    out.append("            }")
+                out.append("        }")
+        out.append(f"        f[{h}] = __dadd_rn(fs, __dmul_rn(scale, __dsub_rn(sE, sA)));")
+        out.append("    }")
+    out.append("}")
+    out.append("")
+
+
 def main():
     out = ["// GENERATED by gen_stream.py -- do not edit.",
            "// Unrolled flattened-table stream sums for the built-in velocity sets (K7 fast path).",
@@ -339,12 +426,20 @@ def main():
            "{",
            "    return per ? (c < 0 ? c + n : (c >= n ? c - n : c)) : c;",
            "}",
+           "",
+           "// MR boundary rule (Decision D.8): wrap periodic axes, clamp the others",
+           "__device__ __forceinline__ int gen_clampw(int c, int n, int per)",
+           "{",
+           "    return per ? (c < 0 ? c + n : (c >= n ? c - n : c)) : (c < 0 ? 0 : (c >= n ? n - 1 : c));",
+           "}",
            ""]
     for name, (d, q, etas) in SETS.items():
         for gc in (0, 1, 2):
             gen_class(name, d, q, etas, gc, out)
     for name, (d, q, etas) in SETS.items():
         gen_fb1h(name, d, q, etas, out)
+    for name, (d, q, etas) in SETS.items():
+        gen_fb1t(name, d, q, etas, out)
     gen_collide(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "stream_gen.cuh")
     open(path, "w").write("\n".join(out) + "\n")

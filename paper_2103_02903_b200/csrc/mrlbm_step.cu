@@ -105,6 +105,7 @@ struct Aux {
     const unsigned short* umask; // [g] union over the pairs
     // obstacle force tracking (null when off): per level, a dense box over the disc's
     // bounding box holding each leaf's (Fx, Fy) term of the current step
+    int fb1t;           // gap-1 fallback leaves with dmask == 0 run in k_stream_collide MODE 2
     double* frc;
     long long frc_off[kL];
     int frc_x0[kL], frc_y0[kL], frc_nx[kL], frc_ny[kL];
@@ -2113,6 +2114,27 @@ __device__ __forceinline__ void gen_fb1h(int h, const double* Fin, long long cap
         gen_fb1h_EQ5(h, Fin, cap, Fj, capj, box, rim, bstride, mask, dmask, sW, sE, sA);
 }
 
+// gap-1 fallback leaf, thread per leaf (stream_gen.cuh gen_fb1t_*)
+template <int EQ, int Q>
+__device__ __forceinline__ void gen_fb1t(const double* Fin, long long cap, const double* Fj, long long capj,
+                                         const uint8_t* kindj, int x, int y, int nx, int ny, int nxj, int nyj,
+                                         int per0, int per1, unsigned mask, long long s, const double* sW, double scale,
+                                         double (&f)[Q])
+{
+#define GEN_FB1T(N) gen_fb1t_EQ##N(Fin, cap, Fj, capj, kindj, x, y, nx, ny, nxj, nyj, per0, per1, mask, s, sW, scale, f);
+    if constexpr (EQ == 1 && Q == 2)
+        GEN_FB1T(1)
+    else if constexpr (EQ == 2 && Q == 9)
+        GEN_FB1T(2)
+    else if constexpr (EQ == 3 && Q == 4)
+        GEN_FB1T(3)
+    else if constexpr (EQ == 4 && Q == 16)
+        GEN_FB1T(4)
+    else if constexpr (EQ == 5 && Q == 9)
+        GEN_FB1T(5)
+#undef GEN_FB1T
+}
+
 // row i of the generated pattern-unrolled M f / M^-1 m
 template <int EQ, int Q, class CC>
 __device__ __forceinline__ double gen_collide_row(const CC& cc, bool inverse, int i, const double (&x)[Q])
@@ -2220,6 +2242,10 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
             {
                 lin = tn.cells[li][sl];
                 isfb = (tn.skind[li][sl] & K_FB) != 0;
+                // generated path: fallback leaves without domain-leaving pairs run one
+                // thread per leaf in k_stream_collide MODE 2; only the boundary rim here
+                if (GEN && isfb && aux.fb1t)
+                    isfb = fl.fbd[li][lin] != 0;
             }
             const unsigned bal = __ballot_sync(0xffffffffu, isfb);
             if (lane == 0)
@@ -2535,13 +2561,25 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
             lin_next = tn.cells[li][s + sstep];
             kd_next = tn.skind[li][s + sstep];
         }
-        if (((kd & K_FB) != 0) != (MODE == 1))
+        if (((kd & K_FB) != 0) != (MODE >= 1))
             continue;
         constexpr bool fb = MODE == 1;
         if (fb && gap == 1)
-            continue; // streamed and collided by k_fb1
+            continue; // streamed and collided by k_fb1 / MODE 2
         double f[Q];
-        if (fb && gap >= kDeepGap)
+        if constexpr (MODE == 2)
+        {
+            // gap-1 fallback leaf without domain-leaving pairs, one thread per leaf:
+            // table + details of the finest-leaf rim cells (Decision D.13b), the same
+            // operands and order as k_fb1
+            if (fl.fbd[li][lin] != 0)
+                continue; // boundary rim: k_fb1
+            int x, y;
+            lin2xy_l<D>(lin, ny, g.lny[li], x, y);
+            gen_fb1t<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], tn.kind[li + 1], x, y, nx, ny, g.nx[li + 1],
+                            g.ny[li + 1], per0, per1, fl.fbm[li][lin], lin, sW, scale, f);
+        }
+        else if (fb && gap >= kDeepGap)
         {
             // deep-gap fallback leaf: post-stream populations from K8
 #pragma unroll
@@ -2989,6 +3027,7 @@ struct mrlbm_ctx {
     bool profiling = false;
     bool use_graph = true;
     bool use_gen = false; // generated stream / collision path (built-in velocity sets)
+    bool use_fb1t = true; // gap-1 fallback leaves thread per leaf (MODE 2); MRLBM_NO_FB1T=1 turns it off
     bool gen_ok = false;  // the generated code's constants match this scheme
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
@@ -3097,6 +3136,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.pmask = c->pmaskd;
     a.umask = c->umaskd;
     a.frc = c->frc;
+    a.fb1t = c->use_fb1t ? 1 : 0;
     for (int i = 0; i < kL; ++i)
     {
         a.frc_off[i] = 2 * c->frc_off[i];
@@ -3328,6 +3368,17 @@ void enqueue_step(mrlbm_ctx* c)
         else
             k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
         kmark(c, "k_fb1", -1);
+        if constexpr (GEN)
+        if (c->use_fb1t)
+        {
+            LGrid l2 = make_lgrid(c, c->J1 - 1, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
+            c->kcount++;
+            if (frc)
+                k_stream_collide<D, Q, BS, EQ, GEN, 2, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
+            else
+                k_stream_collide<D, Q, BS, EQ, GEN, 2, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
+            kmark(c, "k_fb1t", -1);
+        }
     }
     {
         LGrid lg = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
@@ -3743,6 +3794,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         return st;
     }
     ctx->use_gen = builtin_velocities(sc) && ctx->gen_ok && std::getenv("MRLBM_NO_GEN") == nullptr;
+    ctx->use_fb1t = std::getenv("MRLBM_NO_FB1T") == nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
         const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;
