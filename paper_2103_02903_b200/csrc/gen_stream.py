@@ -137,7 +137,7 @@ def gen_class(name, d, q, etas, gclass, out):
             out.append(f"    const int sl{i} = gen_wrap({xs}, nx, per0);")
         else:
             ys = f"y + ({oy})" if oy else "y"
-            out.append(f"    const int sl{i} = gen_wrap({xs}, nx, per0) * ny + gen_wrap({ys}, ny, per1);")
+            out.append(f"    const int sl{i} = gen_vix(gen_wrap({xs}, nx, per0), gen_wrap({ys}, ny, per1), ny);")
     widx = 0
     wts = table_weights(d, g, etas) if gclass < 2 else None
     for h in range(q):
@@ -364,7 +364,7 @@ def gen_fb1t(name, d, q, etas, out):
             out.append(f"    const int b{b} = gen_clampw({xs}, nx, per0);")
         else:
             ys = f"y + ({o[1]})" if o[1] else "y"
-            out.append(f"    const int b{b} = gen_clampw({xs}, nx, per0) * ny + gen_clampw({ys}, ny, per1);")
+            out.append(f"    const int b{b} = gen_vix(gen_clampw({xs}, nx, per0), gen_clampw({ys}, ny, per1), ny);")
     widx = 0
     for h, eta in enumerate(etas):
         out.append("    {")
@@ -398,16 +398,17 @@ def gen_fb1t(name, d, q, etas, out):
                     par = tuple((ci + 1) & 1 for ci in c)
                     xs = f"2 * x + ({c[0] - 1})"
                     if d == 1:
-                        out.append(f"            {{ const int jl = gen_wrap({xs}, nxj, per0);")
+                        out.append(f"            {{ const int jl = gen_wrap({xs}, nxj, per0), jv = jl;")
                     else:
                         ys = f"2 * y + ({c[1] - 1})"
-                        out.append(f"            {{ const int jl = gen_wrap({xs}, nxj, per0) * nyj + gen_wrap({ys}, nyj, per1);")
+                        out.append(f"            {{ const int jx = gen_wrap({xs}, nxj, per0), jy = gen_wrap({ys}, nyj, per1);")
+                        out.append("              const int jl = jx * nyj + jy, jv = gen_vix(jx, jy, nyj);")
                     out.append("              if (kindj[jl] & 1)")
                     out.append("              {")
                     sv = [f"v{bidx(tuple(pi + si for pi, si in zip(p, st)))}" for st in itertools.product((-1, 0, 1), repeat=d)]
                     out.append(f"                const double sv[{len(sv)}] = {{{', '.join(sv)}}};")
                     dy = par[1] if d == 2 else 0
-                    out.append(f"                {nm} = __dadd_rn({nm}, __dsub_rn(Fjh[jl], mr_predict<{d}>(sv, {par[0]}, {dy})));")
+                    out.append(f"                {nm} = __dadd_rn({nm}, __dsub_rn(Fjh[jv], mr_predict<{d}>(sv, {par[0]}, {dy})));")
                     out.append("              }")
                     out.append("            }")
                 out.append("        }")
@@ -425,6 +426,12 @@ def main():
            "__device__ __forceinline__ int gen_wrap(int c, int n, int per)",
            "{",
            "    return per ? (c < 0 ? c + n : (c >= n ? c - n : c)) : c;",
+           "}",
+           "",
+           "// value index in 2x2 sibling blocks (2D layout, mrlbm_step.cu vix)",
+           "__device__ __forceinline__ int gen_vix(int x, int y, int ny)",
+           "{",
+           "    return (((x >> 1) * (ny >> 1) + (y >> 1)) << 2) + ((x & 1) << 1) + (y & 1);",
            "}",
            "",
            "// MR boundary rule (Decision D.8): wrap periodic axes, clamp the others",

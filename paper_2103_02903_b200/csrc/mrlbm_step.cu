@@ -164,9 +164,40 @@ __device__ __forceinline__ int xy2lin(int x, int y, int ny)
     return D == 1 ? x : x * ny + y;
 }
 
-// the 2^D children of cell (px, py) in children order (dx, dy) = (c >> 1, c & 1): two
-// 16-byte loads (2D) / one (1D) -- the sibling pairs along the last axis are adjacent
-// and 16-byte aligned (even index, even level sizes)
+// Value layout: the fp64 population arrays are stored in 2x2 sibling
+// blocks -- the 2^D children of a cell, in children order (dx, dy) = (c >> 1, c & 1),
+// are 2^D consecutive doubles (one 32-byte sector per population in 2D), blocks
+// row-major over the parents.  Kinds / flags / slot lists stay row-major (lin).
+template <int D>
+__device__ __forceinline__ int vix(int x, int y, int ny)
+{
+    if (D == 1)
+        return x;
+    return (((x >> 1) * (ny >> 1) + (y >> 1)) << 2) + ((x & 1) << 1) + (y & 1);
+}
+
+// value index of a row-major linear index
+template <int D>
+__device__ __forceinline__ int vl(int lin, int ny, int lny)
+{
+    if (D == 1)
+        return lin;
+    int x, y;
+    if (lny >= 0)
+    {
+        x = lin >> lny;
+        y = lin & (ny - 1);
+    }
+    else
+    {
+        x = lin / ny;
+        y = lin - x * ny;
+    }
+    return vix<D>(x, y, ny);
+}
+
+// the 2^D children of cell (px, py) in children order: one sibling block, read as
+// 16-byte loads from one 32-byte sector (2D) / one 16-byte load (1D)
 template <int D>
 __device__ __forceinline__ void load_children(const double* __restrict__ src, int px, int py, int ny1,
                                               double (&ch)[1 << D])
@@ -179,8 +210,9 @@ __device__ __forceinline__ void load_children(const double* __restrict__ src, in
     }
     else
     {
-        const double2 a = *reinterpret_cast<const double2*>(src + (long long)(2 * px) * ny1 + 2 * py);
-        const double2 b = *reinterpret_cast<const double2*>(src + (long long)(2 * px + 1) * ny1 + 2 * py);
+        const double* b0 = src + (((long long)px * (ny1 >> 1) + py) << 2);
+        const double2 a = *reinterpret_cast<const double2*>(b0);
+        const double2 b = *reinterpret_cast<const double2*>(b0 + 2);
         ch[0] = a.x;
         ch[1] = a.y;
         ch[D == 1 ? 1 : 2] = b.x;
@@ -198,6 +230,18 @@ __device__ __forceinline__ int mr_lin(const Geo& g, int m, int x, int y)
         return xx;
     const int yy = mr_coord(y, g.ny[li], g.per1);
     return xx * g.ny[li] + yy;
+}
+
+// same, value index
+template <int D>
+__device__ __forceinline__ int mr_vix(const Geo& g, int m, int x, int y)
+{
+    const int li = m - g.J0;
+    const int xx = mr_coord(x, g.nx[li], g.per0);
+    if (D == 1)
+        return xx;
+    const int yy = mr_coord(y, g.ny[li], g.per1);
+    return vix<D>(xx, yy, g.ny[li]);
 }
 
 // reference predict<D> operation order (prediction.hpp:64-75, 143-159), gamma = 1
@@ -320,9 +364,10 @@ __global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Au
                 acc = __dadd_rn(acc, ch[c]);
             v[h] = __ddiv_rn(acc, (double)(1 << D));
         }
+        const int pv = vix<D>(px, py, ny);
 #pragma unroll
         for (int h = 0; h < Q; ++h)
-            F.f[li][(long long)h * cap + plin] = v[h];
+            F.f[li][(long long)h * cap + pv] = v[h];
     }
 }
 
@@ -368,9 +413,10 @@ __global__ void __launch_bounds__(256) k_project_new(Geo g, Tree to, Tree tn, Fl
                 acc = __dadd_rn(acc, ch[c]);
             v[h] = __ddiv_rn(acc, (double)(1 << D));
         }
+        const int pv = vix<D>(px, py, ny);
 #pragma unroll
         for (int h = 0; h < Q; ++h)
-            F.f[li][(long long)h * cap + plin] = v[h];
+            F.f[li][(long long)h * cap + pv] = v[h];
     }
 }
 
@@ -402,7 +448,7 @@ __global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl,
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
             const int lin = mr_lin<D>(g, m, px + ox, py + oy);
-            st[o] = lin;
+            st[o] = mr_vix<D>(g, m, px + ox, py + oy);
             ok = ok && (t.kind[li][lin] & (K_LEAF | K_INT)); // grading: the stencil is in R
         }
         int cs[1 << D];
@@ -909,8 +955,10 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
         if (!dom)
             dmask |= 1u << pair;
     }
-    fl.fbm[li][i] = mask;
-    fl.fbd[li][i] = dmask;
+    // fallback masks live at the value index (read in value-block slot order)
+    const int vi = vix<D>(x, y, ny);
+    fl.fbm[li][vi] = mask;
+    fl.fbd[li][vi] = dmask;
     fl.kind[li][i] = K_LEAF | K_FB;
     if (gap >= 2)
     {
@@ -1292,6 +1340,61 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter(const uint8_t* ki
     }
 }
 
+// The step's slot lists are in VALUE-BLOCK order (2D): cells are enumerated by their
+// value index vix (sibling blocks, blocks row-major over the parents), so the threads
+// of a warp that take consecutive slots touch whole 32-byte value sectors.  The
+// slots still hold row-major linear indices; mrlbm_read_leaves re-sorts a level into
+// the lexicographic CellIndex order.  (1D: value order == lexicographic order.)
+__device__ __forceinline__ bool blk_order(const Geo& g, int li)
+{
+    return g.d == 2;
+}
+
+// row-major linear index of the cell with value index v (2D)
+__device__ __forceinline__ int blk_lin(const Geo& g, int li, long long v)
+{
+    const int ny = g.ny[li], hy = ny >> 1;
+    const int G = (int)(v >> 2), c = (int)(v & 3);
+    const int gx = G / hy, gy = G - gx * hy;
+    return (2 * gx + (c >> 1)) * ny + 2 * gy + (c & 1);
+}
+
+// the kinds of value indices [base, base + 16) in value order
+__device__ __forceinline__ void load16_blk(const Geo& g, int li, const uint8_t* kind, long long base, long long n,
+                                           uint8_t (&b)[16])
+{
+    if (!blk_order(g, li))
+    {
+        load16(kind, base, n, b);
+        return;
+    }
+    const int ny = g.ny[li], hy = ny >> 1;
+    if ((hy & 3) == 0 && base + 16 <= n)
+    {
+        // four sibling blocks of one block row: rows 2gx and 2gx + 1, 8 columns each
+        const int G = (int)(base >> 2);
+        const int gx = G / hy, gy = G - gx * hy;
+        union {
+            uint2 v;
+            uint8_t c[8];
+        } r0, r1;
+        r0.v = *reinterpret_cast<const uint2*>(kind + (long long)(2 * gx) * ny + 2 * gy);
+        r1.v = *reinterpret_cast<const uint2*>(kind + (long long)(2 * gx + 1) * ny + 2 * gy);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+        {
+            b[4 * k + 0] = r0.c[2 * k];
+            b[4 * k + 1] = r0.c[2 * k + 1];
+            b[4 * k + 2] = r1.c[2 * k];
+            b[4 * k + 3] = r1.c[2 * k + 1];
+        }
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        b[j] = base + j < n ? kind[blk_lin(g, li, base + j)] : 0;
+}
+
 // multi-level compaction: block range per level = that level's tiles (count,
 // scatter) or one block per level (scan)
 __global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(Geo g, Flags fl, TileP tp, LGrid lg_)
@@ -1304,7 +1407,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(Geo g, Flags fl,
     __shared__ int red[3][kTileThreads / 32];
     const long long base = (long long)lvb_ * kTile + (long long)threadIdx.x * 16;
     uint8_t b[16];
-    load16(kind, base, n, b);
+    load16_blk(g, li, kind, base, n, b);
     // the kinds are exclusive bits: count them four bytes at a time
     int c[3] = {0, 0, 0};
     {
@@ -1414,7 +1517,8 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
     }
     const long long base = (long long)lvb_ * kTile + (long long)threadIdx.x * 16;
     uint8_t b[16];
-    load16(kind, base, n, b);
+    load16_blk(g, li, kind, base, n, b);
+    const bool blk = blk_order(g, li);
     int c[3] = {0, 0, 0};
 #pragma unroll
     for (int j = 0; j < 16; ++j)
@@ -1466,7 +1570,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
         if (i < n && ct < 3)
         {
             const int sl = pos[ct]++;
-            sCells[sl] = (int)i;
+            sCells[sl] = blk ? blk_lin(g, li, i) : (int)i;
             sKind[sl] = b[j];
         }
     }
@@ -1519,8 +1623,8 @@ __global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld S
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            st[o] = mr_lin<D>(g, m - 1, px + ox, py + oy);
-            ok = ok && (tn.kind[li - 1][st[o]] & (K_LEAF | K_INT));
+            ok = ok && (tn.kind[li - 1][mr_lin<D>(g, m - 1, px + ox, py + oy)] & (K_LEAF | K_INT));
+            st[o] = mr_vix<D>(g, m - 1, px + ox, py + oy);
         }
         if (!ok)
         {
@@ -1537,9 +1641,10 @@ __global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld S
                 sv[o] = S.f[li - 1][(long long)h * capp + st[o]];
             v[h] = mr_predict<D>(sv, dx, dy);
         }
+        const int vi = vix<D>(x, y, ny);
 #pragma unroll
         for (int h = 0; h < Q; ++h)
-            S.f[li][(long long)h * cap + lin] = v[h];
+            S.f[li][(long long)h * cap + vi] = v[h];
     }
 }
 
@@ -1563,8 +1668,8 @@ __global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld S, int m, A
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            st[o] = mr_lin<D>(g, m - 1, px + ox, py + oy);
-            ok = ok && tn.kind[li - 1][st[o]] != 0;
+            ok = ok && tn.kind[li - 1][mr_lin<D>(g, m - 1, px + ox, py + oy)] != 0;
+            st[o] = mr_vix<D>(g, m - 1, px + ox, py + oy);
         }
         if (!ok)
         {
@@ -1580,9 +1685,10 @@ __global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld S, int m, A
                 sv[o] = S.f[li - 1][(long long)h * capp + st[o]];
             v[h] = mr_predict<D>(sv, dx, dy);
         }
+        const int vi = vix<D>(x, y, ny);
 #pragma unroll
         for (int h = 0; h < Q; ++h)
-            S.f[li][(long long)h * cap + lin] = v[h];
+            S.f[li][(long long)h * cap + vi] = v[h];
     }
 }
 
@@ -1687,7 +1793,7 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
     {
         const int lin = mr_lin<D>(g, g.J1, x, y);
         if (tn.kind[lj][lin])
-            return S.f[lj][(long long)h * g.cap[lj] + lin];
+            return S.f[lj][(long long)h * g.cap[lj] + mr_vix<D>(g, g.J1, x, y)];
         // not materialised (rims of gap-1 leaves): one zero-detail prediction from
         // level J1-1, same operands and order as k_virtual would use
         const int lp = lj - 1;
@@ -1704,7 +1810,7 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
                 flag_err(aux.err, 0);
                 return 0.0;
             }
-            sv[o] = S.f[lp][(long long)h * g.cap[lp] + pl];
+            sv[o] = S.f[lp][(long long)h * g.cap[lp] + mr_vix<D>(g, g.J1 - 1, px + ox, py + oy)];
         }
         return mr_predict<D>(sv, xc & 1, yc & 1);
     }
@@ -1719,7 +1825,7 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
             const int sh = g.J1 - m;
             const int lin = xy2lin<D>(cx >> sh, cy >> sh, g.ny[li]);
             if (tn.kind[li][lin] & K_LEAF)
-                return S.f[li][(long long)h * g.cap[li] + lin];
+                return S.f[li][(long long)h * g.cap[li] + vix<D>(cx >> sh, cy >> sh, g.ny[li])];
         }
         flag_err(aux.err, 0);
         return 0.0;
@@ -1730,7 +1836,7 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         flag_err(aux.err, 2);
         return 0.0;
     }
-    const double v = S.f[leaf_li][(long long)hb * g.cap[leaf_li] + leaf_lin];
+    const double v = S.f[leaf_li][(long long)hb * g.cap[leaf_li] + vl<D>((int)leaf_lin, g.ny[leaf_li], g.lny[leaf_li])];
     if (kind == MRLBM_BC_BOUNCE_BACK)
         return v;
     if (kind == MRLBM_BC_ANTI_BOUNCE_BACK)
@@ -1892,7 +1998,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
                         const int sl = mr_lin<D>(g, m, x + o.x, y + o.y);
                         if (!tn.kind[li][sl])
                             flag_err(aux.err, 0);
-                        v = __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + sl]);
+                        v = __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + mr_vix<D>(g, m, x + o.x, y + o.y)]);
                     }
                     const int nv = min(32, ti.y - b0);
                     for (int j = 0; j < nv; ++j)
@@ -1924,7 +2030,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0,
         if (lane == 0)
         {
             const double scale = ldexp(1.0, D * (m - g.J1));
-            const long long o = (long long)h * cap + slot;
+            const long long o = (long long)h * cap + vix<D>(x, y, ny);
             F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
         }
     }
@@ -2245,7 +2351,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                 // generated path: fallback leaves without domain-leaving pairs run one
                 // thread per leaf in k_stream_collide MODE 2; only the boundary rim here
                 if (GEN && isfb && aux.fb1t)
-                    isfb = fl.fbd[li][lin] != 0;
+                    isfb = fl.fbd[li][vl<D>(lin, ny, g.lny[li])] != 0;
             }
             const unsigned bal = __ballot_sync(0xffffffffu, isfb);
             if (lane == 0)
@@ -2292,7 +2398,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                         in = in && yy >= 0 && yy < ny;
                 }
                 // clamped for out-of-domain stencil cells (MR boundary rule, D.8)
-                sBox[e][k] = in ? xy2lin<D>(xx, yy, ny) : mr_lin<D>(g, m, x + ox, y + oy);
+                sBox[e][k] = in ? vix<D>(xx, yy, ny) : mr_vix<D>(g, m, x + ox, y + oy);
             }
             else
             {
@@ -2300,15 +2406,16 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                 const int rx = 2 * x - 1 + (D == 1 ? r : r / 4), ry = D == 1 ? 0 : 2 * y - 1 + r % 4;
                 const bool in = (g.per0 || (rx >= 0 && rx < nxj)) && (D == 1 || g.per1 || (ry >= 0 && ry < nyj));
                 const int rl = in ? mr_lin<D>(g, g.J1, rx, ry) : -1;
-                sRim[r][k] = (rl >= 0 && (tn.kind[lj][rl] & K_LEAF)) ? rl : -1; // finest leaves only
+                sRim[r][k] = (rl >= 0 && (tn.kind[lj][rl] & K_LEAF)) ? mr_vix<D>(g, g.J1, rx, ry) : -1; // finest leaves only
             }
         }
         if (tid < nb)
         {
             const int lin = sQ[tid];
             sLin[tid] = lin;
-            sMask[tid] = fl.fbm[li][lin];
-            sDmask[tid] = fl.fbd[li][lin];
+            const int vi = vl<D>(lin, ny, g.lny[li]);
+            sMask[tid] = fl.fbm[li][vi];
+            sDmask[tid] = fl.fbd[li][vi];
             sBad[tid] = 0;
         }
         __syncthreads();
@@ -2384,7 +2491,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                         sum[side] = rim_sum<D>(g, tn, F1, scg, h, side, bx0, bx1, by0, by1, li, lin, aux);
                     }
             }
-            sF[h][k] = __dadd_rn(F1.f[li][(long long)h * cap + lin], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+            sF[h][k] = __dadd_rn(F1.f[li][(long long)h * cap + vl<D>(lin, ny, g.lny[li])], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
         }
         __syncthreads();
         // C1: m_i = row i of M f
@@ -2459,7 +2566,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                 fi = __dadd_rn(__dmul_rn(alpha, sFeq[i]), __dmul_rn(__dsub_rn(1.0, alpha), fi));
             if (!isfinite(fi))
                 sBad[k] = 1;
-            F0.f[li][(long long)i * cap + sLin[k]] = fi;
+            F0.f[li][(long long)i * cap + vl<D>(sLin[k], ny, g.lny[li])] = fi;
         }
         // shift the queue
         const int rest = qn - nb;
@@ -2555,6 +2662,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     for (; s < nL; s += sstep)
     {
         const int lin = lin_next;
+        const int vself = vl<D>(lin, ny, g.lny[li]);
         const uint8_t kd = kd_next;
         if (s + sstep < nL)
         {
@@ -2572,25 +2680,25 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
             // gap-1 fallback leaf without domain-leaving pairs, one thread per leaf:
             // table + details of the finest-leaf rim cells (Decision D.13b), the same
             // operands and order as k_fb1
-            if (fl.fbd[li][lin] != 0)
+            if (fl.fbd[li][vself] != 0)
                 continue; // boundary rim: k_fb1
             int x, y;
             lin2xy_l<D>(lin, ny, g.lny[li], x, y);
             gen_fb1t<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], tn.kind[li + 1], x, y, nx, ny, g.nx[li + 1],
-                            g.ny[li + 1], per0, per1, fl.fbm[li][lin], lin, sW, scale, f);
+                            g.ny[li + 1], per0, per1, fl.fbm[li][vself], vself, sW, scale, f);
         }
         else if (fb && gap >= kDeepGap)
         {
             // deep-gap fallback leaf: post-stream populations from K8
 #pragma unroll
             for (int h = 0; h < Q; ++h)
-                f[h] = Fout[(long long)h * cap + lin];
+                f[h] = Fout[(long long)h * cap + vself];
         }
         else if (GEN && !fb)
         {
             int x, y;
             lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-            gen_stream<EQ, Q, GC>(gap, Fin, cap, x, y, nx, ny, per0, per1, lin, sW, scale, f);
+            gen_stream<EQ, Q, GC>(gap, Fin, cap, x, y, nx, ny, per0, per1, vself, sW, scale, f);
         }
         else
         {
@@ -2613,9 +2721,9 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
                     else
                         in = in && yy >= 0 && yy < ny;
                 }
-                myslot[u * kT] = in ? xy2lin<D>(xx, yy, ny) : -1;
+                myslot[u * kT] = in ? vix<D>(xx, yy, ny) : -1;
             }
-            const unsigned mask = fb ? fl.fbm[li][lin] : 0u;
+            const unsigned mask = fb ? fl.fbm[li][vself] : 0u;
             if (mask)
             {
                 // shallow fallback leaf: table where exact, recursive rim elsewhere
@@ -2643,7 +2751,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
                         }
                         sum[side] = acc;
                     }
-                    f[h] = __dadd_rn(Fh[lin], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
+                    f[h] = __dadd_rn(Fh[vself], __dmul_rn(scale, __dsub_rn(sum[0], sum[1])));
                 }
             }
             else if (gap == 0)
@@ -2658,7 +2766,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
                     const int2 tE = sIdx[2 * h], tA = sIdx[2 * h + 1];
                     const int slE = tE.y ? myslot[sU[tE.x] * kT] : -1;
                     const int slA = tA.y ? myslot[sU[tA.x] * kT] : -1;
-                    fs[h] = Fh[lin];
+                    fs[h] = Fh[vself];
                     vE[h] = slE >= 0 ? Fh[slE] : 0.0;
                     vA[h] = slA >= 0 ? Fh[slA] : 0.0;
                 }
@@ -2677,7 +2785,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
                 for (int h = 0; h < Q; ++h)
                 {
                     const double* Fh = Fin + (long long)h * cap;
-                    const double fs = Fh[lin];
+                    const double fs = Fh[vself];
                     double sum[2];
 #pragma unroll
                     for (int side = 0; side < 2; ++side)
@@ -2756,7 +2864,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
         for (int h = 0; h < Q; ++h)
         {
             bad = bad || !isfinite(f[h]);
-            Fout[(long long)h * cap + lin] = f[h];
+            Fout[(long long)h * cap + vself] = f[h];
         }
         if (bad)
             flag_err(aux.err, 1);
@@ -2842,7 +2950,7 @@ __global__ void k_lin_to_idx(const int32_t* lin, int n, int d, int ny, int32_t* 
 }
 
 __global__ void k_load_scatter(const int* lins, const double* fin, int n, int q, const uint8_t* kind, double* F,
-                               long long cap, int* err)
+                               long long cap, int* err, int d, int ny, int lny)
 {
     GRID_STRIDE(i, 0, n)
     {
@@ -2852,19 +2960,22 @@ __global__ void k_load_scatter(const int* lins, const double* fin, int n, int q,
             atomicAdd(&err[2], 1);
             continue;
         }
+        const int vi = d == 2 ? vl<2>(lin, ny, lny) : lin;
         for (int h = 0; h < q; ++h)
-            F[(long long)h * cap + lin] = fin[(long long)h * n + i];
+            F[(long long)h * cap + vi] = fin[(long long)h * n + i];
     }
 }
 
 // read: gather the leaves (slot order) of a level into packed SoA q x n
-__global__ void k_gather_leaves(const int32_t* cells, int n, int q, const double* F, long long cap, double* out)
+__global__ void k_gather_leaves(const int32_t* cells, int n, int q, const double* F, long long cap, double* out, int d,
+                                int ny, int lny)
 {
     GRID_STRIDE(i, 0, n)
     {
         const int lin = cells[i];
+        const int vi = d == 2 ? vl<2>(lin, ny, lny) : lin;
         for (int h = 0; h < q; ++h)
-            out[(long long)h * n + i] = F[(long long)h * cap + lin];
+            out[(long long)h * n + i] = F[(long long)h * cap + vi];
     }
 }
 
@@ -2890,9 +3001,9 @@ __global__ void k_recon_project(Geo g, Tree t, Fld F, int m, int q)
             for (int c = 0; c < (1 << D); ++c)
             {
                 const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
-                acc = __dadd_rn(acc, src[xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)]);
+                acc = __dadd_rn(acc, src[vix<D>(2 * px + dx, 2 * py + dy, ny1)]);
             }
-            F.f[li][(long long)h * cap + plin] = __ddiv_rn(acc, (double)(1 << D));
+            F.f[li][(long long)h * cap + vix<D>(px, py, ny)] = __ddiv_rn(acc, (double)(1 << D));
         }
     }
 }
@@ -2912,8 +3023,10 @@ __global__ void k_recon_level(Geo g, Tree t, Fld S, Fld R, int m, int q)
         const int lin = (int)i;
         if (t.kind[li][lin] & (K_LEAF | K_INT))
         {
+            // R is row-major (lexicographic output), S in sibling blocks
+            const int vi = vl<D>(lin, ny, g.lny[li]);
             for (int h = 0; h < q; ++h)
-                R.f[li][(long long)h * cap + lin] = S.f[li][(long long)h * cap + lin];
+                R.f[li][(long long)h * cap + lin] = S.f[li][(long long)h * cap + vi];
             continue;
         }
         int x, y;
@@ -3044,6 +3157,7 @@ struct mrlbm_ctx {
     int frc_x0[kL]{}, frc_y0[kL]{}, frc_nx[kL]{}, frc_ny[kL]{};
     double* fhist = nullptr;
     int* fhn = nullptr;
+    int* rdcnt = nullptr; // read-back: level totals of the lexicographic re-sort
     int fcap = 0;
     cudaEvent_t ev[16]{};
     double phase_ms[MRLBM_PHASE_COUNT]{};
@@ -3580,6 +3694,12 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     g.nlev = ctx->nlev;
     g.per0 = rc->bc_kind[0] == MRLBM_BC_PERIODIC;
     g.per1 = ctx->D == 2 && rc->bc_kind[2] == MRLBM_BC_PERIODIC;
+    // 2D values are stored in 2x2 sibling blocks (vix): even level extents
+    if (ctx->D == 2 && ((rc->base_cells[0] & 1) || (rc->base_cells[1] & 1)))
+    {
+        delete ctx;
+        return MRLBM_ERR_CONFIG;
+    }
     for (int li = 0; li < ctx->nlev; ++li)
     {
         const long long nx = rc->base_cells[0] << li;
@@ -3896,7 +4016,8 @@ int mrlbm_commit(mrlbm_ctx* ctx)
             if (!n)
                 continue;
             k_load_scatter<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->ld_lin[li], ctx->F[1][li], (int)n, ctx->q,
-                                                                     ctx->kind2[v][li], ctx->F[0][li], g.cap[li], ctx->err);
+                                                                     ctx->kind2[v][li], ctx->F[0][li], g.cap[li], ctx->err,
+                                                                     ctx->D, g.ny[li], g.lny[li]);
         }
         CU(cudaGetLastError());
         int counts[4 * kL];
@@ -4036,22 +4157,39 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
         return st;
     if (n == 0)
         return MRLBM_OK;
+    if (!ctx->ld_idx[li])
+    {
+        CU(cudaMalloc(&ctx->ld_idx[li], sizeof(int32_t) * ctx->D * ctx->geo.cap[li]));
+        CU(cudaMalloc(&ctx->ld_lin[li], sizeof(int32_t) * ctx->geo.cap[li]));
+    }
+    // the step's slots are in value-block order (2D): re-sort the level lexicographically
+    // (CellIndex order, cell_set.hpp:333-354) with a row-major compaction of its kinds
+    const int32_t* lcells = ctx->cells[ctx->cur][li];
+    if (ctx->D == 2)
+    {
+        if (!ctx->rdcnt)
+            CU(cudaMalloc(&ctx->rdcnt, sizeof(int) * 4));
+        const long long cap = ctx->geo.cap[li];
+        const int ntl = static_cast<int>((cap + kTile - 1) / kTile);
+        const uint8_t* kind = ctx->kind2[ctx->cur][li];
+        k_tile_count<<<ntl, kTileThreads, 0, ctx->stream>>>(kind, cap, ctx->tiles[li]);
+        k_tile_scan<<<1, 1024, 0, ctx->stream>>>(ctx->tiles[li], ntl, ctx->rdcnt);
+        k_tile_scatter<<<ntl, kTileThreads, 0, ctx->stream>>>(kind, cap, ctx->tiles[li], ctx->rdcnt, nullptr,
+                                                              ctx->ld_lin[li]);
+        lcells = ctx->ld_lin[li];
+    }
     if (idx)
     {
-        if (!ctx->ld_idx[li])
-        {
-            CU(cudaMalloc(&ctx->ld_idx[li], sizeof(int32_t) * ctx->D * ctx->geo.cap[li]));
-            CU(cudaMalloc(&ctx->ld_lin[li], sizeof(int32_t) * ctx->geo.cap[li]));
-        }
-        k_lin_to_idx<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->cells[ctx->cur][li], (int)n, ctx->D, ctx->geo.ny[li],
+        k_lin_to_idx<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(lcells, (int)n, ctx->D, ctx->geo.ny[li],
                                                                  ctx->ld_idx[li]);
         CU(cudaMemcpyAsync(idx, ctx->ld_idx[li], sizeof(int32_t) * ctx->D * n, cudaMemcpyDeviceToHost, ctx->stream));
     }
     if (f)
     {
         double* stage = ctx->F[1 - ctx->curf][li]; // the non-state buffer is free between steps
-        k_gather_leaves<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(ctx->cells[ctx->cur][li], (int)n, ctx->q,
-                                                                   ctx->F[ctx->curf][li], ctx->geo.cap[li], stage);
+        k_gather_leaves<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(lcells, (int)n, ctx->q,
+                                                                   ctx->F[ctx->curf][li], ctx->geo.cap[li], stage, ctx->D,
+                                                                   ctx->geo.ny[li], ctx->geo.lny[li]);
         CU(cudaMemcpyAsync(f, stage, sizeof(double) * ctx->q * n, cudaMemcpyDeviceToHost, ctx->stream));
     }
     CU(cudaStreamSynchronize(ctx->stream));
@@ -4318,6 +4456,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         if (gph)
             cudaGraphExecDestroy(gph);
     free_force(ctx);
+    cudaFree(ctx->rdcnt);
     for (int v = 0; v < 2; ++v)
     {
         cudaFree(ctx->cnt[v]);
