@@ -312,7 +312,7 @@ struct TileP {
 };
 
 // zero the per-step keep / rn flags of every level (16 bytes per thread)
-__global__ void k_zero_flags(Geo g, Flags fl, LGrid lg_, int* fbc)
+__global__ void k_zero_flags(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_, int* fbc)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -335,7 +335,7 @@ __global__ void k_zero_flags(Geo g, Flags fl, LGrid lg_, int* fbc)
 // ---------------------------------------------------------------- K1 / K6 project
 // internal value = (sum of the 2^D children in children order) / 2^D   (prediction.hpp:51-60)
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Aux aux)
+__global__ void __launch_bounds__(256) k_project(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld F, int m, const __grid_constant__ Aux aux)
 {
     const int li = m - g.J0;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256) k_project(Geo g, Tree t, Fld F, int m, Au
 // summation order -> bit-identical).  dirty[] (per level, written for every new
 // internal node) carries the flag bottom-up; leaves are dirty iff not in the old tree.
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_project_new(Geo g, Tree to, Tree tn, Fld F, int m, uint8_t* const* dirty)
+__global__ void __launch_bounds__(256) k_project_new(const __grid_constant__ Geo g, const __grid_constant__ Tree to, const __grid_constant__ Tree tn, const __grid_constant__ Fld F, int m, uint8_t* const* dirty)
 {
     const int li = m - g.J0;
     const int nL = tn.cnt[li * 4 + 0], nI = tn.cnt[li * 4 + 1];
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256) k_project_new(Geo g, Tree to, Tree tn, Fl
 // (PAPER.md:656); keep iff metric >= eps_l (Eq. 10), blow-up
 // refinement iff metric >= 2^{mu+D} eps_l
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl, const SchemeDev* sc, LGrid lg_, Aux aux)
+__global__ void __launch_bounds__(256) k_details(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld F, const __grid_constant__ Flags fl, const SchemeDev* sc, const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -497,10 +497,122 @@ __global__ void __launch_bounds__(256) k_details(Geo g, Tree t, Fld F, Flags fl,
     }
 }
 
+// K1+K2 fused, one launch per level (m = J1-1 .. J0, bottom-up): each internal node
+// p of the old tree at level m projects its children (written: K6, the transfer and
+// the next level need it) and computes the details of its sibling group against the
+// prediction from its 3^D stencil at level m.  Internal stencil neighbours are
+// projected again in registers from their own children -- the same sum in children
+// order and division as their own thread, so bit-identical -- instead of reading the
+// value back after a grid-wide barrier: the children blocks are read once from DRAM
+// (neighbours' blocks are adjacent sectors, L1/L2 hits).
+template <int D>
+__device__ __forceinline__ double proj_block(const double* __restrict__ src, int base)
+{
+    double acc = 0.0;
+    if (D == 1)
+    {
+        const double2 a = *reinterpret_cast<const double2*>(src + base);
+        acc = __dadd_rn(__dadd_rn(acc, a.x), a.y);
+    }
+    else
+    {
+        const double2 a = *reinterpret_cast<const double2*>(src + base);
+        const double2 b = *reinterpret_cast<const double2*>(src + base + 2);
+        acc = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(acc, a.x), a.y), b.x), b.y);
+    }
+    return __ddiv_rn(acc, (double)(1 << D));
+}
+
+template <int D, int Q>
+__global__ void __launch_bounds__(256, 3)
+    k_proj_details(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld F,
+                   const __grid_constant__ Flags fl, const SchemeDev* sc, int m, const __grid_constant__ Aux aux)
+{
+    const int li = m - g.J0;
+    const int l = m + 1;
+    const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
+    const int nx = g.nx[li], ny = g.ny[li], ny1 = g.ny[li + 1];
+    const long long cap = g.cap[li], cap1 = g.cap[li + 1];
+    const double eps_l = ldexp(sc->eps, D * (l - g.J1));
+    const double eps_b = ldexp(eps_l, sc->mu + D);
+    const bool can_b = (l > g.J0) && (l < g.J1);
+    constexpr int NS = D == 1 ? 3 : 9;
+    constexpr int C = D == 1 ? 1 : 4; // stencil centre
+    GRID_STRIDE(s, nL, nL + nI)
+    {
+        const int plin = t.cells[li][s];
+        int px, py;
+        lin2xy_l<D>(plin, ny, g.lny[li], px, py);
+        // stencil sources: value index at level m (leaf) or -1 - child block (internal)
+        int src[NS];
+        bool ok = true;
+        for (int o = 0; o < NS; ++o)
+        {
+            const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
+            const int xx = mr_coord(px + ox, nx, g.per0);
+            const int yy = D == 1 ? 0 : mr_coord(py + oy, ny, g.per1);
+            const uint8_t kd = t.kind[li][xy2lin<D>(xx, yy, ny)];
+            ok = ok && (kd & (K_LEAF | K_INT)); // grading: the stencil is in R
+            src[o] = (kd & K_INT) ? -1 - (D == 1 ? 2 * xx : ((xx * (ny1 >> 1) + yy) << 2)) : vix<D>(xx, yy, ny);
+        }
+        const int pv = vix<D>(px, py, ny);
+        const int cb = D == 1 ? 2 * px : ((px * (ny1 >> 1) + py) << 2);
+        double metric = 0.0;
+#pragma unroll 1
+        for (int h = 0; h < Q; ++h)
+        {
+            const double* fm = F.f[li] + (long long)h * cap;
+            const double* f1 = F.f[li + 1] + (long long)h * cap1;
+            double ch[1 << D];
+            load_children<D>(f1, px, py, ny1, ch);
+            double acc = 0.0;
+#pragma unroll
+            for (int c = 0; c < (1 << D); ++c)
+                acc = __dadd_rn(acc, ch[c]);
+            const double centre = __ddiv_rn(acc, (double)(1 << D));
+            F.f[li][(long long)h * cap + pv] = centre;
+            double sv[NS];
+#pragma unroll
+            for (int o = 0; o < NS; ++o)
+            {
+                if (o == C)
+                    sv[o] = centre;
+                else
+                    sv[o] = src[o] >= 0 ? fm[src[o]] : proj_block<D>(f1, -1 - src[o]);
+            }
+            (void)cb;
+#pragma unroll
+            for (int c = 0; c < (1 << D); ++c)
+            {
+                const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+                const double d = __dsub_rn(ch[c], mr_predict<D>(sv, dx, dy));
+                const double ad = fabs(d);
+                if (ad > metric)
+                    metric = ad;
+            }
+        }
+        if (!ok)
+        {
+            flag_err(aux.err, 0);
+            continue;
+        }
+        if (metric >= eps_l)
+            fl.keep[li][plin] = 1;
+        if (can_b && metric >= eps_b)
+        {
+            for (int c = 0; c < (1 << D); ++c)
+            {
+                const int dx = D == 1 ? c : (c >> 1), dy = D == 1 ? 0 : (c & 1);
+                fl.rn[li + 1][xy2lin<D>(2 * px + dx, 2 * py + dy, ny1)] = 1;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- K3 flags
 // T closure: ancestors of kept groups are kept (Decision D.4)
 template <int D>
-__global__ void k_closure(Geo g, Tree t, Flags fl, int m)
+__global__ void k_closure(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Flags fl, int m)
 {
     const int li = m - g.J0;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
@@ -518,7 +630,7 @@ __global__ void k_closure(Geo g, Tree t, Flags fl, int m)
 
 // rn |= keep;  H(a): (l, k - eta^h) for k in R(T) at level l = m + 1
 template <int D>
-__global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, LGrid lg_, unsigned emask)
+__global__ void k_enlarge(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Flags fl, const SchemeDev* sc, const __grid_constant__ LGrid lg_, unsigned emask)
 {
     LSETUP;
     (void)sc;
@@ -557,7 +669,7 @@ __global__ void k_enlarge(Geo g, Tree t, Flags fl, const SchemeDev* sc, LGrid lg
 // grading G: for p refined at level m, its 3^D box must be in R_m, i.e. the
 // parents of the box at level m-1 are refined (one fine->coarse sweep, Decision D.7)
 template <int D>
-__global__ void k_grade(Geo g, Flags fl, int m)
+__global__ void k_grade(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, int m)
 {
     const int li = m - g.J0;
     const int nx = g.nx[li], ny = g.ny[li], nyp = g.ny[li - 1];
@@ -589,7 +701,7 @@ __global__ void k_grade(Geo g, Flags fl, int m)
 }
 
 // same, 16 cells of a row per thread (one 16-byte load; empty chunks cost one load)
-__global__ void k_grade_v(Geo g, Flags fl, int m)
+__global__ void k_grade_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, int m)
 {
     const int li = m - g.J0;
     const int nx = g.nx[li], ny = g.ny[li], nyp = g.ny[li - 1];
@@ -665,7 +777,7 @@ __global__ void k_grade_v(Geo g, Flags fl, int m)
 
 // ---------------------------------------------------------------- K4 kinds, fallback, ghosts, compaction
 template <int D>
-__global__ void k_kinds(Geo g, Flags fl, LGrid lg_)
+__global__ void k_kinds(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -741,7 +853,7 @@ __device__ __forceinline__ void band_cell(long long t, int side, int W, int bx0,
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_band(Geo g, Flags fl, Aux aux)
+__global__ void __launch_bounds__(256) k_band(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ Aux aux)
 {
     const int lane = threadIdx.x & 31;
     const int warps = (gridDim.x * blockDim.x) >> 5;
@@ -794,7 +906,7 @@ __device__ __forceinline__ int ghost_dist(const Geo& g, int m)
 }
 
 template <int D>
-__global__ void k_ghost_rows(Geo g, Flags fl, LGrid lg_)
+__global__ void k_ghost_rows(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -826,7 +938,7 @@ __global__ void k_ghost_rows(Geo g, Flags fl, LGrid lg_)
 }
 
 template <int D>
-__global__ void k_ghost(Geo g, Flags fl, LGrid lg_)
+__global__ void k_ghost(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -875,7 +987,7 @@ union V16 {
     uint8_t b[16];
 };
 
-__global__ void k_kinds_v(Geo g, Flags fl, LGrid lg_)
+__global__ void k_kinds_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -907,7 +1019,7 @@ __global__ void k_kinds_v(Geo g, Flags fl, LGrid lg_)
 // fallback flags: chunks without a plain leaf are skipped with one load
 template <int D>
 __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int m, int li, int gap, long long i, int x,
-                                              int y, const int4& ub, const int2& pi, Aux& aux, int ib_in = -1,
+                                              int y, const int4& ub, const int2& pi, const Aux& aux, int ib_in = -1,
                                               const int4* sdep = nullptr, const unsigned short* spm = nullptr)
 {
     (void)pi;
@@ -983,7 +1095,7 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
 }
 
 template <int D>
-__global__ void k_fallback(Geo g, Flags fl, LGrid lg_, Aux aux)
+__global__ void k_fallback(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -1002,7 +1114,7 @@ __global__ void k_fallback(Geo g, Flags fl, LGrid lg_, Aux aux)
     }
 }
 
-__global__ void k_fallback_v(Geo g, Flags fl, LGrid lg_, Aux aux)
+__global__ void k_fallback_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
 {
     LSETUP;
     __shared__ int4 sdep[2 * kQ];
@@ -1062,7 +1174,7 @@ __global__ void k_fallback_v(Geo g, Flags fl, LGrid lg_, Aux aux)
 }
 
 // ghost rows: tmp = OR of R membership over y +- 2 (same row)
-__global__ void k_ghost_rows_v(Geo g, Flags fl, LGrid lg_)
+__global__ void k_ghost_rows_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -1109,7 +1221,7 @@ __global__ void k_ghost_rows_v(Geo g, Flags fl, LGrid lg_)
 }
 
 // ghosts: empty cells with an R cell within +-2 rows of tmp
-__global__ void k_ghost_v(Geo g, Flags fl, LGrid lg_)
+__global__ void k_ghost_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -1397,7 +1509,7 @@ __device__ __forceinline__ void load16_blk(const Geo& g, int li, const uint8_t* 
 
 // multi-level compaction: block range per level = that level's tiles (count,
 // scatter) or one block per level (scan)
-__global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(Geo g, Flags fl, TileP tp, LGrid lg_)
+__global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ TileP tp, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     (void)lvg_;
@@ -1448,7 +1560,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(Geo g, Flags fl,
     }
 }
 
-__global__ void k_tile_scan_ml(Geo g, TileP tp, Tree tn, LGrid lg_)
+__global__ void k_tile_scan_ml(const __grid_constant__ Geo g, const __grid_constant__ TileP tp, const __grid_constant__ Tree tn, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     (void)lvb_;
@@ -1490,7 +1602,7 @@ __global__ void k_tile_scan_ml(Geo g, TileP tp, Tree tn, LGrid lg_)
         }
 }
 
-__global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags fl, TileP tp, Tree tn, LGrid lg_)
+__global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ TileP tp, const __grid_constant__ Tree tn, const __grid_constant__ LGrid lg_)
 {
     LSETUP;
     (void)lvg_;
@@ -1595,7 +1707,7 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(Geo g, Flags f
 // new R cell: old value if it was in the old complete tree (copy / projected),
 // else prediction from the new level m-1 values (Decision D.24)
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld S, int m, Aux aux)
+__global__ void __launch_bounds__(256) k_transfer(const __grid_constant__ Geo g, const __grid_constant__ Tree to, const __grid_constant__ Tree tn, const __grid_constant__ Fld S, int m, const __grid_constant__ Aux aux)
 {
     // in place in the state buffer S: cells of the old complete tree keep their value
     // (old leaf / projected internal); cells new to the complete tree are predicted
@@ -1650,7 +1762,7 @@ __global__ void __launch_bounds__(256) k_transfer(Geo g, Tree to, Tree tn, Fld S
 
 // virtual cells (ghosts + reconstruction bands): zero-detail prediction from level m-1
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_virtual(Geo g, Tree tn, Fld S, int m, Aux aux)
+__global__ void __launch_bounds__(256) k_virtual(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld S, int m, const __grid_constant__ Aux aux)
 {
     const int li = m - g.J0;
     const int nR = tn.cnt[li * 4 + 0] + tn.cnt[li * 4 + 1], nV = tn.cnt[li * 4 + 2];
@@ -1957,7 +2069,7 @@ __device__ __forceinline__ int rim_cell(int side, int ex, int ey, int bx0, int b
 // table / rim order through shuffles, so the arithmetic is rim_sum's.  Writes
 // post-stream populations into F0; K7 collides them.
 template <int D>
-__global__ void __launch_bounds__(256) k_stream_fallback(Geo g, Tree tn, Fld F0, Fld F1, Flags fl, const SchemeDev* sc,
+__global__ void __launch_bounds__(256) k_stream_fallback(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld F0, const __grid_constant__ Fld F1, const __grid_constant__ Flags fl, const SchemeDev* sc,
                                                          Aux aux)
 {
     const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
@@ -2884,7 +2996,7 @@ __global__ void k_count_updates(const int* cnt, int nlev, long long* acc)
 
 // loading: mark loaded leaves and their ancestors; scatter values after compaction
 template <int D>
-__global__ void k_load_mark(Geo g, Flags fl, const int* lins, int n, int m)
+__global__ void k_load_mark(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const int* lins, int n, int m)
 {
     const int li = m - g.J0;
     const int ny = g.ny[li];
@@ -2902,7 +3014,7 @@ __global__ void k_load_mark(Geo g, Flags fl, const int* lins, int n, int m)
 }
 
 template <int D>
-__global__ void k_closure_dense(Geo g, Flags fl, int m)
+__global__ void k_closure_dense(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, int m)
 {
     const int li = m - g.J0;
     const int ny = g.ny[li];
@@ -2983,7 +3095,7 @@ __global__ void k_gather_leaves(const int32_t* cells, int n, int q, const double
 // Internal values of the current tree = projection of its leaves (the values K1 of the
 // next step recomputes identically), runtime q.  Slots [nL, nL + nI) of level m.
 template <int D>
-__global__ void k_recon_project(Geo g, Tree t, Fld F, int m, int q)
+__global__ void k_recon_project(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld F, int m, int q)
 {
     const int li = m - g.J0;
     const int nL = t.cnt[li * 4 + 0], nI = t.cnt[li * 4 + 1];
@@ -3013,7 +3125,7 @@ __global__ void k_recon_project(Geo g, Tree t, Fld F, int m, int q)
 // (complete) reconstruction of level m-1 with the clamp / wrap stencil rule (D.8).
 // Level J0 lies entirely in R.  Same recursion as the oracle's rec().
 template <int D>
-__global__ void k_recon_level(Geo g, Tree t, Fld S, Fld R, int m, int q)
+__global__ void k_recon_level(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld S, const __grid_constant__ Fld R, int m, int q)
 {
     const int li = m - g.J0;
     const long long cap = g.cap[li];
@@ -3141,6 +3253,10 @@ struct mrlbm_ctx {
     bool use_graph = true;
     bool use_gen = false; // generated stream / collision path (built-in velocity sets)
     bool use_fb1t = true; // gap-1 fallback leaves thread per leaf (MODE 2); MRLBM_NO_FB1T=1 turns it off
+    // K1+K2 fused per level (MRLBM_FUSE_PD=1): measured slower than the separate
+    // kernels (re-projecting the internal stencil neighbours costs more than the
+    // second read of the children), so off by default
+    bool fuse_pd = false;
     bool gen_ok = false;  // the generated code's constants match this scheme
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
@@ -3360,12 +3476,24 @@ void enqueue_step(mrlbm_ctx* c)
         kmark(c, "k_zero_flags", -1);
     }
     phase_mark(c, 0);
-    // K1 projection of the old tree (bottom-up)
-    for (int m = c->J1 - 1; m >= c->J0; --m)
-        { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
-    phase_mark(c, 1);
-    // K2 details + flags
+    if (c->fuse_pd)
     {
+        // K1 + K2 fused per level, bottom-up (the details phase is folded into "project")
+        for (int m = c->J1 - 1; m >= c->J0; --m)
+        {
+            c->kcount++;
+            k_proj_details<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, fl, c->sch, m, aux);
+            kmark(c, "k_proj_details", m);
+        }
+        phase_mark(c, 1);
+    }
+    else
+    {
+        // K1 projection of the old tree (bottom-up)
+        for (int m = c->J1 - 1; m >= c->J0; --m)
+            { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
+        phase_mark(c, 1);
+        // K2 details + flags
         LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
         c->kcount++;
         k_details<D, Q><<<nb, T, 0, s>>>(g, to, Sf, fl, c->sch, lg, aux);
@@ -3915,6 +4043,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     }
     ctx->use_gen = builtin_velocities(sc) && ctx->gen_ok && std::getenv("MRLBM_NO_GEN") == nullptr;
     ctx->use_fb1t = std::getenv("MRLBM_NO_FB1T") == nullptr;
+    ctx->fuse_pd = std::getenv("MRLBM_FUSE_PD") != nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
         const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;

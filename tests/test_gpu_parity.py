@@ -85,3 +85,19 @@ def test_generic_table_path_parity(cid, J, monkeypatch):
         assert rel <= 1e-12
     gpu.close()
     ora.close()
+
+
+@pytest.mark.parametrize("env", ["MRLBM_FUSE_PD", "MRLBM_NO_FB1T"])
+@pytest.mark.parametrize("cid,J", [(3, 6), (4, 6), (5, 7)])
+def test_kernel_variant_parity(cid, J, env, monkeypatch):
+    """The alternative kernel schedules (fused projection + details; gap-1 fallback
+    leaves in the block kernel k_fb1 only) stay bit-identical to the oracle."""
+    monkeypatch.setenv(env, "1")
+    sc, rc, gpu, ora = make_pair(cid, J)
+    for k in range(12):
+        gpu.step(1)
+        ora.step(1)
+        rel, bitwise, _ = compare(gpu, ora, rc, f"{env} config {cid} step {k}")
+        assert rel <= 1e-12
+    gpu.close()
+    ora.close()
