@@ -341,11 +341,11 @@ def gen_fb1t(name, d, q, etas, out):
     box = [o for o in itertools.product(range(-2, 3), repeat=d)]
     bidx = (lambda o: o[0] + 2) if d == 1 else (lambda o: (o[0] + 2) * 5 + (o[1] + 2))
     out.append(f"__device__ __forceinline__ void gen_fb1t_{name}(const double* __restrict__ Fin, long long cap, "
-               f"const double* __restrict__ Fj, long long capj, const uint8_t* __restrict__ kindj, "
+               f"const double* __restrict__ Fj, long long capj, unsigned ring, "
                f"int x, int y, int nx, int ny, int nxj, int nyj, int per0, int per1, unsigned mask, "
                f"long long s, const double* sW, double scale, double (&f)[{q}])")
     out.append("{")
-    out.append("    (void)y; (void)ny; (void)nyj; (void)per1; (void)capj; (void)Fj; (void)kindj; (void)nxj;")
+    out.append("    (void)y; (void)ny; (void)nyj; (void)per1; (void)capj; (void)Fj; (void)ring; (void)nxj;")
     used_all = set()
     for h, eta in enumerate(etas):
         for side in (0, 1):
@@ -397,13 +397,15 @@ def gen_fb1t(name, d, q, etas, out):
                     p = tuple((ci + 1) // 2 - 1 for ci in c)
                     par = tuple((ci + 1) & 1 for ci in c)
                     xs = f"2 * x + ({c[0] - 1})"
+                    r = c[0] if d == 1 else c[0] * 4 + c[1]
+                    # ring bit r: the finest cell is a leaf (computed once per leaf by the caller)
+                    out.append(f"            if ((ring >> {r}) & 1u)")
+                    out.append("            {")
                     if d == 1:
-                        out.append(f"            {{ const int jl = gen_wrap({xs}, nxj, per0), jv = jl;")
+                        out.append(f"              const int jv = gen_wrap({xs}, nxj, per0);")
                     else:
                         ys = f"2 * y + ({c[1] - 1})"
-                        out.append(f"            {{ const int jx = gen_wrap({xs}, nxj, per0), jy = gen_wrap({ys}, nyj, per1);")
-                        out.append("              const int jl = jx * nyj + jy, jv = gen_vix(jx, jy, nyj);")
-                    out.append("              if (kindj[jl] & 1)")
+                        out.append(f"              const int jv = gen_vix(gen_wrap({xs}, nxj, per0), gen_wrap({ys}, nyj, per1), nyj);")
                     out.append("              {")
                     sv = [f"v{bidx(tuple(pi + si for pi, si in zip(p, st)))}" for st in itertools.product((-1, 0, 1), repeat=d)]
                     out.append(f"                const double sv[{len(sv)}] = {{{', '.join(sv)}}};")

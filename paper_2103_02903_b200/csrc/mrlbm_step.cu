@@ -105,7 +105,7 @@ struct Aux {
     const unsigned short* umask; // [g] union over the pairs
     // obstacle force tracking (null when off): per level, a dense box over the disc's
     // bounding box holding each leaf's (Fx, Fy) term of the current step
-    int fb1t;           // gap-1 fallback leaves with dmask == 0 run in k_stream_collide MODE 2
+    int fb1t;           // thread-per-leaf gap-1 path on: k_fb1 takes only the listed boundary-rim leaves
     double* frc;
     long long frc_off[kL];
     int frc_x0[kL], frc_y0[kL], frc_nx[kL], frc_ny[kL];
@@ -1072,7 +1072,9 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     fl.fbm[li][vi] = mask;
     fl.fbd[li][vi] = dmask;
     fl.kind[li][i] = K_LEAF | K_FB;
-    if (gap >= 2)
+    // listed: deep-gap leaves (K8, bands) and, with the thread-per-leaf gap-1 path,
+    // the gap-1 leaves whose pairs leave the domain (k_fb1)
+    if (gap >= 2 || (gap == 1 && dmask != 0 && aux.fb1t))
     {
         const int k = atomicAdd(aux.fb_count, 1);
         if (k < aux.fb_cap)
@@ -1086,7 +1088,7 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     }
     else
     {
-        // gap 0 / 1 fallback leaves are found by slot scans (K7 / k_fb1);
+        // gap 0 / 1 fallback leaves are found by slot scans (K7 / MODE 2 or k_fb1);
         // count them for the statistics with one atomic per warp
         const unsigned am = __activemask();
         if ((threadIdx.x & 31) == __ffs(am) - 1)
@@ -1144,6 +1146,19 @@ __global__ void k_fallback_v(const __grid_constant__ Geo g, const __grid_constan
         const int lin0 = (int)(c * 16);
         const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
         const int nx = g.nx[li];
+        if (aux.umask[gap] == 0)
+        {
+            // no parent can break the table at this gap (the finest level): only the
+            // domain test flags a leaf, so interior chunks are done
+            const bool edge = (!g.per0 && (x + ub.x < 0 || x + ub.y >= nx)) ||
+                              (!g.per1 && (y0 + ub.z < 0 || y0 + 15 + ub.w >= ny));
+            if (!edge)
+                continue;
+            for (int j = 0; j < 16; ++j)
+                if (k.b[j] == K_LEAF)
+                    fallback_cell<2>(g, fl, m, li, gap, lin0 + j, x, y0 + j, ub, pi, aux, 0, sdep, spm);
+            continue;
+        }
         // internal flags of rows x-1, x, x+1 over y0-1 .. y0+16 (clip / wrap)
         uint8_t w[3][18];
 #pragma unroll
@@ -2335,11 +2350,11 @@ __device__ __forceinline__ void gen_fb1h(int h, const double* Fin, long long cap
 // gap-1 fallback leaf, thread per leaf (stream_gen.cuh gen_fb1t_*)
 template <int EQ, int Q>
 __device__ __forceinline__ void gen_fb1t(const double* Fin, long long cap, const double* Fj, long long capj,
-                                         const uint8_t* kindj, int x, int y, int nx, int ny, int nxj, int nyj,
+                                         unsigned ring, int x, int y, int nx, int ny, int nxj, int nyj,
                                          int per0, int per1, unsigned mask, long long s, const double* sW, double scale,
                                          double (&f)[Q])
 {
-#define GEN_FB1T(N) gen_fb1t_EQ##N(Fin, cap, Fj, capj, kindj, x, y, nx, ny, nxj, nyj, per0, per1, mask, s, sW, scale, f);
+#define GEN_FB1T(N) gen_fb1t_EQ##N(Fin, cap, Fj, capj, ring, x, y, nx, ny, nxj, nyj, per0, per1, mask, s, sW, scale, f);
     if constexpr (EQ == 1 && Q == 2)
         GEN_FB1T(1)
     else if constexpr (EQ == 2 && Q == 9)
@@ -2445,7 +2460,10 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
     const int nx = g.nx[li], ny = g.ny[li], nxj = g.nx[lj], nyj = g.ny[lj];
     const long long cap = g.cap[li], capj = g.cap[lj];
     const double scale = ldexp(1.0, D * (m - g.J1));
-    const long long nchunk = (nL + NT - 1) / NT;
+    // list mode (thread-per-leaf gap-1 path on): only the listed boundary-rim leaves
+    const bool from_list = GEN && aux.fb1t;
+    const int nfb = from_list ? min(*aux.fb_count, (int)aux.fb_cap) : 0;
+    const long long nchunk = from_list ? (nfb + NT - 1) / NT : (nL + NT - 1) / NT;
     int qn = 0;
     long long ch = blockIdx.x;
     while (ch < nchunk || qn > 0)
@@ -2456,14 +2474,19 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
             const long long sl = ch * NT + tid;
             int lin = -1;
             bool isfb = false;
-            if (sl < nL)
+            if (from_list)
+            {
+                if (sl < nfb)
+                {
+                    const int2 e = aux.fb_list[sl];
+                    isfb = e.x == m;
+                    lin = e.y;
+                }
+            }
+            else if (sl < nL)
             {
                 lin = tn.cells[li][sl];
                 isfb = (tn.skind[li][sl] & K_FB) != 0;
-                // generated path: fallback leaves without domain-leaving pairs run one
-                // thread per leaf in k_stream_collide MODE 2; only the boundary rim here
-                if (GEN && isfb && aux.fb1t)
-                    isfb = fl.fbd[li][vl<D>(lin, ny, g.lny[li])] != 0;
             }
             const unsigned bal = __ballot_sync(0xffffffffu, isfb);
             if (lane == 0)
@@ -2791,13 +2814,40 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
         {
             // gap-1 fallback leaf without domain-leaving pairs, one thread per leaf:
             // table + details of the finest-leaf rim cells (Decision D.13b), the same
-            // operands and order as k_fb1
+            // operands and order as k_fb1 (which takes the boundary rim leaves, listed)
             if (fl.fbd[li][vself] != 0)
-                continue; // boundary rim: k_fb1
+                continue;
             int x, y;
             lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-            gen_fb1t<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], tn.kind[li + 1], x, y, nx, ny, g.nx[li + 1],
-                            g.ny[li + 1], per0, per1, fl.fbm[li][vself], vself, sW, scale, f);
+            // finest leaves among the 4^D cells around the children (the E-rim ring;
+            // the inner 2^D are the leaf's own children, never leaves): one bit each
+            const int nxj = g.nx[li + 1], nyj = g.ny[li + 1];
+            const uint8_t* kj = tn.kind[li + 1];
+            unsigned ring = 0;
+#pragma unroll
+            for (int r = 0; r < (D == 1 ? 4 : 16); ++r)
+            {
+                const int dx = D == 1 ? r : r >> 2, dy = D == 1 ? 0 : r & 3;
+                if (dx >= 1 && dx <= 2 && (D == 1 || (dy >= 1 && dy <= 2)))
+                    continue;
+                int xr = 2 * x - 1 + dx, yr = D == 1 ? 0 : 2 * y - 1 + dy;
+                if (xr < 0 || xr >= nxj)
+                {
+                    if (!per0)
+                        continue;
+                    xr = mr_coord(xr, nxj, 1);
+                }
+                if (D == 2 && (yr < 0 || yr >= nyj))
+                {
+                    if (!per1)
+                        continue;
+                    yr = mr_coord(yr, nyj, 1);
+                }
+                if (kj[xy2lin<D>(xr, yr, nyj)] & K_LEAF)
+                    ring |= 1u << r;
+            }
+            gen_fb1t<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], ring, x, y, nx, ny, nxj, nyj, per0, per1,
+                            fl.fbm[li][vself], vself, sW, scale, f);
         }
         else if (fb && gap >= kDeepGap)
         {
@@ -3252,7 +3302,7 @@ struct mrlbm_ctx {
     bool profiling = false;
     bool use_graph = true;
     bool use_gen = false; // generated stream / collision path (built-in velocity sets)
-    bool use_fb1t = true; // gap-1 fallback leaves thread per leaf (MODE 2); MRLBM_NO_FB1T=1 turns it off
+    bool use_fb1t = true; // gap-1 fallback leaves thread per leaf (K7 MODE 2) instead of k_fb1; MRLBM_NO_FB1T=1 turns it off
     // K1+K2 fused per level (MRLBM_FUSE_PD=1): measured slower than the separate
     // kernels (re-projecting the internal stencil neighbours costs more than the
     // second read of the children), so off by default
@@ -3366,7 +3416,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.pmask = c->pmaskd;
     a.umask = c->umaskd;
     a.frc = c->frc;
-    a.fb1t = c->use_fb1t ? 1 : 0;
+    a.fb1t = (c->use_fb1t && c->use_gen) ? 1 : 0;
     for (int i = 0; i < kL; ++i)
     {
         a.frc_off[i] = 2 * c->frc_off[i];
@@ -3602,14 +3652,19 @@ void enqueue_step(mrlbm_ctx* c)
     // default kernels carry no extra code
     constexpr bool kObs = EQ == MRLBM_EQ_NS_D2Q9 && D == 2;
     const bool frc = kObs && c->frc != nullptr;
+    const bool tpl = GEN && c->use_fb1t;
     if (c->J1 > c->J0)
     {
-        c->kcount++;
-        if (frc)
-            k_fb1<D, Q, BS, EQ, GEN, kObs><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
-        else
-            k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
-        kmark(c, "k_fb1", -1);
+        {
+            // list mode (tpl) has little work: one block per SM
+            const int nbf = tpl ? 148 : c->grid_cap;
+            c->kcount++;
+            if (frc)
+                k_fb1<D, Q, BS, EQ, GEN, kObs><<<nbf, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+            else
+                k_fb1<D, Q, BS, EQ, GEN><<<nbf, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+            kmark(c, "k_fb1", -1);
+        }
         if constexpr (GEN)
         if (c->use_fb1t)
         {
