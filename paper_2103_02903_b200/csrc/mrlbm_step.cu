@@ -1779,16 +1779,39 @@ __global__ void __launch_bounds__(256) k_transfer(const __grid_constant__ Geo g,
 template <int D, int Q>
 __global__ void __launch_bounds__(256) k_virtual(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld S, int m, const __grid_constant__ Aux aux)
 {
+    // Virtual slots are in value-block order, so the virtual siblings of one parent are
+    // consecutive slots: the first of them (the group leader) loads the parent's stencil
+    // once per population and writes every virtual sibling (same mr_predict operands and
+    // order as one thread per cell); the other threads of the group return.
     const int li = m - g.J0;
     const int nR = tn.cnt[li * 4 + 0] + tn.cnt[li * 4 + 1], nV = tn.cnt[li * 4 + 2];
     const int ny = g.ny[li];
     const long long cap = g.cap[li], capp = g.cap[li - 1];
+    constexpr int NC = 1 << D;
     GRID_STRIDE(s, nR, nR + nV)
     {
         const int lin = tn.cells[li][s];
         int x, y;
         lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-        const int px = x >> 1, py = y >> 1, dx = x & 1, dy = y & 1;
+        const int px = x >> 1, py = y >> 1;
+        if (s > nR)
+        {
+            int xp, yp;
+            lin2xy_l<D>(tn.cells[li][s - 1], ny, g.lny[li], xp, yp);
+            if ((xp >> 1) == px && (D == 1 || (yp >> 1) == py))
+                continue; // a sibling leads this group
+        }
+        // the group's virtual cells: children codes c = 2 dx + dy (1D: dx)
+        int cc[NC], nc = 0;
+        cc[nc++] = D == 1 ? (x & 1) : ((x & 1) << 1) | (y & 1);
+        for (int k = 1; k < NC && s + k < nR + nV; ++k)
+        {
+            int xn, yn;
+            lin2xy_l<D>(tn.cells[li][s + k], ny, g.lny[li], xn, yn);
+            if ((xn >> 1) != px || (D == 2 && (yn >> 1) != py))
+                break;
+            cc[nc++] = D == 1 ? (xn & 1) : ((xn & 1) << 1) | (yn & 1);
+        }
         constexpr int NS = D == 1 ? 3 : 9;
         int st[NS];
         bool ok = true;
@@ -1803,19 +1826,22 @@ __global__ void __launch_bounds__(256) k_virtual(const __grid_constant__ Geo g, 
             flag_err(aux.err, 0);
             continue;
         }
-        double v[Q];
-#pragma unroll
+        // the parent's value block at level m holds the children in code order
+        const long long base = D == 1 ? 2LL * px : ((long long)px * (ny >> 1) + py) << 2;
+#pragma unroll 3
         for (int h = 0; h < Q; ++h)
         {
             double sv[NS];
+#pragma unroll
             for (int o = 0; o < NS; ++o)
                 sv[o] = S.f[li - 1][(long long)h * capp + st[o]];
-            v[h] = mr_predict<D>(sv, dx, dy);
+            double* dst = S.f[li] + (long long)h * cap + base;
+            for (int k = 0; k < nc; ++k)
+            {
+                const int c = cc[k];
+                dst[c] = mr_predict<D>(sv, D == 1 ? c : c >> 1, D == 1 ? 0 : c & 1);
+            }
         }
-        const int vi = vix<D>(x, y, ny);
-#pragma unroll
-        for (int h = 0; h < Q; ++h)
-            S.f[li][(long long)h * cap + vi] = v[h];
     }
 }
 
