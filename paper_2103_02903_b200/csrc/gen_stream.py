@@ -330,7 +330,7 @@ def gen_collide(out):
         out.append("")
 
 
-def gen_fb1t(name, d, q, etas, out):
+def gen_fb1t(name, d, q, etas, out, rs=False):
     """Gap-1 fallback leaves, one thread per leaf (k_fb1t): every population's
     table sums + details of the rim cells that are finest leaves (Decision D.13b),
     the same operands and order as gen_fb1h.  For leaves without domain-leaving
@@ -340,10 +340,19 @@ def gen_fb1t(name, d, q, etas, out):
     tabs = {(h, side): table_offsets(d, 1, eta, side) for h, eta in enumerate(etas) for side in (0, 1)}
     box = [o for o in itertools.product(range(-2, 3), repeat=d)]
     bidx = (lambda o: o[0] + 2) if d == 1 else (lambda o: (o[0] + 2) * 5 + (o[1] + 2))
-    out.append(f"__device__ __forceinline__ void gen_fb1t_{name}(const double* __restrict__ Fin, long long cap, "
-               f"const double* __restrict__ Fj, long long capj, unsigned ring, "
-               f"int x, int y, int nx, int ny, int nxj, int nyj, int per0, int per1, unsigned mask, "
-               f"long long s, const double* sW, double scale, double (&f)[{q}])")
+    if rs:
+        # boundary-rim variant: pairs whose dependencies leave the domain take rs(h, side)
+        # (the recursive rim sum with the boundary rule) instead of table + details
+        out.append("template <class RS>")
+        out.append(f"__device__ __forceinline__ void gen_fb1t_rs_{name}(const double* __restrict__ Fin, long long cap, "
+                   f"const double* __restrict__ Fj, long long capj, unsigned ring, "
+                   f"int x, int y, int nx, int ny, int nxj, int nyj, int per0, int per1, unsigned mask, unsigned dmask, "
+                   f"const RS& rs, long long s, const double* sW, double scale, double (&f)[{q}])")
+    else:
+        out.append(f"__device__ __forceinline__ void gen_fb1t_{name}(const double* __restrict__ Fin, long long cap, "
+                   f"const double* __restrict__ Fj, long long capj, unsigned ring, "
+                   f"int x, int y, int nx, int ny, int nxj, int nyj, int per0, int per1, unsigned mask, "
+                   f"long long s, const double* sW, double scale, double (&f)[{q}])")
     out.append("{")
     out.append("    (void)y; (void)ny; (void)nyj; (void)per1; (void)capj; (void)Fj; (void)ring; (void)nxj;")
     used_all = set()
@@ -414,6 +423,9 @@ def gen_fb1t(name, d, q, etas, out):
                     out.append("              }")
                     out.append("            }")
                 out.append("        }")
+            if rs:
+                out.append(f"        if ((dmask >> {pair}) & 1u)")
+                out.append(f"            {nm} = rs({h}, {side});")
         out.append(f"        f[{h}] = __dadd_rn(fs, __dmul_rn(scale, __dsub_rn(sE, sA)));")
         out.append("    }")
     out.append("}")
@@ -449,6 +461,7 @@ def main():
         gen_fb1h(name, d, q, etas, out)
     for name, (d, q, etas) in SETS.items():
         gen_fb1t(name, d, q, etas, out)
+        gen_fb1t(name, d, q, etas, out, rs=True)
     gen_collide(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "stream_gen.cuh")
     open(path, "w").write("\n".join(out) + "\n")

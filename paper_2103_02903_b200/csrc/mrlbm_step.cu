@@ -105,7 +105,11 @@ struct Aux {
     const unsigned short* umask; // [g] union over the pairs
     // obstacle force tracking (null when off): per level, a dense box over the disc's
     // bounding box holding each leaf's (Fx, Fy) term of the current step
-    int fb1t;           // thread-per-leaf gap-1 path on: k_fb1 takes only the listed boundary-rim leaves
+    int fb1t;           // thread-per-leaf gap-1 path on: the boundary-rim fallback leaves are listed
+    int* fbs;           // [2] segment lists of linear indices: 0 = gap-0 fallback leaves (level J1),
+                        //     1 = gap-1 fallback leaves with domain-leaving pairs (level J1-1);
+                        //     counts at fb_count[2 + seg]
+    long long fbs_off[2], fbs_cap[2];
     double* frc;
     long long frc_off[kL];
     int frc_x0[kL], frc_y0[kL], frc_nx[kL], frc_ny[kL];
@@ -317,7 +321,7 @@ __global__ void k_zero_flags(const __grid_constant__ Geo g, const __grid_constan
     LSETUP;
     const int li = m - g.J0;
     const long long n16 = g.cap[li] / 16, n = g.cap[li];
-    if (blockIdx.x == 0 && threadIdx.x < 2)
+    if (blockIdx.x == 0 && threadIdx.x < 4)
         fbc[threadIdx.x] = 0;
     LGRID_STRIDE(i, 0, n16)
     {
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(256) k_project_new(const __grid_constant__ Geo
 // (PAPER.md:656); keep iff metric >= eps_l (Eq. 10), blow-up
 // refinement iff metric >= 2^{mu+D} eps_l
 template <int D, int Q>
-__global__ void __launch_bounds__(256) k_details(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld F, const __grid_constant__ Flags fl, const SchemeDev* sc, const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
+__global__ void __launch_bounds__(256, 4) k_details(const __grid_constant__ Geo g, const __grid_constant__ Tree t, const __grid_constant__ Fld F, const __grid_constant__ Flags fl, const SchemeDev* sc, const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
 {
     LSETUP;
     const int li = m - g.J0;
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(256) k_details(const __grid_constant__ Geo g, 
             continue;
         }
         double metric = 0.0;
-        #pragma unroll
+        #pragma unroll 3
         for (int h = 0; h < Q; ++h)
         {
             const double* fm = F.f[li] + (long long)h * cap;
@@ -1072,9 +1076,19 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     fl.fbm[li][vi] = mask;
     fl.fbd[li][vi] = dmask;
     fl.kind[li][i] = K_LEAF | K_FB;
-    // listed: deep-gap leaves (K8, bands) and, with the thread-per-leaf gap-1 path,
-    // the gap-1 leaves whose pairs leave the domain (k_fb1)
-    if (gap >= 2 || (gap == 1 && dmask != 0 && aux.fb1t))
+    // segment lists (thread-per-leaf path): gap-0 fallback leaves and gap-1 leaves whose
+    // pairs leave the domain, streamed by K7 MODE 5 / MODE 3 from the lists
+    if (aux.fb1t && (gap == 0 || (gap == 1 && dmask != 0)))
+    {
+        const int seg = gap == 0 ? 0 : 1;
+        const int k = atomicAdd(aux.fb_count + 2 + seg, 1);
+        if (k < aux.fbs_cap[seg])
+            aux.fbs[aux.fbs_off[seg] + k] = (int)i;
+        else
+            flag_err(aux.err, 2);
+    }
+    // listed: deep-gap leaves (K8, bands)
+    if (gap >= 2)
     {
         const int k = atomicAdd(aux.fb_count, 1);
         if (k < aux.fb_cap)
@@ -2049,6 +2063,32 @@ __device__ double rim_sum(const Geo& g, const Tree& tn, const Fld& F1, const Sch
     return s;
 }
 
+// out-of-line rim sum for the rarely taken boundary branch of K7 MODE 3
+template <int D>
+__device__ __noinline__ double rim_sum_cold(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int h,
+                                            int side, int bx0, int bx1, int by0, int by1, int leaf_li,
+                                            long long leaf_lin, const Aux& aux)
+{
+    return rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, leaf_li, leaf_lin, aux);
+}
+
+// the boundary rim sum of a gap-1 leaf as a by-value functor (params by address:
+// __grid_constant__, no copies)
+template <int D>
+struct RimCold {
+    const Geo* g;
+    const Tree* tn;
+    const Fld* F1;
+    const SchemeDev* sc;
+    const Aux* aux;
+    int x, y, li, lin;
+    __device__ __forceinline__ double operator()(int h, int side) const
+    {
+        return rim_sum_cold<D>(*g, *tn, *F1, sc, h, side, 2 * x, 2 * x + 2, D == 1 ? 0 : 2 * y, D == 1 ? 1 : 2 * y + 2,
+                               li, lin, *aux);
+    }
+};
+
 // The i-th finest-level cell of the E (side 0) or A (side 1) rim of the box
 // [bx0, bx1) x [by0, by1) for velocity (ex, ey), in rim_sum's loop order: at most one
 // x of the range contributes a whole column (the first or the last), the others one
@@ -2394,6 +2434,26 @@ __device__ __forceinline__ void gen_fb1t(const double* Fin, long long cap, const
 #undef GEN_FB1T
 }
 
+template <int EQ, int Q, class RS>
+__device__ __forceinline__ void gen_fb1t_rs(const double* Fin, long long cap, const double* Fj, long long capj,
+                                            unsigned ring, int x, int y, int nx, int ny, int nxj, int nyj, int per0,
+                                            int per1, unsigned mask, unsigned dmask, const RS& rs, long long s,
+                                            const double* sW, double scale, double (&f)[Q])
+{
+#define GEN_FB1TR(N) gen_fb1t_rs_EQ##N(Fin, cap, Fj, capj, ring, x, y, nx, ny, nxj, nyj, per0, per1, mask, dmask, rs, s, sW, scale, f);
+    if constexpr (EQ == 1 && Q == 2)
+        GEN_FB1TR(1)
+    else if constexpr (EQ == 2 && Q == 9)
+        GEN_FB1TR(2)
+    else if constexpr (EQ == 3 && Q == 4)
+        GEN_FB1TR(3)
+    else if constexpr (EQ == 4 && Q == 16)
+        GEN_FB1TR(4)
+    else if constexpr (EQ == 5 && Q == 9)
+        GEN_FB1TR(5)
+#undef GEN_FB1TR
+}
+
 // row i of the generated pattern-unrolled M f / M^-1 m
 template <int EQ, int Q, class CC>
 __device__ __forceinline__ double gen_collide_row(const CC& cc, bool inverse, int i, const double (&x)[Q])
@@ -2486,10 +2546,13 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
     const int nx = g.nx[li], ny = g.ny[li], nxj = g.nx[lj], nyj = g.ny[lj];
     const long long cap = g.cap[li], capj = g.cap[lj];
     const double scale = ldexp(1.0, D * (m - g.J1));
-    // list mode (thread-per-leaf gap-1 path on): only the listed boundary-rim leaves
-    const bool from_list = GEN && aux.fb1t;
-    const int nfb = from_list ? min(*aux.fb_count, (int)aux.fb_cap) : 0;
-    const long long nchunk = from_list ? (nfb + NT - 1) / NT : (nL + NT - 1) / NT;
+    // list mode (thread-per-leaf path on): the listed boundary-rim gap-1 leaves (segment 1)
+    const bool from_list = aux.fb1t != 0;
+    const int nfb = from_list ? min(aux.fb_count[3], (int)aux.fbs_cap[1]) : 0;
+    // list mode: one batch (32 leaves) per block and chunk, so the few, long-latency
+    // boundary-rim leaves spread over all blocks instead of queueing in a few
+    const int CH = from_list ? 32 : NT;
+    const long long nchunk = from_list ? (nfb + CH - 1) / CH : (nL + NT - 1) / NT;
     int qn = 0;
     long long ch = blockIdx.x;
     while (ch < nchunk || qn > 0)
@@ -2502,11 +2565,11 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
             bool isfb = false;
             if (from_list)
             {
-                if (sl < nfb)
+                const long long sll = ch * CH + tid;
+                if (tid < CH && sll < nfb)
                 {
-                    const int2 e = aux.fb_list[sl];
-                    isfb = e.x == m;
-                    lin = e.y;
+                    lin = aux.fbs[aux.fbs_off[1] + sll];
+                    isfb = true;
                 }
             }
             else if (sl < nL)
@@ -2816,32 +2879,42 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     int* myslot = &sSlot[0][threadIdx.x];
     // grid-stride over the leaf slots with the next slot's (index, kind) loaded one
     // iteration ahead, so the value gathers never wait on the slot list
+    // MODE 3 / 5 take their leaves from the fallback segment lists instead of the slots
+    const int* lst = nullptr;
+    int nItems = nL;
+    if constexpr (MODE == 3 || MODE == 5)
+    {
+        constexpr int seg = MODE == 5 ? 0 : 1;
+        lst = aux.fbs + aux.fbs_off[seg];
+        nItems = min(aux.fb_count[2 + seg], (int)aux.fbs_cap[seg]);
+    }
     const long long sstep = (long long)lvg_ * blockDim.x;
     long long s = (long long)lvb_ * blockDim.x + threadIdx.x;
-    int lin_next = s < nL ? tn.cells[li][s] : 0;
-    uint8_t kd_next = s < nL ? tn.skind[li][s] : 0;
-    for (; s < nL; s += sstep)
+    int lin_next = s < nItems ? (lst ? lst[s] : tn.cells[li][s]) : 0;
+    uint8_t kd_next = s < nItems ? (lst ? (uint8_t)(K_LEAF | K_FB) : tn.skind[li][s]) : 0;
+    for (; s < nItems; s += sstep)
     {
         const int lin = lin_next;
         const int vself = vl<D>(lin, ny, g.lny[li]);
         const uint8_t kd = kd_next;
-        if (s + sstep < nL)
+        if (s + sstep < nItems)
         {
-            lin_next = tn.cells[li][s + sstep];
-            kd_next = tn.skind[li][s + sstep];
+            lin_next = lst ? lst[s + sstep] : tn.cells[li][s + sstep];
+            kd_next = lst ? (uint8_t)(K_LEAF | K_FB) : tn.skind[li][s + sstep];
         }
         if (((kd & K_FB) != 0) != (MODE >= 1))
             continue;
-        constexpr bool fb = MODE == 1;
+        constexpr bool fb = MODE == 1 || MODE == 5;
         if (fb && gap == 1)
             continue; // streamed and collided by k_fb1 / MODE 2
         double f[Q];
-        if constexpr (MODE == 2)
+        if constexpr (MODE == 2 || MODE == 3)
         {
-            // gap-1 fallback leaf without domain-leaving pairs, one thread per leaf:
-            // table + details of the finest-leaf rim cells (Decision D.13b), the same
-            // operands and order as k_fb1 (which takes the boundary rim leaves, listed)
-            if (fl.fbd[li][vself] != 0)
+            // gap-1 fallback leaf, one thread per leaf: table + details of the finest-leaf
+            // rim cells (Decision D.13b), the same operands and order as k_fb1.  MODE 2: the
+            // leaves without domain-leaving pairs (slot scan); MODE 3: the listed others,
+            // whose domain-leaving pairs take the boundary rim sum (rim_sum)
+            if (MODE == 2 && fl.fbd[li][vself] != 0)
                 continue;
             int x, y;
             lin2xy_l<D>(lin, ny, g.lny[li], x, y);
@@ -2872,8 +2945,15 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
                 if (kj[xy2lin<D>(xr, yr, nyj)] & K_LEAF)
                     ring |= 1u << r;
             }
-            gen_fb1t<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], ring, x, y, nx, ny, nxj, nyj, per0, per1,
-                            fl.fbm[li][vself], vself, sW, scale, f);
+            if constexpr (MODE == 2)
+                gen_fb1t<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], ring, x, y, nx, ny, nxj, nyj, per0, per1,
+                                fl.fbm[li][vself], vself, sW, scale, f);
+            else
+            {
+                const RimCold<D> rs{&g, &tn, &F1, scg, &aux, x, y, li, lin};
+                gen_fb1t_rs<EQ, Q>(Fin, cap, F1.f[li + 1], g.cap[li + 1], ring, x, y, nx, ny, nxj, nyj, per0, per1,
+                                   fl.fbm[li][vself], fl.fbd[li][vself], rs, vself, sW, scale, f);
+            }
         }
         else if (fb && gap >= kDeepGap)
         {
@@ -3302,6 +3382,8 @@ struct mrlbm_ctx {
     SchemeDev* sch = nullptr;
     int* err = nullptr;
     int* fbc = nullptr;
+    int* fbs = nullptr; // fallback segment lists (Aux::fbs)
+    long long fbs_off[2]{}, fbs_cap[2]{};
     int2* fbl = nullptr;
     unsigned* fbm = nullptr;
     unsigned* fbdm = nullptr;
@@ -3329,6 +3411,7 @@ struct mrlbm_ctx {
     bool use_graph = true;
     bool use_gen = false; // generated stream / collision path (built-in velocity sets)
     bool use_fb1t = true; // gap-1 fallback leaves thread per leaf (K7 MODE 2) instead of k_fb1; MRLBM_NO_FB1T=1 turns it off
+    bool rim_tpl = false; // boundary-rim gap-1 leaves thread per leaf too (K7 MODE 3, MRLBM_RIM_TPL=1) instead of k_fb1 (list)
     // K1+K2 fused per level (MRLBM_FUSE_PD=1): measured slower than the separate
     // kernels (re-projecting the internal stencil neighbours costs more than the
     // second read of the children), so off by default
@@ -3443,6 +3526,12 @@ Aux aux_of(mrlbm_ctx* c)
     a.umask = c->umaskd;
     a.frc = c->frc;
     a.fb1t = (c->use_fb1t && c->use_gen) ? 1 : 0;
+    a.fbs = c->fbs;
+    for (int k = 0; k < 2; ++k)
+    {
+        a.fbs_off[k] = c->fbs_off[k];
+        a.fbs_cap[k] = c->fbs_cap[k];
+    }
     for (int i = 0; i < kL; ++i)
     {
         a.frc_off[i] = 2 * c->frc_off[i];
@@ -3678,29 +3767,52 @@ void enqueue_step(mrlbm_ctx* c)
     // default kernels carry no extra code
     constexpr bool kObs = EQ == MRLBM_EQ_NS_D2Q9 && D == 2;
     const bool frc = kObs && c->frc != nullptr;
+    // thread-per-leaf fallback path (generated code): gap-1 fallback leaves in K7 MODE 2
+    // (slot scan) and MODE 3 (listed boundary-rim ones), gap-0 fallback leaves in MODE 5
+    // (listed); otherwise k_fb1 scans the gap-1 leaves and MODE 1 all levels
     const bool tpl = GEN && c->use_fb1t;
     if (c->J1 > c->J0)
     {
+        if (!tpl)
         {
-            // list mode (tpl) has little work: one block per SM
-            const int nbf = tpl ? 148 : c->grid_cap;
             c->kcount++;
             if (frc)
-                k_fb1<D, Q, BS, EQ, GEN, kObs><<<nbf, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+                k_fb1<D, Q, BS, EQ, GEN, kObs><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
             else
-                k_fb1<D, Q, BS, EQ, GEN><<<nbf, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+                k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
             kmark(c, "k_fb1", -1);
         }
+        else if (!c->rim_tpl)
+        {
+            // the listed boundary-rim gap-1 leaves: Q warps per batch, compact generic loops
+            c->kcount++;
+            if (frc)
+                k_fb1<D, Q, BS, EQ, false, kObs><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+            else
+                k_fb1<D, Q, BS, EQ, false><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+            kmark(c, "k_fb1_rim", -1);
+        }
         if constexpr (GEN)
-        if (c->use_fb1t)
+        if (tpl)
         {
             LGrid l2 = make_lgrid(c, c->J1 - 1, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
-            c->kcount++;
+            c->kcount += 2;
             if (frc)
                 k_stream_collide<D, Q, BS, EQ, GEN, 2, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
             else
                 k_stream_collide<D, Q, BS, EQ, GEN, 2, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
             kmark(c, "k_fb1t", -1);
+            if (c->rim_tpl)
+            {
+                LGrid l3 = make_lgrid(c, c->J1 - 1, c->J1 - 1, [&](int) { return 148; }, &nb);
+                if (frc)
+                    k_stream_collide<D, Q, BS, EQ, GEN, 3, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l3, aux, cc);
+                else
+                    k_stream_collide<D, Q, BS, EQ, GEN, 3, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l3, aux, cc);
+                kmark(c, "k_fb1_rim", -1);
+            }
+            else
+                c->kcount--;
         }
     }
     {
@@ -3735,13 +3847,30 @@ void enqueue_step(mrlbm_ctx* c)
                 k_stream_collide<D, Q, BS, EQ, GEN, 0, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
             kmark(c, "k_stream_collide", -1);
         }
-        LGrid lf = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 8, 256); }, &nb);
-        c->kcount++;
-        if (frc)
-            k_stream_collide<D, Q, BS, EQ, GEN, 1, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
-        else
-            k_stream_collide<D, Q, BS, EQ, GEN, 1, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
-        kmark(c, "k_stream_collide_fb", -1);
+        // MODE 1: deep-gap fallback leaves (collide K8's output) by slot scan, and with
+        // !tpl also the gap-0 ones; with tpl the gap-0 ones come from their list (MODE 5)
+        const int mtop = tpl ? c->J1 - 2 : c->J1;
+        if (mtop >= c->J0)
+        {
+            LGrid lf = make_lgrid(c, c->J0, mtop, [&](int li) { return grid_for(c, g.cap[li] / 8, 256); }, &nb);
+            c->kcount++;
+            if (frc)
+                k_stream_collide<D, Q, BS, EQ, GEN, 1, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
+            else
+                k_stream_collide<D, Q, BS, EQ, GEN, 1, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
+            kmark(c, "k_stream_collide_fb", -1);
+        }
+        if constexpr (GEN)
+        if (tpl)
+        {
+            LGrid l5 = make_lgrid(c, c->J1, c->J1, [&](int) { return 148; }, &nb);
+            c->kcount++;
+            if (frc)
+                k_stream_collide<D, Q, BS, EQ, GEN, 5, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l5, aux, cc);
+            else
+                k_stream_collide<D, Q, BS, EQ, GEN, 5, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l5, aux, cc);
+            kmark(c, "k_stream_collide_fb0", -1);
+        }
     }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
     if (c->frc)
@@ -3969,7 +4098,14 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         CU(cudaMalloc(&ctx->fbl, sizeof(int2) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbm, sizeof(unsigned) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbdm, sizeof(unsigned) * ctx->fbcap));
-        CU(cudaMalloc(&ctx->fbc, sizeof(int) * 2));
+        CU(cudaMalloc(&ctx->fbc, sizeof(int) * 4));
+        CU(cudaMemset(ctx->fbc, 0, sizeof(int) * 4));
+        // segment lists: capacity = the level's cell count (J1 for gap 0, J1-1 for gap 1)
+        ctx->fbs_cap[0] = ctx->geo.cap[ctx->nlev - 1];
+        ctx->fbs_cap[1] = ctx->nlev > 1 ? ctx->geo.cap[ctx->nlev - 2] : 0;
+        ctx->fbs_off[0] = 0;
+        ctx->fbs_off[1] = ctx->fbs_cap[0];
+        CU(cudaMalloc(&ctx->fbs, sizeof(int) * (ctx->fbs_cap[0] + ctx->fbs_cap[1] + 1)));
         CU(cudaMalloc(&ctx->err, sizeof(int) * 4));
         CU(cudaMemset(ctx->err, 0, sizeof(int) * 4));
         CU(cudaMalloc(&ctx->upd, sizeof(long long)));
@@ -4124,6 +4260,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     }
     ctx->use_gen = builtin_velocities(sc) && ctx->gen_ok && std::getenv("MRLBM_NO_GEN") == nullptr;
     ctx->use_fb1t = std::getenv("MRLBM_NO_FB1T") == nullptr;
+    ctx->rim_tpl = std::getenv("MRLBM_RIM_TPL") != nullptr;
     ctx->fuse_pd = std::getenv("MRLBM_FUSE_PD") != nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
@@ -4693,6 +4830,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->ld_bad);
     cudaFree(ctx->err);
     cudaFree(ctx->fbc);
+    cudaFree(ctx->fbs);
     cudaFree(ctx->fbl);
     cudaFree(ctx->fbm);
     cudaFree(ctx->fbdm);
