@@ -1958,26 +1958,33 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
         face = y < 0 ? 2 : 3;
     if (face < 0)
     {
+        // the kind and the materialised value are loaded together (the value is
+        // speculative: used only when the cell is materialised), one latency
         const int lin = mr_lin<D>(g, g.J1, x, y);
-        if (tn.kind[lj][lin])
-            return S.f[lj][(long long)h * g.cap[lj] + mr_vix<D>(g, g.J1, x, y)];
+        const uint8_t kself = tn.kind[lj][lin];
+        const double vself = S.f[lj][(long long)h * g.cap[lj] + mr_vix<D>(g, g.J1, x, y)];
+        if (kself)
+            return vself;
         // not materialised (rims of gap-1 leaves): one zero-detail prediction from
-        // level J1-1, same operands and order as k_virtual would use
+        // level J1-1, same operands and order as k_virtual would use; the stencil's
+        // kinds and values are again loaded together
         const int lp = lj - 1;
         const int xc = mr_coord(x, nx, g.per0), yc = D == 2 ? mr_coord(y, ny, g.per1) : 0;
         const int px = xc >> 1, py = yc >> 1;
         constexpr int NS = D == 1 ? 3 : 9;
         double sv[NS];
+        bool ok = true;
+#pragma unroll
         for (int o = 0; o < NS; ++o)
         {
             const int ox = D == 1 ? o - 1 : o / 3 - 1, oy = D == 1 ? 0 : o % 3 - 1;
-            const int pl = mr_lin<D>(g, g.J1 - 1, px + ox, py + oy);
-            if (!tn.kind[lp][pl])
-            {
-                flag_err(aux.err, 0);
-                return 0.0;
-            }
+            ok = ok && tn.kind[lp][mr_lin<D>(g, g.J1 - 1, px + ox, py + oy)] != 0;
             sv[o] = S.f[lp][(long long)h * g.cap[lp] + mr_vix<D>(g, g.J1 - 1, px + ox, py + oy)];
+        }
+        if (!ok)
+        {
+            flag_err(aux.err, 0);
+            return 0.0;
         }
         return mr_predict<D>(sv, xc & 1, yc & 1);
     }
