@@ -1151,11 +1151,10 @@ __global__ void k_fallback_v(const __grid_constant__ Geo g, const __grid_constan
     {
         V16 k;
         k.v = reinterpret_cast<const uint4*>(fl.kind[li])[c];
-        bool any = false;
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            any = any || k.b[j] == K_LEAF;
-        if (!any)
+        // any byte == K_LEAF (a plain leaf), four bytes per compare
+        const unsigned anyw = __vcmpeq4(k.v.x, 0x01010101u * K_LEAF) | __vcmpeq4(k.v.y, 0x01010101u * K_LEAF) |
+                              __vcmpeq4(k.v.z, 0x01010101u * K_LEAF) | __vcmpeq4(k.v.w, 0x01010101u * K_LEAF);
+        if (!anyw)
             continue;
         const int lin0 = (int)(c * 16);
         const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
@@ -1660,14 +1659,20 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(const __grid_c
     uint8_t b[16];
     load16_blk(g, li, kind, base, n, b);
     const bool blk = blk_order(g, li);
+    // the kinds are exclusive bits: count them four bytes at a time
     int c[3] = {0, 0, 0};
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
     {
-        c[0] += b[j] & K_LEAF ? 1 : 0;
-        c[1] += b[j] & K_INT ? 1 : 0;
-        c[2] += b[j] & K_VIRT ? 1 : 0;
+        unsigned wv[4];
+        memcpy(wv, b, 16);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+        {
+            c[0] += __popc(wv[k] & 0x01010101u * K_LEAF);
+            c[1] += __popc(wv[k] & 0x01010101u * K_INT);
+            c[2] += __popc(wv[k] & 0x01010101u * K_VIRT);
+        }
     }
+    const bool mine = (c[0] | c[1] | c[2]) != 0;
     int pre[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -1703,16 +1708,19 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(const __grid_c
     }
     pos[1] += tot[0];
     pos[2] += tot[0] + tot[1];
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
+    if (mine)
     {
-        const long long i = base + j;
-        const int ct = cat_of(b[j]);
-        if (i < n && ct < 3)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
         {
-            const int sl = pos[ct]++;
-            sCells[sl] = blk ? blk_lin(g, li, i) : (int)i;
-            sKind[sl] = b[j];
+            const long long i = base + j;
+            const int ct = cat_of(b[j]);
+            if (i < n && ct < 3)
+            {
+                const int sl = pos[ct]++;
+                sCells[sl] = blk ? blk_lin(g, li, i) : (int)i;
+                sKind[sl] = b[j];
+            }
         }
     }
     __syncthreads();

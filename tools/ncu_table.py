@@ -26,7 +26,7 @@ def main():
         rd, wr = g(r, "dram__bytes_read.sum"), g(r, "dram__bytes_write.sum")
         req = g(r, "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")
         sec = g(r, "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum")
-        print(f"{d:8.1f}us {r[ix['Kernel Name']][:34]:34s} rd {rd:7.1f} wr {wr:6.1f} MB {(rd + wr) / d * 1e-3:5.2f} TB/s "
+        print(f"{d:8.1f}us {r[ix['Kernel Name']][:34]:34s} rd {rd:7.1f} wr {wr:6.1f} MB {(rd + wr) / d:5.2f} TB/s "
               f"iss {g(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active'):4.1f} "
               f"wrp {g(r, 'sm__warps_active.avg.pct_of_peak_sustained_active'):4.1f} "
               f"L1h {g(r, 'l1tex__t_sector_hit_rate.pct'):4.1f} L2h {g(r, 'lts__t_sector_hit_rate.pct'):4.1f} "
