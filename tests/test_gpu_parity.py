@@ -87,11 +87,12 @@ def test_generic_table_path_parity(cid, J, monkeypatch):
     ora.close()
 
 
-@pytest.mark.parametrize("env", ["MRLBM_FUSE_PD", "MRLBM_NO_FB1T"])
+@pytest.mark.parametrize("env", ["MRLBM_FUSE_PD", "MRLBM_NO_FB1T", "MRLBM_RIM_TPL"])
 @pytest.mark.parametrize("cid,J", [(3, 6), (4, 6), (5, 7)])
 def test_kernel_variant_parity(cid, J, env, monkeypatch):
-    """The alternative kernel schedules (fused projection + details; gap-1 fallback
-    leaves in the block kernel k_fb1 only) stay bit-identical to the oracle."""
+    """The alternative kernel schedules stay bit-identical to the oracle: fused
+    projection + details; all gap-1 fallback leaves in the block kernel k_fb1 (slot
+    scan, no segment lists); boundary-rim gap-1 leaves thread per leaf (K7 MODE 3)."""
     monkeypatch.setenv(env, "1")
     sc, rc, gpu, ora = make_pair(cid, J)
     for k in range(12):
