@@ -2165,7 +2165,7 @@ __device__ __forceinline__ int rim_cell(int side, int ex, int ey, int bx0, int b
 // table / rim order through shuffles, so the arithmetic is rim_sum's.  Writes
 // post-stream populations into F0; K7 collides them.
 template <int D>
-__global__ void __launch_bounds__(256) k_stream_fallback(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld F0, const __grid_constant__ Fld F1, const __grid_constant__ Flags fl, const SchemeDev* sc,
+__global__ void __launch_bounds__(256, 4) k_stream_fallback(const __grid_constant__ Geo g, const __grid_constant__ Tree tn, const __grid_constant__ Fld F0, const __grid_constant__ Fld F1, const __grid_constant__ Flags fl, const SchemeDev* sc,
                                                          Aux aux)
 {
     const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
