@@ -807,52 +807,52 @@ __global__ void k_kinds(const __grid_constant__ Geo g, const __grid_constant__ F
 // level above) and W = 1 at the finest level (the E/A rims themselves).
 // One warp per fallback leaf.
 template <int D>
-__device__ __forceinline__ long long band_count(int side, int W)
+__device__ __forceinline__ int band_count(int side, int W)
 {
-    const long long S = side + 2 * W;
+    const int S = side + 2 * W;
     if (D == 1)
         return side <= 2 * W ? S : 4 * W;
-    return side <= 2 * W ? S * S : S * S - (long long)(side - 2 * W) * (side - 2 * W);
+    return side <= 2 * W ? S * S : S * S - (side - 2 * W) * (side - 2 * W);
 }
 
 template <int D>
-__device__ __forceinline__ void band_cell(long long t, int side, int W, int bx0, int by0, int& x, int& y)
+__device__ __forceinline__ void band_cell(int t, int side, int W, int bx0, int by0, int& x, int& y)
 {
     const int S = side + 2 * W;
     y = 0;
     if (D == 1)
     {
         if (side <= 2 * W)
-            x = bx0 - W + (int)t;
+            x = bx0 - W + t;
         else
-            x = t < 2 * W ? bx0 - W + (int)t : bx0 + side - W + (int)(t - 2 * W);
+            x = t < 2 * W ? bx0 - W + t : bx0 + side - W + (int)(t - 2 * W);
         return;
     }
     if (side <= 2 * W)
     {
-        x = bx0 - W + (int)(t / S);
-        y = by0 - W + (int)(t % S);
+        x = bx0 - W + (t / S);
+        y = by0 - W + (t % S);
         return;
     }
-    const long long top = 2LL * W * S;
-    const long long mid = (long long)(side - 2 * W) * 4 * W;
+    const int top = 2 * W * S;
+    const int mid = (side - 2 * W) * 4 * W;
     if (t < top)
     {
-        x = bx0 - W + (int)(t / S);
-        y = by0 - W + (int)(t % S);
+        x = bx0 - W + (t / S);
+        y = by0 - W + (t % S);
     }
     else if (t < top + mid)
     {
-        const long long u = t - top;
-        x = bx0 + W + (int)(u / (4 * W));
-        const int c = (int)(u % (4 * W));
+        const int u = t - top;
+        x = bx0 + W + (u / (4 * W));
+        const int c = (u % (4 * W));
         y = c < 2 * W ? by0 - W + c : by0 + side - W + (c - 2 * W);
     }
     else
     {
-        const long long u = t - top - mid;
-        x = bx0 + side - W + (int)(u / S);
-        y = by0 - W + (int)(u % S);
+        const int u = t - top - mid;
+        x = bx0 + side - W + (u / S);
+        y = by0 - W + (u % S);
     }
 }
 
@@ -878,8 +878,8 @@ __global__ void __launch_bounds__(256) k_band(const __grid_constant__ Geo g, con
             const int nx = g.nx[li], ny = g.ny[li];
             const int side = 1 << (m - l);
             const int W = m == g.J1 ? 1 : 2;
-            const long long total = band_count<D>(side, W);
-            for (long long t = lane; t < total; t += 32)
+            const int total = band_count<D>(side, W); // < 2^31: side <= 2^(J1 - J0)
+            for (int t = lane; t < total; t += 32)
             {
                 int x, y;
                 band_cell<D>(t, side, W, kx * side, ky * side, x, y);
