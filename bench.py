@@ -230,13 +230,17 @@ def bench_product(args):
     sprof.set_profiling(True)
     nprof = args.steps
     phase_tot = [0.0] * len(PHASES)
-    stream_bytes_tot, model_bytes_tot = 0, 0
+    stream_bytes_tot, model_bytes_tot, fin_bytes_tot = 0, 0, 0
     for _ in range(nprof):
         sp = sprof.step(1)
         for i in range(len(PHASES)):
             phase_tot[i] += sp.ms_phase[i]
         stream_bytes_tot += sp.bytes_stream      # per-step algorithmic bytes
         model_bytes_tot += sp.bytes_model
+        # finest-level table stream + collision (K7 gap 0): read f* of the level's leaves and
+        # ghosts, write the leaves (boundary-rim fallback leaves are a negligible part)
+        nl, nv = int(sp.leaves[sp.levels - 1]), int(sp.virtual_cells[sp.levels - 1])
+        fin_bytes_tot += 8 * sc.q * (2 * nl + nv)
     kern_prof = sprof.profile_text()
     sprof.close()
     phase_ms = {p: phase_tot[i] / nprof for i, p in enumerate(PHASES)}
@@ -244,6 +248,8 @@ def bench_product(args):
     for (kname, lv), (kms, kn) in kern_prof.items():
         if kname.startswith(("k_stream", "k_fb1")):
             stream_kernels[kname] = stream_kernels.get(kname, 0.0) + kms / nprof
+    fin_ms = kern_prof.get(("k_stream_collide", rc.j_max), (0.0, 0))[0] / nprof
+    fin_bytes = fin_bytes_tot / nprof
     dom = max(phase_ms, key=phase_ms.get)
     peak, peak_kind = load_peaks()
     stream_bytes = stream_bytes_tot / nprof
@@ -337,6 +343,10 @@ def bench_product(args):
                          "timing": "CUDA events per kernel on the context stream over the same K steps as the "
                                    "timed window (eager replay from the post-warm-up state)",
                          "kernels_ms_per_step": stream_kernels},
+            "kernel_roofline": {"kernel": "K7 finest level (gap-0 table stream + MRT collision), per launch",
+                                "algorithmic_bytes": fin_bytes, "ms": fin_ms,
+                                "achieved_gbs": fin_bytes / (fin_ms / 1e3) / 1e9 if fin_ms > 0 else 0.0,
+                                "frac": (fin_bytes / (fin_ms / 1e3) / 1e9 / peak) if fin_ms > 0 else 0.0},
             "step_roofline": {"bytes_model_per_step": model_bytes,
                               "achieved_gbs": model_bytes / (ms_max / args.steps / 1e3) / 1e9,
                               "frac": model_bytes / (ms_max / args.steps / 1e3) / 1e9 / peak},
