@@ -219,6 +219,8 @@ def bench_product(args):
     value = utot / (ms_max / 1e3)
     state_bytes = 8 * sc.q * sum(int(st.leaves[i]) for i in range(st.levels))
 
+    end_counts = {lv: s.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1)}
+
     # ---- phase breakdown over the SAME K steps as the timed window: a second context
     # restarts from the post-warm-up state (bit-identical evolution) with eager launches
     # and CUDA events after every phase / kernel on the context's stream (~5-9 % slower
@@ -288,9 +290,11 @@ def bench_product(args):
         pi_[...] = ix
         pf_[...] = ff
         snap_p[lv] = (pi_, pf_)
-    # read-back buffers: flat pinned arrays per level, twice the snapshot size (mesh growth)
-    out_flat = {lv: (pinned_like(np.zeros(2 * ix.size + 16, np.int32)), pinned_like(np.zeros(2 * ff.size + 16)))
-                for lv, (ix, ff) in snap.items()}
+    # read-back buffers: pinned, sized by the level counts the timed run ended with (the
+    # e2e context replays the same deterministic K steps from the same state)
+    out_flat = {lv: (pinned_like(np.zeros(sc.d * end_counts[lv] + 16, np.int32)),
+                     pinned_like(np.zeros(sc.q * end_counts[lv] + 16)))
+                for lv in snap}
     s2 = Solver(sc, rc)
     h2d = sum(v[0].nbytes + v[1].nbytes for v in snap_p.values())
     barrier()

@@ -4106,7 +4106,13 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
             CU(cudaMalloc(&ctx->fbdd[li], sizeof(unsigned) * n));
             ctx->ntiles[li] = (n + kTile - 1) / kTile;
             CU(cudaMalloc(&ctx->tiles[li], sizeof(int) * 3 * ctx->ntiles[li]));
+            // load / read-back staging (coordinates and linear indices of one level),
+            // allocated with the context so the first load or read pays no allocation
+            CU(cudaMalloc(&ctx->ld_idx[li], sizeof(int32_t) * ctx->D * n));
+            CU(cudaMalloc(&ctx->ld_lin[li], sizeof(int32_t) * n));
         }
+        CU(cudaMalloc(&ctx->ld_bad, sizeof(int)));
+        CU(cudaMalloc(&ctx->rdcnt, sizeof(int) * 4));
         ctx->fbcap = total_cells;
         CU(cudaMalloc(&ctx->dirty_d, sizeof(uint8_t*) * kL));
         CU(cudaMemcpy(ctx->dirty_d, ctx->keep, sizeof(uint8_t*) * kL, cudaMemcpyHostToDevice));
