@@ -670,6 +670,70 @@ __global__ void k_enlarge(const __grid_constant__ Geo g, const __grid_constant__
     }
 }
 
+union V16 {
+    uint4 v;
+    uint8_t b[16];
+};
+
+// same as a gather over a dense level (2D, 16 cells of a row per thread): rn(c) |=
+// keep(c) | OR over the emask offsets o of keep(c - o), wrap on periodic axes, nothing
+// from outside the domain otherwise -- the set k_enlarge scatters, without per-parent
+// scattered byte stores
+__global__ void k_enlarge_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl,
+                            const __grid_constant__ LGrid lg_, unsigned emask)
+{
+    LSETUP;
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = g.ny[li];
+    const long long nch = (long long)nx * ny / 16;
+    const uint8_t* keep = fl.keep[li];
+    uint8_t* rn = fl.rn[li];
+    LGRID_STRIDE(c, 0, nch)
+    {
+        const int lin0 = (int)(c * 16);
+        const int x = lin0 >> g.lny[li], y0 = lin0 & (ny - 1);
+        // keep of rows x-1, x, x+1 over columns y0-1 .. y0+16
+        uint8_t w[3][18];
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+        {
+            int xr = x + r - 1;
+            const bool ok = (xr >= 0 && xr < nx) || g.per0;
+            xr = mr_coord(xr, nx, 1);
+            V16 v;
+            v.v = ok ? reinterpret_cast<const uint4*>(keep + (long long)xr * ny)[y0 >> 4] : make_uint4(0, 0, 0, 0);
+            any = any || (v.v.x | v.v.y | v.v.z | v.v.w);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                w[r][j + 1] = v.b[j];
+            const int yl = y0 - 1, yr = y0 + 16;
+            w[r][0] = (ok && (yl >= 0 || g.per1)) ? keep[(long long)xr * ny + mr_coord(yl, ny, 1)] : 0;
+            w[r][17] = (ok && (yr < ny || g.per1)) ? keep[(long long)xr * ny + mr_coord(yr, ny, 1)] : 0;
+            any = any || w[r][0] || w[r][17];
+        }
+        if (!any)
+            continue;
+        V16 o;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+        {
+            uint8_t v = w[1][j + 1];
+#pragma unroll
+            for (int b = 0; b < 9; ++b)
+                if ((emask >> b) & 1u)
+                {
+                    const int ox = b / 3 - 1, oy = b % 3 - 1;
+                    v |= w[1 - ox][j + 1 - oy];
+                }
+            o.b[j] = v;
+        }
+        uint4* dst = reinterpret_cast<uint4*>(rn) + c;
+        const uint4 cur = *dst;
+        *dst = make_uint4(cur.x | o.v.x, cur.y | o.v.y, cur.z | o.v.z, cur.w | o.v.w);
+    }
+}
+
 // grading G: for p refined at level m, its 3^D box must be in R_m, i.e. the
 // parents of the box at level m-1 are refined (one fine->coarse sweep, Decision D.7)
 template <int D>
@@ -986,10 +1050,6 @@ __global__ void k_ghost(const __grid_constant__ Geo g, const __grid_constant__ F
     for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < (nchunks);                    \
          c += (long long)gridDim.x * blockDim.x)
 
-union V16 {
-    uint4 v;
-    uint8_t b[16];
-};
 
 __global__ void k_kinds_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
 {
@@ -3683,13 +3743,27 @@ void enqueue_step(mrlbm_ctx* c)
     // K3 closure, enlargement, grading
     for (int m = c->J1 - 1; m > c->J0; --m)
         { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);  kmark(c, "k_closure", m); }
-    {
-        LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
-        c->kcount++;
-        k_enlarge<D><<<nb, T, 0, s>>>(g, to, fl, c->sch, lg, c->emask);
-        kmark(c, "k_enlarge", -1);
-    }
     auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
+    {
+        // H(a): levels [J0, me) scatter from the kept parents, [me, J1) gather 16 cells per thread
+        int me = c->J1;
+        for (int m = c->J1 - 1; m >= c->J0 && vec_ok(m); --m)
+            me = m;
+        if (me > c->J0)
+        {
+            LGrid lg = make_lgrid(c, c->J0, me - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
+            c->kcount++;
+            k_enlarge<D><<<nb, T, 0, s>>>(g, to, fl, c->sch, lg, c->emask);
+            kmark(c, "k_enlarge", -1);
+        }
+        if (me < c->J1)
+        {
+            LGrid lg = make_lgrid(c, me, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li] / 16, T); }, &nb);
+            c->kcount++;
+            k_enlarge_v<<<nb, T, 0, s>>>(g, fl, lg, c->emask);
+            kmark(c, "k_enlarge", -1);
+        }
+    }
     for (int m = c->J1 - 1; m > c->J0; --m)
     {
         c->kcount++;
