@@ -675,6 +675,44 @@ union V16 {
     uint8_t b[16];
 };
 
+// T closure as a gather (2D, 16 parents of a row per thread): keep(p) |= OR of the
+// keep flags of p's 2x2 children at level m (keep is only ever set on internal nodes)
+__global__ void k_closure_v(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, int m)
+{
+    const int li = m - g.J0; // children level
+    const int nyp = g.ny[li - 1], ny = g.ny[li];
+    const long long nch = (long long)g.nx[li - 1] * nyp / 16;
+    const uint8_t* kc = fl.keep[li];
+    uint8_t* kp = fl.keep[li - 1];
+    GRID_STRIDE(c, 0, nch)
+    {
+        const int lin0 = (int)(c * 16);
+        const int px = lin0 >> g.lny[li - 1], py0 = lin0 & (nyp - 1);
+        const uint4* r0 = reinterpret_cast<const uint4*>(kc + (long long)(2 * px) * ny + 2 * py0);
+        const uint4* r1 = reinterpret_cast<const uint4*>(kc + (long long)(2 * px + 1) * ny + 2 * py0);
+        V16 a0, a1, b0, b1;
+        a0.v = r0[0];
+        a1.v = r0[1];
+        b0.v = r1[0];
+        b1.v = r1[1];
+        if (((a0.v.x | a0.v.y | a0.v.z | a0.v.w) | (a1.v.x | a1.v.y | a1.v.z | a1.v.w) |
+             (b0.v.x | b0.v.y | b0.v.z | b0.v.w) | (b1.v.x | b1.v.y | b1.v.z | b1.v.w)) == 0)
+            continue;
+        V16 o;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+        {
+            const V16& A = j < 8 ? a0 : a1;
+            const V16& B = j < 8 ? b0 : b1;
+            const int k = 2 * (j & 7);
+            o.b[j] = A.b[k] | A.b[k + 1] | B.b[k] | B.b[k + 1];
+        }
+        uint4* dst = reinterpret_cast<uint4*>(kp) + c;
+        const uint4 cur = *dst;
+        *dst = make_uint4(cur.x | o.v.x, cur.y | o.v.y, cur.z | o.v.z, cur.w | o.v.w);
+    }
+}
+
 // same as a gather over a dense level (2D, 16 cells of a row per thread): rn(c) |=
 // keep(c) | OR over the emask offsets o of keep(c - o), wrap on periodic axes, nothing
 // from outside the domain otherwise -- the set k_enlarge scatters, without per-parent
@@ -3741,9 +3779,16 @@ void enqueue_step(mrlbm_ctx* c)
     }
     phase_mark(c, 2);
     // K3 closure, enlargement, grading
-    for (int m = c->J1 - 1; m > c->J0; --m)
-        { c->kcount++; k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);  kmark(c, "k_closure", m); }
     auto vec_ok = [&](int m) { return D == 2 && g.ny[m - c->J0] % 16 == 0 && g.lny[m - c->J0] >= 0; };
+    for (int m = c->J1 - 1; m > c->J0; --m)
+    {
+        c->kcount++;
+        if (vec_ok(m - 1))
+            k_closure_v<<<grid_for(c, g.cap[m - 1 - c->J0] / 16, T), T, 0, s>>>(g, fl, m);
+        else
+            k_closure<D><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, fl, m);
+        kmark(c, "k_closure", m);
+    }
     {
         // H(a): levels [J0, me) scatter from the kept parents, [me, J1) gather 16 cells per thread
         int me = c->J1;
