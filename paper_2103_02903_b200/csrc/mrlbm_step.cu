@@ -2633,6 +2633,10 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
     const int m = g.J1 - 1, li = m - g.J0, lj = li + 1;
     if (li < 0)
         return;
+    // list mode: blocks beyond the listed leaves (one 32-leaf chunk per block in the first
+    // sweep) leave before the shared-memory prologue
+    if (aux.fb1t && (long long)blockIdx.x * 32 >= min(aux.fb_count[3], (int)aux.fbs_cap[1]))
+        return;
     {
         // gap-1 table weights in table order, scheme constants
         const int base = aux.tidx[1 * 2 * Q].x;
