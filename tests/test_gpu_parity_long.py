@@ -52,3 +52,17 @@ def test_full_size_config5_invariants():
     assert np.isfinite(f).all()
     s.close()
     assert area == 2.0
+
+
+def test_parity_full_size_config5():
+    """The bench configuration itself (config 5, levels 2..12, 8192 x 4096 finest,
+    33.5 M initial leaves): two adaptive steps, GPU vs oracle, bit-exact on every level."""
+    sc, rc, gpu, ora = make_pair(5, 12)
+    for k in range(2):
+        gpu.step(1)
+        ora.step(1)
+        rel, bitwise, total = compare(gpu, ora, rc, f"config 5 J=12 step {k}")
+        assert rel <= 1e-12 and bitwise
+    print(f"config 5 J=12: 2 steps bit-exact, {total} leaves")
+    gpu.close()
+    ora.close()
