@@ -1808,6 +1808,11 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(const __grid_c
     pos[2] += tot[0] + tot[1];
     if (mine)
     {
+        // row-major index of the first cell (block row of 4 sibling blocks when the
+        // fast path applies): the others follow by constant offsets, no division per cell
+        const int nyl = g.ny[li];
+        const bool fast = blk && ((nyl >> 1) & 3) == 0 && base + 16 <= n;
+        const int lin0 = fast ? blk_lin(g, li, base) : 0;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
         {
@@ -1816,7 +1821,9 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(const __grid_c
             if (i < n && ct < 3)
             {
                 const int sl = pos[ct]++;
-                sCells[sl] = blk ? blk_lin(g, li, i) : (int)i;
+                // block k = j / 4, child c = j % 4: (2gx + (c >> 1), 2(gy0 + k) + (c & 1))
+                sCells[sl] = fast ? lin0 + ((j & 3) >> 1) * nyl + 2 * (j >> 2) + (j & 1)
+                                  : (blk ? blk_lin(g, li, i) : (int)i);
                 sKind[sl] = b[j];
             }
         }
