@@ -1688,6 +1688,9 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(const __grid_con
 
 __global__ void k_tile_scan_ml(const __grid_constant__ Geo g, const __grid_constant__ TileP tp, const __grid_constant__ Tree tn, const __grid_constant__ LGrid lg_)
 {
+    // one block per level: per-thread sums of a contiguous tile range, a block-wide
+    // exclusive scan of those sums (warp shuffles + warp totals), then the per-tile
+    // exclusive offsets; the level totals go to cnt
     LSETUP;
     (void)lvb_;
     (void)lvg_;
@@ -1695,30 +1698,57 @@ __global__ void k_tile_scan_ml(const __grid_constant__ Geo g, const __grid_const
     const int ntiles = (int)((g.cap[li] + kTile - 1) / kTile);
     int* tile_counts = tp.t[li];
     int* cnt = tn.cnt + li * 4;
-    __shared__ int part[3][1024];
+    __shared__ int wsum[3][32];
     const int T = blockDim.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = T >> 5;
     const int per = (ntiles + T - 1) / T;
     const int b = threadIdx.x * per, e = min(ntiles, b + per);
     int loc[3] = {0, 0, 0};
     for (int t = b; t < e; ++t)
         for (int k = 0; k < 3; ++k)
             loc[k] += tile_counts[t * 3 + k];
+    int incl[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k)
-        part[k][threadIdx.x] = loc[k];
-    __syncthreads();
-    if (threadIdx.x < 3)
     {
-        int run = 0;
-        for (int i = 0; i < T; ++i)
+        int v = loc[k];
+        for (int o = 1; o < 32; o <<= 1)
         {
-            const int v = part[threadIdx.x][i];
-            part[threadIdx.x][i] = run;
-            run += v;
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
         }
-        cnt[threadIdx.x] = run;
+        incl[k] = v;
+        if (lane == 31)
+            wsum[k][wid] = v;
     }
     __syncthreads();
-    int run[3] = {part[0][threadIdx.x], part[1][threadIdx.x], part[2][threadIdx.x]};
+    if (wid == 0)
+    {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+        {
+            int v = lane < nwarps ? wsum[k][lane] : 0;
+            for (int o = 1; o < 32; o <<= 1)
+            {
+                const int u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o)
+                    v += u;
+            }
+            if (lane < nwarps)
+                wsum[k][lane] = v; // inclusive over warps
+        }
+    }
+    __syncthreads();
+    int run[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        const int before = wid > 0 ? wsum[k][wid - 1] : 0;
+        run[k] = before + incl[k] - loc[k];
+        if (threadIdx.x == T - 1)
+            cnt[k] = before + incl[k];
+    }
     for (int t = b; t < e; ++t)
         for (int k = 0; k < 3; ++k)
         {
