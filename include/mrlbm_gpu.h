@@ -124,6 +124,19 @@ enum {
     MRLBM_PHASE_COUNT = 6
 };
 
+/* Near-threshold tie record (BASELINE north_star: "except where a detail lies within
+   1e-12 relative of its threshold; any such case is logged").
+   The thresholds stay inclusive (metric >= threshold keeps). */
+typedef struct mrlbm_tie_record {
+    int32_t step;        /* 1-based step since mrlbm_commit in which the group was tested */
+    int32_t level;       /* level l of the sibling group (its parent lies at l - 1)       */
+    int32_t cell[3];     /* parent cell coordinates at level l - 1 (unused axes 0)        */
+    int32_t which;       /* 0: keep threshold eps_l = 2^{d(l-J)} eps (Eq. 10);
+                            1: blow-up threshold 2^{mu+d} eps_l           */
+    double metric;       /* group metric max |d| over siblings and populations */
+    double threshold;
+} mrlbm_tie_record;
+
 typedef struct mrlbm_ctx mrlbm_ctx;
 
 int mrlbm_create(const mrlbm_scheme_spec* scheme, const mrlbm_run_config* cfg, mrlbm_ctx** out);
@@ -134,6 +147,12 @@ int mrlbm_commit(mrlbm_ctx* ctx);
 int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats);
 int mrlbm_level_count(mrlbm_ctx* ctx, int level, int64_t* n);
 int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f);
+/* Tie log since commit (or the last reset): every group metric m with
+   |m - t| <= 1e-12 t for t = eps_l or 2^{mu+d} eps_l (t > 0), sorted by
+   (step, level, cell, which).  n = records logged; at most cap are copied.  Status 5
+   when more records were logged than the device buffer holds (65536).  reset != 0
+   clears the log.  The oracle logs the same records (tests/test_ties.py). */
+int mrlbm_tie_log(mrlbm_ctx* ctx, mrlbm_tie_record* out, int cap, int64_t* n, int reset);
 int mrlbm_set_profiling(mrlbm_ctx* ctx, int on);
 int mrlbm_set_graph(mrlbm_ctx* ctx, int on);
 /* per-kernel device times accumulated over profiled steps: lines "kernel level ms launches" */

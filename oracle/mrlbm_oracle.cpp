@@ -396,6 +396,16 @@ class Oracle {
     // obstacle force history: one (Fx, Fy) per step while tracking
     bool track_force = false;
     std::vector<double> force_hist;
+    // near-threshold tie log (BASELINE north_star): steps since commit
+    int step_no = 0;
+    std::vector<mrlbm_tie_record> ties;
+
+    // log a group metric within 1e-12 relative of a (positive) threshold; the
+    // comparison metric >= threshold itself stays inclusive
+    static bool tie_near(double metric, double thr)
+    {
+        return thr > 0.0 && std::fabs(metric - thr) <= 1e-12 * thr;
+    }
 
     Oracle(const mrlbm_scheme_spec& s_, const mrlbm_run_config& r_) : sc(s_), rc(r_)
     {
@@ -624,6 +634,8 @@ class Oracle {
         for (auto& st : staged)
             st.clear();
         committed = true;
+        step_no = 0;
+        ties.clear();
     }
 
     // install a tree given refined sets per level (index m - J0, m < J1)
@@ -778,6 +790,23 @@ class Oracle {
                     }
                     kflag[i] = metric >= eps_l;
                     bflag[i] = (l > J0 && l < J1) && metric >= eps_b;
+                    for (int which = 0; which < 2; ++which)
+                    {
+                        const double thr = which == 0 ? eps_l : eps_b;
+                        if ((which == 0 || (l > J0 && l < J1)) && tie_near(metric, thr))
+                        {
+                            mrlbm_tie_record r{};
+                            r.step = step_no + 1;
+                            r.level = l;
+                            for (int a = 0; a < D; ++a)
+                                r.cell[a] = static_cast<int32_t>(p[a]);
+                            r.which = which;
+                            r.metric = metric;
+                            r.threshold = thr;
+#pragma omp critical(oracle_ties)
+                            ties.push_back(r);
+                        }
+                    }
                     });
             }
             oe.rethrow();
@@ -1160,6 +1189,7 @@ class Oracle {
             lev[l - J0].lf = std::move(pending[l - J0]);
         pending.clear();
         fallback_last = nfb;
+        ++step_no;
         if (trk)
         {
             force_hist.push_back(force[0]);
@@ -1458,6 +1488,27 @@ int oracle_force_history(void* p, double* fx, double* fy, int cap, int* n)
     });
 }
 
+// tie log since commit (or the last reset), sorted by (step, level, cell, which)
+int oracle_tie_log(void* p, mrlbm_tie_record* out, int cap, int64_t* n, int reset)
+{
+    auto* h = static_cast<Handle*>(p);
+    return guard(h, [&] {
+        std::vector<mrlbm_tie_record>& t = h->o1 ? h->o1->ties : h->o2->ties;
+        std::sort(t.begin(), t.end(), [](const mrlbm_tie_record& a, const mrlbm_tie_record& b) {
+            if (a.step != b.step) return a.step < b.step;
+            if (a.level != b.level) return a.level < b.level;
+            for (int k = 0; k < 3; ++k)
+                if (a.cell[k] != b.cell[k]) return a.cell[k] < b.cell[k];
+            return a.which < b.which;
+        });
+        *n = static_cast<int64_t>(t.size());
+        for (int i = 0; out && i < cap && i < static_cast<int>(t.size()); ++i)
+            out[i] = t[i];
+        if (reset)
+            t.clear();
+    });
+}
+
 const char* oracle_last_error(void* p)
 {
     return static_cast<Handle*>(p)->err.c_str();
@@ -1547,6 +1598,281 @@ int oracle_stream_table_sets(int d, int gap, const int32_t eta[3], int side, int
     {
         return MRLBM_ERR_NUMERIC;
     }
+}
+
+
+} // extern "C"
+
+// ---------------------------------------------------------------------------
+// Independent scheme / run descriptors and initial data for the five BASELINE
+// configurations, written from BASELINE.json configs[0..4] and the decisions
+// ledger (D.2, D.9, D.14-D.22), NOT from the product's builder
+// (paper_2103_02903_b200/csrc/host_configs.cpp).  tests/test_descriptors.py pins
+// every field of the product's descriptors against these, and bench.py's
+// reference arm builds its run from these alone (no product library loaded).
+// M^-1 = the reference DenseMatrix::inverse (dense_matrix.hpp:58-113); equilibrium
+// populations = the reference DenseMatrix::multiply (dense_matrix.hpp:42-54) of
+// M^-1 and this file's equilibrium() (used by the oracle's collision as well).
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Blk {
+    int first, size; // population range of one block of a (block-diagonal) vectorial scheme
+};
+
+// D2Q4 change of basis: rows 1, lambda xi_x, lambda xi_y, lambda^2 (xi_x^2 - xi_y^2)
+// over the velocities (1,0), (0,1), (-1,0), (0,-1)
+void d2q4_rows(double lam, double r[4][4])
+{
+    static const int ex[4] = {1, 0, -1, 0}, ey[4] = {0, 1, 0, -1};
+    for (int j = 0; j < 4; ++j)
+    {
+        r[0][j] = 1.0;
+        r[1][j] = lam * ex[j];
+        r[2][j] = lam * ey[j];
+        r[3][j] = lam * lam * (ex[j] * ex[j] - ey[j] * ey[j]);
+    }
+}
+
+int build_descriptors(int id, int jmax_override, double eps_override, mrlbm_scheme_spec* sc, mrlbm_run_config* rc)
+{
+    *sc = mrlbm_scheme_spec{};
+    *rc = mrlbm_run_config{};
+    rc->gamma = 1;            // prediction stencil gamma = 1 (BASELINE, all configs)
+    rc->graduation = 1;       // grading box half-width = gamma (D.9)
+    rc->obstacle_subsamples = 16;
+    rc->j_min = 2;
+    auto set_eta = [&](int h, int x, int y) { sc->eta[h][0] = x; sc->eta[h][1] = y; };
+    // entries are stored as v + 0.0: structural zeros are +0.0 (no -0.0 from x * 0)
+    auto Mset = [&](int i, int j, double v) { sc->M[i * sc->q + j] = v + 0.0; };
+    double rho0 = 1.0, u0 = 0.0, radius = 0.0, Re = 0.0;
+    if (id == 1)
+    {   // D1Q2 Burgers, [-3,3], levels 2..10, lambda 1, s 1.5, eps 1e-4, outflow (D.2, D.18)
+        sc->d = 1; sc->q = 2; sc->nblocks = 1; sc->equilibrium = MRLBM_EQ_BURGERS_D1Q2; sc->lambda = 1.0;
+        set_eta(0, 1, 0); set_eta(1, -1, 0);
+        Mset(0, 0, 1.0); Mset(0, 1, 1.0); Mset(1, 0, sc->lambda); Mset(1, 1, -sc->lambda);
+        sc->s[1] = 1.5;
+        rc->j_max = 10; rc->base_cells[0] = 24; rc->origin[0] = -3.0; rc->epsilon = 1e-4; rc->mu = 0;
+        rc->bc_kind[0] = rc->bc_kind[1] = MRLBM_BC_COPY;
+    }
+    else if (id == 2)
+    {   // three coupled D1Q3 (rho, q, E), lambda 3, s 1.9, eps 1e-4, levels 2..14 (D.19)
+        sc->d = 1; sc->q = 9; sc->nblocks = 3; sc->equilibrium = MRLBM_EQ_EULER_D1Q3X3; sc->lambda = 3.0;
+        sc->eq_params[0] = 1.4;
+        const double lam = sc->lambda;
+        for (Blk b : {Blk{0, 3}, Blk{3, 3}, Blk{6, 3}})
+        {
+            const int v[3] = {0, 1, -1};
+            for (int j = 0; j < 3; ++j)
+            {
+                set_eta(b.first + j, v[j], 0);
+                Mset(b.first + 0, b.first + j, 1.0);
+                Mset(b.first + 1, b.first + j, lam * v[j]);
+                Mset(b.first + 2, b.first + j, v[j] == 0 ? 0.0 : lam * lam);
+            }
+            sc->s[b.first + 1] = sc->s[b.first + 2] = 1.9;
+        }
+        rc->j_max = 14; rc->base_cells[0] = 4; rc->epsilon = 1e-4; rc->mu = 0;
+        rc->bc_kind[0] = rc->bc_kind[1] = MRLBM_BC_COPY;
+    }
+    else if (id == 3 || id == 4)
+    {   // D2Q4 advection (a, b) = (1, 1), periodic (D.20) / D2Q4^4 Euler, lambda 4, outflow (D.21)
+        const int nb = id == 3 ? 1 : 4;
+        sc->d = 2; sc->q = 4 * nb; sc->nblocks = nb;
+        sc->equilibrium = id == 3 ? MRLBM_EQ_ADVECTION_D2Q4 : MRLBM_EQ_EULER_D2Q4X4;
+        sc->lambda = id == 3 ? 1.0 : 4.0;
+        if (id == 3) { sc->eq_params[0] = 1.0; sc->eq_params[1] = 1.0; }
+        else sc->eq_params[0] = 1.4;
+        double r[4][4];
+        d2q4_rows(sc->lambda, r);
+        static const int ex[4] = {1, 0, -1, 0}, ey[4] = {0, 1, 0, -1};
+        for (int b = 0; b < nb; ++b)
+            for (int i = 0; i < 4; ++i)
+            {
+                set_eta(4 * b + i, ex[i], ey[i]);
+                for (int j = 0; j < 4; ++j)
+                    Mset(4 * b + i, 4 * b + j, r[i][j]);
+                sc->s[4 * b + i] = i == 0 ? 0.0 : 1.9;
+            }
+        rc->j_max = id == 3 ? 9 : 11;
+        rc->base_cells[0] = rc->base_cells[1] = 4;
+        rc->epsilon = id == 3 ? 1e-4 : 1e-3;
+        rc->mu = 0;
+        for (int f = 0; f < 4; ++f)
+            rc->bc_kind[f] = id == 3 ? MRLBM_BC_PERIODIC : MRLBM_BC_COPY;
+    }
+    else if (id == 5)
+    {   // D2Q9 Lallemand-Luo past a cylinder (D.14-D.17)
+        sc->d = 2; sc->q = 9; sc->nblocks = 1; sc->equilibrium = MRLBM_EQ_NS_D2Q9; sc->lambda = 1.0;
+        const double lam = sc->lambda;
+        // xi^h: 0; lambda (cos, sin)(pi/2 (h-1)); lambda (cos, sin)(pi/2 (h-5) + pi/4) / |.| -> unit lattice
+        const int vx[9] = {0, 1, 0, -1, 0, 1, -1, -1, 1}, vy[9] = {0, 0, 1, 0, -1, 1, 1, -1, -1};
+        for (int h = 0; h < 9; ++h)
+        {
+            set_eta(h, vx[h], vy[h]);
+            const double x = vx[h], y = vy[h], n2 = x * x + y * y;
+            // rows of PAPER.md:1334-1343 as polynomials of the velocity, lambda powers applied
+            const double row[9] = {1.0,
+                                   lam * x,
+                                   lam * y,
+                                   lam * lam * (3.0 * n2 - 4.0),
+                                   lam * lam * lam * (3.0 * n2 - 5.0) * x,
+                                   lam * lam * lam * (3.0 * n2 - 5.0) * y,
+                                   lam * lam * lam * lam * (9.0 * n2 * n2 / 2.0 - 21.0 * n2 / 2.0 + 4.0),
+                                   lam * lam * (x * x - y * y),
+                                   lam * lam * x * y};
+            for (int i = 0; i < 9; ++i)
+                Mset(i, h, row[i]);
+        }
+        const double cs2 = lam * lam / 3.0; // c_s = lambda / sqrt(3)
+        sc->eq_params[0] = cs2;
+        sc->eq_params[1] = 0.0;             // |q|^2 / rho form (D.17)
+        rho0 = 1.0; u0 = 0.05; Re = 1200.0; radius = 0.0625;
+        rc->j_max = 12; rc->base_cells[0] = 8; rc->base_cells[1] = 4; rc->epsilon = 1e-4; rc->mu = 1;
+        rc->bc_kind[0] = rc->bc_kind[2] = rc->bc_kind[3] = MRLBM_BC_VELOCITY_BOUNCE_BACK; // inlet, bottom, top
+        rc->bc_kind[1] = MRLBM_BC_COPY;                                                // outlet
+        rc->obstacle = 1;
+        rc->obstacle_center[0] = 0.3125;
+        rc->obstacle_center[1] = 0.5;
+        rc->obstacle_radius = radius;
+    }
+    else
+        return MRLBM_ERR_CONFIG;
+    if (jmax_override > 0)
+    {
+        if (jmax_override <= rc->j_min)
+            return MRLBM_ERR_CONFIG;
+        rc->j_max = jmax_override;
+    }
+    if (eps_override >= 0.0)
+        rc->epsilon = eps_override;
+    const int q = sc->q;
+    if (id == 5)
+    {
+        // s1 pinned (D.17); s2 from the viscosity:
+        // s2 = (1/2 + mu_visc / (c_s^2 dt rho0))^-1, mu_visc = rho0 u0 L / Re, L = 2 r, dt = dx_J / lambda
+        const double cs2 = sc->eq_params[0];
+        const double L = 2.0 * radius;
+        const double mu_visc = rho0 * u0 * L / Re;
+        const double dt = std::ldexp(1.0, -rc->j_max) / sc->lambda;
+        const double s2 = 1.0 / (0.5 + mu_visc / (cs2 * dt * rho0));
+        for (int h = 3; h < 7; ++h)
+            sc->s[h] = 1.5;
+        sc->s[7] = sc->s[8] = s2;
+        // moving-wall (Ladd) term 2 w_h rho0 (xi_h . u_w) / c_s^2 with u_w = (u0, 0) on the
+        // velocity bounce-back faces (D.14); D2Q9 weights 4/9, 1/9, 1/36
+        for (int f = 0; f < 4; ++f)
+            for (int h = 0; h < 9; ++h)
+            {
+                const int n1 = std::abs(sc->eta[h][0]) + std::abs(sc->eta[h][1]);
+                const double w = n1 == 0 ? 4.0 / 9 : (n1 == 1 ? 1.0 / 9 : 1.0 / 36);
+                const double xu = sc->lambda * sc->eta[h][0] * u0;
+                rc->bc_add[f][h] = rc->bc_kind[f] == MRLBM_BC_VELOCITY_BOUNCE_BACK ? 2.0 * w * rho0 * xu / cs2 : 0.0;
+            }
+    }
+    mrlbm::DenseMatrix M(q, q);
+    for (int i = 0; i < q; ++i)
+        for (int j = 0; j < q; ++j)
+            M(i, j) = sc->M[i * q + j];
+    const mrlbm::DenseMatrix Mi = M.inverse();
+    for (int i = 0; i < q; ++i)
+        for (int j = 0; j < q; ++j)
+            sc->Minv[i * q + j] = Mi(i, j);
+    if (id == 5)
+    {   // obstacle target M^-1 m^eq(rho0, 0, 0)
+        double m[MRLBM_MAX_Q] = {rho0, 0.0, 0.0}, meq[MRLBM_MAX_Q] = {};
+        equilibrium(*sc, m, meq);
+        Mi.multiply(meq, rc->obstacle_feq);
+    }
+    return MRLBM_OK;
+}
+
+// splitmix64 finaliser -> uniform double in [-1, 1) (D.16: 53 high bits)
+double unit_sm64(std::uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return static_cast<double>(z >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+}
+
+} // namespace
+
+extern "C" {
+
+int oracle_build_config(int id, int jmax_override, double eps_override, mrlbm_scheme_spec* sc, mrlbm_run_config* rc)
+{
+    try
+    {
+        return build_descriptors(id, jmax_override, eps_override, sc, rc);
+    }
+    catch (...)
+    {
+        return MRLBM_ERR_CONFIG;
+    }
+}
+
+// f = M^-1 m^eq(conserved moments of the datum at the finest cell centre) (D.22),
+// SoA q x N, cells in CellIndex order (axis 0 slow)
+int oracle_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, uint64_t seed, double* f)
+{
+    const int q = sc->q, d = sc->d, J = rc->j_max;
+    const std::int64_t nx = rc->base_cells[0] << (J - rc->j_min);
+    const std::int64_t ny = d == 2 ? (rc->base_cells[1] << (J - rc->j_min)) : 1;
+    const std::int64_t N = nx * ny;
+    const double h = std::ldexp(1.0, -J);
+    mrlbm::DenseMatrix Mi(q, q);
+    for (int i = 0; i < q; ++i)
+        for (int j = 0; j < q; ++j)
+            Mi(i, j) = sc->Minv[i * q + j];
+    const int bs = q / sc->nblocks;
+    auto energy = [](double rho, double u, double v, double p, double gam) {
+        return p / (gam - 1.0) + 0.5 * rho * (u * u + v * v);
+    };
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < N; ++i)
+    {
+        const std::int64_t ix = i / ny, iy = i % ny;
+        const double x = rc->origin[0] + (static_cast<double>(ix) + 0.5) * h;
+        const double y = rc->origin[1] + (static_cast<double>(iy) + 0.5) * h;
+        double U[4] = {0, 0, 0, 0}; // conserved variables, one per block
+        switch (id)
+        {
+            case 1: U[0] = std::max(0.0, 1.0 - std::fabs(x)); break;
+            case 2:
+            {   // Lax shock tube, (rho, u, p)_L = (0.445, 0.698, 3.528), _R = (0.5, 0, 0.571), jump at 0.5
+                const double rho = x < 0.5 ? 0.445 : 0.5, u = x < 0.5 ? 0.698 : 0.0, p = x < 0.5 ? 3.528 : 0.571;
+                U[0] = rho; U[1] = rho * u; U[2] = energy(rho, u, 0.0, p, sc->eq_params[0]);
+                break;
+            }
+            case 3: U[0] = ((x - 0.5) * (x - 0.5) + (y - 0.5) * (y - 0.5) <= 0.04) ? 1.0 : 0.0; break;
+            case 4:
+            {   // quadrant states (rho, u, v, p): NE, NW, SW, SE
+                static const double st[4][4] = {{1.5, 0.0, 0.0, 1.5}, {0.5323, 1.206, 0.0, 0.3},
+                                                {0.138, 1.206, 1.206, 0.029}, {0.5323, 0.0, 1.206, 0.3}};
+                const int k = (x > 0.5 && y > 0.5) ? 0 : (x < 0.5 && y > 0.5) ? 1 : (x < 0.5 && y < 0.5) ? 2 : 3;
+                U[0] = st[k][0]; U[1] = st[k][0] * st[k][1]; U[2] = st[k][0] * st[k][2];
+                U[3] = energy(st[k][0], st[k][1], st[k][2], st[k][3], sc->eq_params[0]);
+                break;
+            }
+            case 5: U[0] = 1.0; U[1] = 0.0; U[2] = 1.0 * (1e-3 * unit_sm64(seed ^ static_cast<std::uint64_t>(i))); break;
+            default: break;
+        }
+        double m[MRLBM_MAX_Q] = {}, meq[MRLBM_MAX_Q] = {}, fl[MRLBM_MAX_Q] = {};
+        if (id == 5)
+        {
+            m[0] = U[0]; m[1] = U[1]; m[2] = U[2];
+        }
+        else
+            for (int b = 0; b < sc->nblocks; ++b)
+                m[b * bs] = U[b];
+        equilibrium(*sc, m, meq);
+        Mi.multiply(meq, fl);
+        for (int k = 0; k < q; ++k)
+            f[k * N + i] = fl[k];
+    }
+    return (id >= 1 && id <= 5) ? MRLBM_OK : MRLBM_ERR_CONFIG;
 }
 
 } // extern "C"

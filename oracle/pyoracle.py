@@ -10,7 +10,7 @@ import subprocess
 
 import numpy as np
 
-from paper_2103_02903_b200.abi import SchemeSpec, RunConfig
+from paper_2103_02903_b200.abi import SchemeSpec, RunConfig, TieRecord, tie_tuples
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_lib", "libmrlbm_oracle.so")
@@ -53,6 +53,9 @@ def oracle_lib():
         L.oracle_destroy.argtypes = [vp]
         L.oracle_destroy.restype = None
         L.oracle_set_threads.argtypes = [C.c_int]
+        L.oracle_tie_log.argtypes = [vp, P(TieRecord), C.c_int, P(C.c_int64), C.c_int]
+        L.oracle_build_config.argtypes = [C.c_int, C.c_int, C.c_double, P(SchemeSpec), P(RunConfig)]
+        L.oracle_initial_finest.argtypes = [C.c_int, P(SchemeSpec), P(RunConfig), C.c_uint64, vp]
         L.oracle_set_force_tracking.argtypes = [vp, C.c_int]
         L.oracle_force_history.argtypes = [vp, vp, vp, C.c_int, P(C.c_int)]
         L.oracle_stream_table.argtypes = [C.c_int, C.c_int, P(C.c_int32), C.c_int, C.c_int, vp, vp, P(C.c_int)]
@@ -81,6 +84,38 @@ def ref_lib():
         L.ref_cellindex_slots2.argtypes = [C.c_int, vp, vp]
         _ref = L
     return _ref
+
+
+def build_config(config_id, j_max=0, epsilon=-1.0):
+    """The oracle's own descriptors for BASELINE config `config_id` (independent of the
+    product's builder; pinned field by field in tests/test_descriptors.py)."""
+    sc, rc = SchemeSpec(), RunConfig()
+    st = oracle_lib().oracle_build_config(int(config_id), int(j_max), float(epsilon), C.byref(sc), C.byref(rc))
+    if st != 0:
+        raise ValueError(f"oracle_build_config({config_id}) failed with status {st}")
+    return sc, rc
+
+
+def finest_cells(sc, rc):
+    """int32 coordinates (N, d) of the full finest mesh in CellIndex order."""
+    sh = rc.j_max - rc.j_min
+    nx = int(rc.base_cells[0]) << sh
+    if sc.d == 1:
+        return np.arange(nx, dtype=np.int32).reshape(-1, 1)
+    ny = int(rc.base_cells[1]) << sh
+    xs, ys = np.meshgrid(np.arange(nx, dtype=np.int32), np.arange(ny, dtype=np.int32), indexing="ij")
+    return np.stack([xs.ravel(), ys.ravel()], axis=1).astype(np.int32)
+
+
+def initial_finest(config_id, sc, rc, seed=2103_02903):
+    """The oracle's initial datum (D.22) on the full finest mesh, SoA (q, N)."""
+    n = finest_cells(sc, rc).shape[0]
+    f = np.empty((sc.q, n), dtype=np.float64)
+    st = oracle_lib().oracle_initial_finest(int(config_id), C.byref(sc), C.byref(rc), C.c_uint64(seed),
+                                            f.ctypes.data_as(C.c_void_p))
+    if st != 0:
+        raise ValueError(f"oracle_initial_finest({config_id}) failed with status {st}")
+    return f
 
 
 def set_threads(n):
@@ -122,6 +157,14 @@ class Oracle:
 
     def step(self, n=1):
         self._check(self.L.oracle_step(self.h, int(n)))
+
+    def tie_log(self, reset=False):
+        """Near-threshold tie records since commit, sorted (same tuples as Solver.tie_log)."""
+        n = C.c_int64(0)
+        self._check(self.L.oracle_tie_log(self.h, None, 0, C.byref(n), 0))
+        recs = (TieRecord * max(1, n.value))()
+        self._check(self.L.oracle_tie_log(self.h, recs, n.value, C.byref(n), int(bool(reset))))
+        return tie_tuples(recs, n.value)
 
     def level_count(self, level):
         n = C.c_int64(0)

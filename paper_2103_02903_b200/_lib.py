@@ -6,7 +6,7 @@ product path.
 import ctypes as C
 import os
 
-from .abi import SchemeSpec, RunConfig, StepStats
+from .abi import SchemeSpec, RunConfig, StepStats, TieRecord
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmrlbm_b200.so")
@@ -30,6 +30,7 @@ def lib():
         "mrlbm_level_count": (C.c_int, [vp, C.c_int, P(C.c_int64)]),
         "mrlbm_read_leaves": (C.c_int, [vp, C.c_int, vp, vp]),
         "mrlbm_set_profiling": (C.c_int, [vp, C.c_int]),
+        "mrlbm_tie_log": (C.c_int, [vp, P(TieRecord), C.c_int, P(C.c_int64), C.c_int]),
         "mrlbm_set_graph": (C.c_int, [vp, C.c_int]),
         "mrlbm_profile_text": (C.c_int, [vp, C.c_char_p, C.c_int, C.c_int]),
         "mrlbm_stream_handle": (vp, [vp]),

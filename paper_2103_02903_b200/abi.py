@@ -60,6 +60,19 @@ class StepStats(C.Structure):
     ]
 
 
+class TieRecord(C.Structure):
+    """mrlbm_tie_record: a group metric within 1e-12 relative of a threshold."""
+    _fields_ = [
+        ("step", C.c_int32), ("level", C.c_int32), ("cell", C.c_int32 * 3), ("which", C.c_int32),
+        ("metric", C.c_double), ("threshold", C.c_double),
+    ]
+
+
+def tie_tuples(recs, n):
+    """(step, level, cell..., which, metric, threshold) tuples of the first n records."""
+    return [(r.step, r.level, r.cell[0], r.cell[1], r.cell[2], r.which, r.metric, r.threshold) for r in recs[:n]]
+
+
 def level_extent(cfg: RunConfig, d: int, level: int):
     sh = level - cfg.j_min
     nx = cfg.base_cells[0] << sh

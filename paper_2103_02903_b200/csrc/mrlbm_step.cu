@@ -111,6 +111,12 @@ struct Aux {
                         //     counts at fb_count[2 + seg]
     long long fbs_off[2], fbs_cap[2];
     double* frc;
+    // near-threshold tie log (north_star): records of group metrics within
+    // 1e-12 relative of eps_l or 2^{mu+d} eps_l; step_no = steps completed since commit
+    mrlbm_tie_record* ties;
+    int* tie_n;
+    int tie_cap;
+    const int* step_no;
     long long frc_off[kL];
     int frc_x0[kL], frc_y0[kL], frc_nx[kL], frc_ny[kL];
 };
@@ -280,6 +286,31 @@ __device__ __forceinline__ double mr_predict(const double* st, int dx, int dy)
 __device__ __forceinline__ void flag_err(int* err, int which)
 {
     atomicAdd(&err[which], 1);
+}
+
+// Near-threshold tie logging (BASELINE north_star: a mesh may differ from the CPU run
+// only where a detail lies within 1e-12 relative of its threshold, and every such case
+// is logged).  The comparison itself stays inclusive (>=,
+// SPEC.md:247); this only records the group.  Same expression as the oracle's
+// (oracle/mrlbm_oracle.cpp, tie_check), no FMA on either side.
+__device__ __forceinline__ void tie_check(const Aux& aux, int l, int px, int py, int which, double metric, double thr)
+{
+    if (!(thr > 0.0) || !(fabs(__dsub_rn(metric, thr)) <= __dmul_rn(1e-12, thr)))
+        return;
+    const int k = atomicAdd(aux.tie_n, 1);
+    if (k < aux.tie_cap)
+    {
+        mrlbm_tie_record r;
+        r.step = *aux.step_no + 1;
+        r.level = l;
+        r.cell[0] = px;
+        r.cell[1] = py;
+        r.cell[2] = 0;
+        r.which = which;
+        r.metric = metric;
+        r.threshold = thr;
+        aux.ties[k] = r;
+    }
 }
 
 #define GRID_STRIDE(i, begin, end)                                                                  \
@@ -487,6 +518,9 @@ __global__ void __launch_bounds__(256, 4) k_details(const __grid_constant__ Geo 
                     metric = ad;
             }
         }
+        tie_check(aux, l, px, py, 0, metric, eps_l);
+        if (can_b)
+            tie_check(aux, l, px, py, 1, metric, eps_b);
         if (metric >= eps_l)
             fl.keep[li][plin] = 1;
         if (can_b && metric >= eps_b)
@@ -600,6 +634,9 @@ __global__ void __launch_bounds__(256, 3)
             flag_err(aux.err, 0);
             continue;
         }
+        tie_check(aux, l, px, py, 0, metric, eps_l);
+        if (can_b)
+            tie_check(aux, l, px, py, 1, metric, eps_b);
         if (metric >= eps_l)
             fl.keep[li][plin] = 1;
         if (can_b && metric >= eps_b)
@@ -1479,33 +1516,62 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count(const uint8_t* kind
     }
 }
 
-// single block: exclusive scan of the tile counts per category; totals -> cnt
-__global__ void k_tile_scan(int* tile_counts, int ntiles, int* cnt)
+// one block: exclusive scan of the tile counts per category, in place; totals -> cnt.
+// Per-thread sums of a contiguous tile range, a block-wide exclusive scan of those
+// sums (warp shuffles + warp totals in shared memory), then the per-tile offsets.
+__device__ __forceinline__ void block_scan_tiles(int* tile_counts, int ntiles, int* cnt)
 {
-    __shared__ int part[3][1024];
+    __shared__ int wsum[3][32];
     const int T = blockDim.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = T >> 5;
     const int per = (ntiles + T - 1) / T;
     const int b = threadIdx.x * per, e = min(ntiles, b + per);
     int loc[3] = {0, 0, 0};
     for (int t = b; t < e; ++t)
         for (int k = 0; k < 3; ++k)
             loc[k] += tile_counts[t * 3 + k];
+    int incl[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k)
-        part[k][threadIdx.x] = loc[k];
-    __syncthreads();
-    if (threadIdx.x < 3)
     {
-        int run = 0;
-        for (int i = 0; i < T; ++i)
+        int v = loc[k];
+        for (int o = 1; o < 32; o <<= 1)
         {
-            const int v = part[threadIdx.x][i];
-            part[threadIdx.x][i] = run;
-            run += v;
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o)
+                v += u;
         }
-        cnt[threadIdx.x] = run;
+        incl[k] = v;
+        if (lane == 31)
+            wsum[k][wid] = v;
     }
     __syncthreads();
-    int run[3] = {part[0][threadIdx.x], part[1][threadIdx.x], part[2][threadIdx.x]};
+    if (wid == 0)
+    {
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+        {
+            int v = lane < nwarps ? wsum[k][lane] : 0;
+            for (int o = 1; o < 32; o <<= 1)
+            {
+                const int u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o)
+                    v += u;
+            }
+            if (lane < nwarps)
+                wsum[k][lane] = v; // inclusive over warps
+        }
+    }
+    __syncthreads();
+    int run[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+    {
+        const int before = wid > 0 ? wsum[k][wid - 1] : 0;
+        run[k] = before + incl[k] - loc[k];
+        if (threadIdx.x == T - 1)
+            cnt[k] = before + incl[k];
+    }
     for (int t = b; t < e; ++t)
         for (int k = 0; k < 3; ++k)
         {
@@ -1513,6 +1579,11 @@ __global__ void k_tile_scan(int* tile_counts, int ntiles, int* cnt)
             tile_counts[t * 3 + k] = run[k];
             run[k] += v;
         }
+}
+
+__global__ void k_tile_scan(int* tile_counts, int ntiles, int* cnt)
+{
+    block_scan_tiles(tile_counts, ntiles, cnt);
 }
 
 // per-thread counts of its 16 cells -> block exclusive scan (warp shuffles + warp
@@ -1688,74 +1759,13 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_count_ml(const __grid_con
 
 __global__ void k_tile_scan_ml(const __grid_constant__ Geo g, const __grid_constant__ TileP tp, const __grid_constant__ Tree tn, const __grid_constant__ LGrid lg_)
 {
-    // one block per level: per-thread sums of a contiguous tile range, a block-wide
-    // exclusive scan of those sums (warp shuffles + warp totals), then the per-tile
-    // exclusive offsets; the level totals go to cnt
+    // one block per level; the level totals go to cnt
     LSETUP;
     (void)lvb_;
     (void)lvg_;
     const int li = m - g.J0;
     const int ntiles = (int)((g.cap[li] + kTile - 1) / kTile);
-    int* tile_counts = tp.t[li];
-    int* cnt = tn.cnt + li * 4;
-    __shared__ int wsum[3][32];
-    const int T = blockDim.x;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = T >> 5;
-    const int per = (ntiles + T - 1) / T;
-    const int b = threadIdx.x * per, e = min(ntiles, b + per);
-    int loc[3] = {0, 0, 0};
-    for (int t = b; t < e; ++t)
-        for (int k = 0; k < 3; ++k)
-            loc[k] += tile_counts[t * 3 + k];
-    int incl[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-    {
-        int v = loc[k];
-        for (int o = 1; o < 32; o <<= 1)
-        {
-            const int u = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o)
-                v += u;
-        }
-        incl[k] = v;
-        if (lane == 31)
-            wsum[k][wid] = v;
-    }
-    __syncthreads();
-    if (wid == 0)
-    {
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-        {
-            int v = lane < nwarps ? wsum[k][lane] : 0;
-            for (int o = 1; o < 32; o <<= 1)
-            {
-                const int u = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o)
-                    v += u;
-            }
-            if (lane < nwarps)
-                wsum[k][lane] = v; // inclusive over warps
-        }
-    }
-    __syncthreads();
-    int run[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-    {
-        const int before = wid > 0 ? wsum[k][wid - 1] : 0;
-        run[k] = before + incl[k] - loc[k];
-        if (threadIdx.x == T - 1)
-            cnt[k] = before + incl[k];
-    }
-    for (int t = b; t < e; ++t)
-        for (int k = 0; k < 3; ++k)
-        {
-            const int v = tile_counts[t * 3 + k];
-            tile_counts[t * 3 + k] = run[k];
-            run[k] += v;
-        }
+    block_scan_tiles(tp.t[li], ntiles, tn.cnt + li * 4);
 }
 
 __global__ void __launch_bounds__(kTileThreads) k_tile_scatter_ml(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ TileP tp, const __grid_constant__ Tree tn, const __grid_constant__ LGrid lg_)
@@ -3293,7 +3303,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     }
 }
 
-__global__ void k_count_updates(const int* cnt, int nlev, long long* acc)
+__global__ void k_count_updates(const int* cnt, int nlev, long long* acc, int* step_no)
 {
     if (threadIdx.x == 0 && blockIdx.x == 0)
     {
@@ -3301,6 +3311,7 @@ __global__ void k_count_updates(const int* cnt, int nlev, long long* acc)
         for (int i = 0; i < nlev; ++i)
             s += cnt[i * 4];
         *acc += s;
+        *step_no += 1;
     }
 }
 
@@ -3587,6 +3598,11 @@ struct mrlbm_ctx {
     double* fhist = nullptr;
     int* fhn = nullptr;
     int* rdcnt = nullptr; // read-back: level totals of the lexicographic re-sort
+    // near-threshold tie log (mrlbm_tie_log)
+    mrlbm_tie_record* ties = nullptr;
+    int* tie_n = nullptr;
+    int* step_no = nullptr;
+    int tie_cap = 1 << 16;
     int fcap = 0;
     cudaEvent_t ev[16]{};
     double phase_ms[MRLBM_PHASE_COUNT]{};
@@ -3679,6 +3695,10 @@ Aux aux_of(mrlbm_ctx* c)
     a.pmask = c->pmaskd;
     a.umask = c->umaskd;
     a.frc = c->frc;
+    a.ties = c->ties;
+    a.tie_n = c->tie_n;
+    a.tie_cap = c->tie_cap;
+    a.step_no = c->step_no;
     a.fb1t = (c->use_fb1t && c->use_gen) ? 1 : 0;
     a.fbs = c->fbs;
     for (int k = 0; k < 2; ++k)
@@ -4047,7 +4067,7 @@ void enqueue_step(mrlbm_ctx* c)
             kmark(c, "k_stream_collide_fb0", -1);
         }
     }
-    { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd);  kmark(c, "k_count_updates", -1); }
+    { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd, c->step_no);  kmark(c, "k_count_updates", -1); }
     if (c->frc)
         { c->kcount++; k_force_sum<<<1, 1024, 0, s>>>(c->frc, c->frc_n, c->fhist, c->fhn, c->fcap);  kmark(c, "k_force_sum", -1); }
     phase_mark(c, 6);
@@ -4291,6 +4311,11 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         CU(cudaMemset(ctx->err, 0, sizeof(int) * 4));
         CU(cudaMalloc(&ctx->upd, sizeof(long long)));
         CU(cudaMemset(ctx->upd, 0, sizeof(long long)));
+        CU(cudaMalloc(&ctx->ties, sizeof(mrlbm_tie_record) * ctx->tie_cap));
+        CU(cudaMalloc(&ctx->tie_n, sizeof(int)));
+        CU(cudaMemset(ctx->tie_n, 0, sizeof(int)));
+        CU(cudaMalloc(&ctx->step_no, sizeof(int)));
+        CU(cudaMemset(ctx->step_no, 0, sizeof(int)));
         // scheme constants
         SchemeDev h{};
         h.q = sc->q;
@@ -4508,6 +4533,8 @@ int mrlbm_commit(mrlbm_ctx* ctx)
         CU(cudaMemsetAsync(ctx->rn[li], 0, g.cap[li], ctx->stream));
     }
     CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
+    CU(cudaMemsetAsync(ctx->step_no, 0, sizeof(int), ctx->stream));
+    CU(cudaMemsetAsync(ctx->tie_n, 0, sizeof(int), ctx->stream));
     auto cleanup = [&]() {};
     int st = [&]() -> int
     {
@@ -4679,6 +4706,9 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
     if (!ctx || level < ctx->J0 || level > ctx->J1)
         return MRLBM_ERR_CONFIG;
     const int li = level - ctx->J0;
+    for (int k = 0; k < ctx->nlev; ++k)
+        if (ctx->ld_n[k])
+            return set_err(ctx, MRLBM_ERR_STATE, "read_leaves between load_leaves and commit (staged load pending)");
     int64_t n = 0;
     int st = mrlbm_level_count(ctx, level, &n);
     if (st != MRLBM_OK)
@@ -4948,6 +4978,36 @@ int mrlbm_force_history(mrlbm_ctx* ctx, double* fx, double* fy, int cap, int* n)
     return MRLBM_OK;
 }
 
+int mrlbm_tie_log(mrlbm_ctx* ctx, mrlbm_tie_record* out, int cap, int64_t* n, int reset)
+{
+    if (!ctx || !n || cap < 0)
+        return MRLBM_ERR_CONFIG;
+    int total = 0;
+    CU(cudaMemcpyAsync(&total, ctx->tie_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *n = total;
+    const int stored = std::min(total, ctx->tie_cap);
+    if (out && cap > 0 && stored > 0)
+    {
+        std::vector<mrlbm_tie_record> r(stored);
+        CU(cudaMemcpy(r.data(), ctx->ties, sizeof(mrlbm_tie_record) * stored, cudaMemcpyDeviceToHost));
+        // the device appends in arrival order: sort into (step, level, cell, which)
+        std::sort(r.begin(), r.end(), [](const mrlbm_tie_record& a, const mrlbm_tie_record& b) {
+            if (a.step != b.step) return a.step < b.step;
+            if (a.level != b.level) return a.level < b.level;
+            for (int k = 0; k < 3; ++k)
+                if (a.cell[k] != b.cell[k]) return a.cell[k] < b.cell[k];
+            return a.which < b.which;
+        });
+        std::memcpy(out, r.data(), sizeof(mrlbm_tie_record) * std::min(cap, stored));
+    }
+    if (reset)
+        CU(cudaMemsetAsync(ctx->tie_n, 0, sizeof(int), ctx->stream));
+    return total > ctx->tie_cap ? set_err(ctx, MRLBM_ERR_CAPACITY, "tie log overflow: " + std::to_string(total) +
+                                                                      " records, capacity " + std::to_string(ctx->tie_cap))
+                                : MRLBM_OK;
+}
+
 int mrlbm_set_graph(mrlbm_ctx* ctx, int on)
 {
     if (!ctx)
@@ -5016,6 +5076,9 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->fbm);
     cudaFree(ctx->fbdm);
     cudaFree(ctx->upd);
+    cudaFree(ctx->ties);
+    cudaFree(ctx->tie_n);
+    cudaFree(ctx->step_no);
     cudaFree(ctx->tidx);
     cudaFree(ctx->toff);
     cudaFree(ctx->tw);

@@ -11,7 +11,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .abi import StepStats, PHASES, ERR_CONFIG, ERR_NUMERIC
+from .abi import StepStats, TieRecord, tie_tuples, PHASES, ERR_CONFIG, ERR_NUMERIC
 
 
 class MRLBMError(RuntimeError):
@@ -75,6 +75,15 @@ class Solver:
 
     def commit(self):
         self._check(self.L.mrlbm_commit(self.h))
+
+    def tie_log(self, reset=False):
+        """Near-threshold tie records since commit, sorted: list of (step, level, cx, cy,
+        cz, which, metric, threshold) tuples (include/mrlbm_gpu.h, mrlbm_tie_log)."""
+        n = C.c_int64(0)
+        self._check(self.L.mrlbm_tie_log(self.h, None, 0, C.byref(n), 0))
+        recs = (TieRecord * max(1, n.value))()
+        self._check(self.L.mrlbm_tie_log(self.h, recs, n.value, C.byref(n), int(bool(reset))))
+        return tie_tuples(recs, n.value)
 
     def step(self, n=1):
         stats = StepStats()
