@@ -21,6 +21,7 @@
 #include "mrlbm_internal.h"
 
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cmath>
@@ -34,6 +35,8 @@
 #include <vector>
 
 namespace mrlbm_b200 {
+
+namespace cg = cooperative_groups;
 
 constexpr int kL = MRLBM_MAX_LEVELS;
 constexpr int kQ = MRLBM_MAX_Q;
@@ -108,8 +111,9 @@ struct Aux {
     int fb1t;           // thread-per-leaf gap-1 path on: the boundary-rim fallback leaves are listed
     int* fbs;           // [2] segment lists of linear indices: 0 = gap-0 fallback leaves (level J1),
                         //     1 = gap-1 fallback leaves with domain-leaving pairs (level J1-1);
+                        //     2 = the other gap-1 fallback leaves (level J1-1, K7 MODE 2),
                         //     counts at fb_count[2 + seg]
-    long long fbs_off[2], fbs_cap[2];
+    long long fbs_off[3], fbs_cap[3];
     double* frc;
     // near-threshold tie log (north_star): records of group metrics within
     // 1e-12 relative of eps_l or 2^{mu+d} eps_l; step_no = steps completed since commit
@@ -288,6 +292,17 @@ __device__ __forceinline__ void flag_err(int* err, int which)
     atomicAdd(&err[which], 1);
 }
 
+// warp-aggregated append: one atomicAdd per group of lanes that arrive together
+__device__ __forceinline__ int agg_inc(int* ctr)
+{
+    cg::coalesced_group grp = cg::coalesced_threads();
+    int base = 0;
+    if (grp.thread_rank() == 0)
+        base = atomicAdd(ctr, (int)grp.size());
+    base = grp.shfl(base, 0);
+    return base + (int)grp.thread_rank();
+}
+
 // Near-threshold tie logging (BASELINE north_star: a mesh may differ from the CPU run
 // only where a detail lies within 1e-12 relative of its threshold, and every such case
 // is logged).  The comparison itself stays inclusive (>=,
@@ -352,7 +367,7 @@ __global__ void k_zero_flags(const __grid_constant__ Geo g, const __grid_constan
     LSETUP;
     const int li = m - g.J0;
     const long long n16 = g.cap[li] / 16, n = g.cap[li];
-    if (blockIdx.x == 0 && threadIdx.x < 4)
+    if (blockIdx.x == 0 && threadIdx.x < 8)
         fbc[threadIdx.x] = 0;
     LGRID_STRIDE(i, 0, n16)
     {
@@ -1211,12 +1226,14 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     fl.fbm[li][vi] = mask;
     fl.fbd[li][vi] = dmask;
     fl.kind[li][i] = K_LEAF | K_FB;
-    // segment lists (thread-per-leaf path): gap-0 fallback leaves and gap-1 leaves whose
-    // pairs leave the domain, streamed by K7 MODE 5 / MODE 3 from the lists
-    if (aux.fb1t && (gap == 0 || (gap == 1 && dmask != 0)))
+    // segment lists (thread-per-leaf path): gap-0 fallback leaves, gap-1 leaves whose
+    // pairs leave the domain, and the other gap-1 leaves, streamed by K7 MODE 5 / k_fb1
+    // (or MODE 3) / MODE 2 from the lists, so no warp of those kernels idles on the
+    // leaves it does not take.  One atomic per coalesced group of lanes.
+    if (aux.fb1t && gap <= 1)
     {
-        const int seg = gap == 0 ? 0 : 1;
-        const int k = atomicAdd(aux.fb_count + 2 + seg, 1);
+        const int seg = gap == 0 ? 0 : (dmask != 0 ? 1 : 2);
+        const int k = agg_inc(aux.fb_count + 2 + seg);
         if (k < aux.fbs_cap[seg])
             aux.fbs[aux.fbs_off[seg] + k] = (int)i;
         else
@@ -1225,7 +1242,7 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     // listed: deep-gap leaves (K8, bands)
     if (gap >= 2)
     {
-        const int k = atomicAdd(aux.fb_count, 1);
+        const int k = agg_inc(aux.fb_count);
         if (k < aux.fb_cap)
         {
             aux.fb_list[k] = make_int2(m, (int)i);
@@ -2389,6 +2406,123 @@ __global__ void __launch_bounds__(256, 4) k_stream_fallback(const __grid_constan
     }
 }
 
+// K8 (default): the same stream of the deep-gap fallback leaves, one THREAD per (leaf,
+// population).  Each side's sum is accumulated serially in table / rim order from 0.0,
+// exactly rim_sum's arithmetic (and the warp kernel's), but 32 independent sums run per
+// warp instead of one, so no lane idles on short rims (4..2^(gap+1) cells) and no
+// shuffle chain serialises the adds.  Rim cells are fetched in batches of kRimB: the
+// kinds and the (speculative) materialised values of a batch are loaded together so
+// kRimB independent loads are in flight per thread; cells outside the domain or not
+// materialised take the general rim_value path.
+constexpr int kRimB = 8;
+
+template <int D>
+__global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+                                                           const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
+                                                           const SchemeDev* sc, const __grid_constant__ Aux aux)
+{
+    const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
+    const int q = g.q;
+    const int lj = g.J1 - g.J0;
+    const int nxf = g.nx[lj], nyf = g.ny[lj];
+    const long long capf = g.cap[lj];
+    GRID_STRIDE(t, 0, (long long)nfb * q)
+    {
+        const int it = (int)(t / q), h = (int)(t - (long long)it * q);
+        const int2 e = aux.fb_list[it];
+        const int m = e.x;
+        const int gap = g.J1 - m;
+        if (gap < 2)
+            continue; // gap 0 / 1: K7 MODE 2 / 5 and k_fb1
+        const unsigned mask = aux.fb_mask[it];
+        const int li = m - g.J0;
+        const int ny = g.ny[li];
+        const long long cap = g.cap[li];
+        int x, y;
+        lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
+        const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
+        double sums[2];
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side)
+        {
+            double acc = 0.0;
+            if (((mask >> (2 * h + side)) & 1u) == 0)
+            {
+                // flattened table, in table order
+                const int2 ti = aux.tidx[(gap * q + h) * 2 + side];
+                const double* fm = F1.f[li] + (long long)h * cap;
+#pragma unroll 1
+                for (int k0 = 0; k0 < ti.y; k0 += kRimB)
+                {
+                    double v[kRimB];
+#pragma unroll
+                    for (int j = 0; j < kRimB; ++j)
+                    {
+                        v[j] = 0.0;
+                        if (k0 + j < ti.y)
+                        {
+                            const int k = ti.x + k0 + j;
+                            const int2 o = aux.toff[k];
+                            if (!tn.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)])
+                                flag_err(aux.err, 0);
+                            v[j] = __dmul_rn(aux.tw[k], fm[mr_vix<D>(g, m, x + o.x, y + o.y)]);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < kRimB; ++j)
+                        if (k0 + j < ti.y)
+                            acc = __dadd_rn(acc, v[j]);
+                }
+            }
+            else if (ex != 0 || ey != 0)
+            {
+                const int side_n = 1 << gap;
+                const int bx0 = x * side_n, bx1 = bx0 + side_n;
+                const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
+                int xr = 0, yr = 0;
+                const int n = rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, -1, xr, yr);
+                const double* ff = F1.f[lj] + (long long)h * capf;
+#pragma unroll 1
+                for (int b0 = 0; b0 < n; b0 += kRimB)
+                {
+                    double v[kRimB];
+                    uint8_t kd[kRimB];
+                    int cx[kRimB], cy[kRimB];
+#pragma unroll
+                    for (int j = 0; j < kRimB; ++j)
+                    {
+                        kd[j] = 0;
+                        v[j] = 0.0;
+                        cx[j] = cy[j] = 0;
+                        if (b0 + j < n)
+                        {
+                            rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, b0 + j, cx[j], cy[j]);
+                            const bool inside = (g.per0 || (cx[j] >= 0 && cx[j] < nxf)) &&
+                                                (D == 1 || g.per1 || (cy[j] >= 0 && cy[j] < nyf));
+                            if (inside)
+                            {
+                                kd[j] = tn.kind[lj][mr_lin<D>(g, g.J1, cx[j], cy[j])];
+                                v[j] = ff[mr_vix<D>(g, g.J1, cx[j], cy[j])];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < kRimB; ++j)
+                        if (b0 + j < n)
+                        {
+                            const double w = kd[j] ? v[j] : rim_value<D>(g, tn, F1, sc, cx[j], cy[j], h, li, e.y, aux);
+                            acc = __dadd_rn(acc, w);
+                        }
+                }
+            }
+            sums[side] = acc;
+        }
+        const double scale = ldexp(1.0, D * (m - g.J1));
+        const long long o = (long long)h * cap + vix<D>(x, y, ny);
+        F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+    }
+}
+
 // config 5 volume-fraction blend: the fraction alpha
 // of the cell (level m, index x, y) inside the disc, from ns x ns sub-samples; 0 when
 // the cell's box misses the disc's bounding box.
@@ -3046,9 +3180,9 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
     // MODE 3 / 5 take their leaves from the fallback segment lists instead of the slots
     const int* lst = nullptr;
     int nItems = nL;
-    if constexpr (MODE == 3 || MODE == 5)
+    if constexpr (MODE == 2 || MODE == 3 || MODE == 5)
     {
-        constexpr int seg = MODE == 5 ? 0 : 1;
+        constexpr int seg = MODE == 5 ? 0 : (MODE == 3 ? 1 : 2);
         lst = aux.fbs + aux.fbs_off[seg];
         nItems = min(aux.fb_count[2 + seg], (int)aux.fbs_cap[seg]);
     }
@@ -3548,7 +3682,7 @@ struct mrlbm_ctx {
     int* err = nullptr;
     int* fbc = nullptr;
     int* fbs = nullptr; // fallback segment lists (Aux::fbs)
-    long long fbs_off[2]{}, fbs_cap[2]{};
+    long long fbs_off[3]{}, fbs_cap[3]{};
     int2* fbl = nullptr;
     unsigned* fbm = nullptr;
     unsigned* fbdm = nullptr;
@@ -3581,6 +3715,8 @@ struct mrlbm_ctx {
     // kernels (re-projecting the internal stencil neighbours costs more than the
     // second read of the children), so off by default
     bool fuse_pd = false;
+    // K8 one warp per (leaf, population) (MRLBM_K8_WARP=1, round-1 kernel) instead of one thread
+    bool k8_warp = false;
     bool gen_ok = false;  // the generated code's constants match this scheme
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
@@ -3701,7 +3837,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.step_no = c->step_no;
     a.fb1t = (c->use_fb1t && c->use_gen) ? 1 : 0;
     a.fbs = c->fbs;
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < 3; ++k)
     {
         a.fbs_off[k] = c->fbs_off[k];
         a.fbs_cap[k] = c->fbs_cap[k];
@@ -3949,7 +4085,12 @@ void enqueue_step(mrlbm_ctx* c)
         { c->kcount++; k_virtual<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, Sf, m, aux);  kmark(c, "k_virtual", m); }
     phase_mark(c, 5);
     // K7/K8 stream + collide (+ obstacle) on every new leaf
-    { c->kcount++; k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);  kmark(c, "k_stream_fallback", -1); }
+    c->kcount++;
+    if (c->k8_warp)
+        k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);
+    else
+        k_stream_fallback_t<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+    kmark(c, "k_stream_fallback", -1);
     CollC<Q, BS> cc;
     for (int i = 0; i < Q; ++i)
         for (int j = 0; j < BS; ++j)
@@ -4299,14 +4440,16 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         CU(cudaMalloc(&ctx->fbl, sizeof(int2) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbm, sizeof(unsigned) * ctx->fbcap));
         CU(cudaMalloc(&ctx->fbdm, sizeof(unsigned) * ctx->fbcap));
-        CU(cudaMalloc(&ctx->fbc, sizeof(int) * 4));
-        CU(cudaMemset(ctx->fbc, 0, sizeof(int) * 4));
+        CU(cudaMalloc(&ctx->fbc, sizeof(int) * 8));
+        CU(cudaMemset(ctx->fbc, 0, sizeof(int) * 8));
         // segment lists: capacity = the level's cell count (J1 for gap 0, J1-1 for gap 1)
         ctx->fbs_cap[0] = ctx->geo.cap[ctx->nlev - 1];
         ctx->fbs_cap[1] = ctx->nlev > 1 ? ctx->geo.cap[ctx->nlev - 2] : 0;
+        ctx->fbs_cap[2] = ctx->fbs_cap[1];
         ctx->fbs_off[0] = 0;
         ctx->fbs_off[1] = ctx->fbs_cap[0];
-        CU(cudaMalloc(&ctx->fbs, sizeof(int) * (ctx->fbs_cap[0] + ctx->fbs_cap[1] + 1)));
+        ctx->fbs_off[2] = ctx->fbs_cap[0] + ctx->fbs_cap[1];
+        CU(cudaMalloc(&ctx->fbs, sizeof(int) * (ctx->fbs_cap[0] + ctx->fbs_cap[1] + ctx->fbs_cap[2] + 1)));
         CU(cudaMalloc(&ctx->err, sizeof(int) * 4));
         CU(cudaMemset(ctx->err, 0, sizeof(int) * 4));
         CU(cudaMalloc(&ctx->upd, sizeof(long long)));
@@ -4468,6 +4611,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     ctx->use_fb1t = std::getenv("MRLBM_NO_FB1T") == nullptr;
     ctx->rim_tpl = std::getenv("MRLBM_RIM_TPL") != nullptr;
     ctx->fuse_pd = std::getenv("MRLBM_FUSE_PD") != nullptr;
+    ctx->k8_warp = std::getenv("MRLBM_K8_WARP") != nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
         const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;
