@@ -5,12 +5,18 @@ updates/s for the full step incl. adaptation; HBM GB/s vs peak).
 Workload (config.workload): BASELINE configs[4], D2Q9 Navier-Stokes past a
 cylinder, levels 2..12 (finest 8192 x 4096), epsilon = 1e-4, from its seeded
 initial datum.  A "step" is one Algorithm-1 iteration (adapt -> transfer ->
-stream -> collide -> obstacle) over the whole adaptive mesh.
+stream -> collide -> obstacle) over the whole adaptive mesh.  `value` times the
+K steps after W warm-up steps (the contract's window: the transient in which the
+mesh coarsens from the full 33.5 M-cell grid); `regimes` reports the settled mesh
+(step 200), the developing flow (step 3000) and the mean of the complete
+50 000-step BASELINE run, measured in the same process.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
+                  [--quick] [--no-cpu]
 
---impl reference times the CPU restatement of the reference path (the oracle;
-the reference ships no step of its own) on the host cores.
+--impl reference times the CPU restatement of the reference path (the oracle,
+built only from its own descriptors and initial data; the reference ships no step
+of its own) on the host cores, same config and window.
 Multi-GPU: the path does not shard in this tier (DESIGN.md: replicas only);
 every rank runs an independent replica, value = total updates / max time.
 """
@@ -27,6 +33,7 @@ sys.path.insert(0, ROOT)
 CONFIG_ID = 5
 METRIC = "MR-LBM leaf-cell updates/s (full step incl. adaptation)"
 UNIT = "leaf-updates/s"
+PHASES = ("project", "details", "flags", "compact", "transfer", "stream")
 
 
 def dist_env():
@@ -39,6 +46,16 @@ def load_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -102,71 +119,216 @@ def reduce_replicas(ms, updates, device, world):
 
 
 def snapshot(s, rc):
-    out = {}
-    for lv in range(rc.j_min, rc.j_max + 1):
-        out[lv] = s.read_leaves(lv)
-    return out
+    return {lv: s.read_leaves(lv) for lv in range(rc.j_min, rc.j_max + 1)}
 
 
-def run_cpu_sample(min_seconds=10.0, max_steps=40, jmax=10, threads=None):
-    """CPU oracle (the reference path restated on the reference headers) on a
-    bounded sample: config 5 at J_bar = jmax from its initial datum, stepping
-    until min_seconds of step time (at least 2 steps, at most max_steps)."""
+def leaves_of(st):
+    return sum(int(st.leaves[i]) for i in range(st.levels))
+
+
+def workload_name(cid, rc):
+    names = {3: "config 3: D2Q4 advection (periodic disc)", 4: "config 4: D2Q4x4 Euler 4-quadrant Riemann",
+             5: "config 5: D2Q9 Navier-Stokes past a cylinder"}
+    ext = f"finest {rc.base_cells[0] << (rc.j_max - rc.j_min)}x{rc.base_cells[1] << (rc.j_max - rc.j_min)}"
+    return f"{names[cid]}, levels {rc.j_min}..{rc.j_max} ({ext}), eps={rc.epsilon:g}"
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_leaf_updates(o, rc):
+    return sum(o.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1))
+
+
+def run_cpu_sample(snap, steps=1):
+    """cpu_baseline: the CPU oracle (the reference path restated on the reference's own
+    headers) on a BOUNDED sample of the SAME workload and window: the GPU's post-warm-up
+    state at J_bar = 12 is loaded into the oracle, which then runs `steps` steps (the
+    first step(s) of the timed window), all host threads."""
     from oracle import pyoracle
-    from paper_2103_02903_b200 import build_config, finest_cells, initial_finest
-    cores = threads or os.cpu_count() or 1
+    cores = os.cpu_count() or 1
     pyoracle.set_threads(cores)
-    sc, rc = build_config(CONFIG_ID, jmax)
+    sc, rc = pyoracle.build_config(CONFIG_ID)
     o = pyoracle.Oracle(sc, rc)
-    o.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
+    for lv, (ix, ff) in snap.items():
+        if ix.shape[0]:
+            o.load_leaves(lv, ix, ff)
     o.commit()
-    upd, secs, steps = 0, 0.0, 0
-    while steps < max_steps and (steps < 2 or secs < min_seconds):
+    upd, secs = 0, 0.0
+    for _ in range(steps):
         t = time.perf_counter()
         o.step(1)
         secs += time.perf_counter() - t
-        upd += sum(o.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1))
-        steps += 1
+        upd += oracle_leaf_updates(o, rc)
     o.close()
     return {"value": upd / secs, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"config 5 (D2Q9 cylinder) at J_bar={jmax} ({(8 << (jmax - 2)) * (4 << (jmax - 2))} finest cells), "
-                      f"{steps} oracle steps from the initial datum, {cores} threads, {secs:.2f} s"}
+            "sample": f"config 5 at J_bar=12 (8192x4096 finest), the first {steps} step(s) of the timed window "
+                      f"(the GPU's post-warm-up state loaded into the oracle), {cores} OpenMP threads on "
+                      f"{cpu_model()}, {secs:.2f} s for {upd} leaf updates"}
 
 
 def bench_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    # each step: one oracle step of the bounded sample (config 5 at J_bar = 9)
+    # the oracle with its OWN descriptors and initial datum (no product library is
+    # loaded): config 5 at J_bar = 12, W untimed warm-up steps, then K timed steps --
+    # the same configuration and window as the product arm
     from oracle import pyoracle
-    from paper_2103_02903_b200 import build_config, finest_cells, initial_finest
     cores = os.cpu_count() or 1
     pyoracle.set_threads(cores)
-    jmax = 9
-    sc, rc = build_config(CONFIG_ID, jmax)
+    sc, rc = pyoracle.build_config(CONFIG_ID, args.jmax)
     o = pyoracle.Oracle(sc, rc)
-    o.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
+    o.load_leaves(rc.j_max, pyoracle.finest_cells(sc, rc), pyoracle.initial_finest(CONFIG_ID, sc, rc))
     o.commit()
-    for _ in range(args.warmup):
-        o.step(1)
+    o.step(args.warmup)
     upd, secs = 0, 0.0
     for _ in range(args.steps):
         t = time.perf_counter()
         o.step(1)
         secs += time.perf_counter() - t
-        upd += sum(o.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1))
+        upd += oracle_leaf_updates(o, rc)
+    o.close()
     v = upd / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (config 5 initial datum, seeded perturbation)",
-        "config": {"workload": f"config 5 D2Q9 cylinder, levels 2..{jmax} (bounded CPU sample of levels 2..12)",
-                   "epsilon": rc.epsilon},
+        "config": {"workload": workload_name(CONFIG_ID, rc), "window": f"steps {args.warmup}..{args.warmup + args.steps - 1}",
+                   "parallelism": "cpu"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"config 5 at J_bar={jmax}, {args.steps} timed oracle steps after {args.warmup} warm-up"},
+                         "sample": f"config 5 at J_bar={rc.j_max}, {args.steps} timed oracle steps after {args.warmup} "
+                                   f"warm-up steps (same window as the GPU arm), {cores} OpenMP threads on {cpu_model()}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ product legs
+def phase_replay(sc, rc, snap, steps, peak):
+    """Per-phase / per-kernel CUDA-event times over the SAME steps as a timed window: a
+    second context restarts from the snapshot (bit-identical evolution) with eager
+    launches and an event after every kernel (~5-9 % slower than the graph)."""
+    from paper_2103_02903_b200 import Solver
+    sp = Solver(sc, rc)
+    for lv, (ix, ff) in snap.items():
+        if ix.shape[0]:
+            sp.load_leaves(lv, ix, ff)
+    sp.commit()
+    sp.set_profiling(True)
+    ms = [0.0] * len(PHASES)
+    by = [0] * len(PHASES)
+    fin_bytes = 0
+    for _ in range(steps):
+        st = sp.step(1)
+        for i in range(len(PHASES)):
+            ms[i] += st.ms_phase[i]
+            by[i] += st.bytes_phase[i]
+        fin_bytes += 16 * sc.q * int(st.leaves[st.levels - 1])
+    kern = sp.profile_text()
+    sp.close()
+    phases = {}
+    for i, p in enumerate(PHASES):
+        m, b = ms[i] / steps, by[i] / steps
+        e = {"ms": m, "algorithmic_bytes": b}
+        if b:
+            gbs = b / (m / 1e3) / 1e9 if m > 0 else 0.0
+            e.update({"gbs": gbs, "frac": gbs / peak})
+        phases[p] = e
+    kernels = {}
+    for (kname, lv), (kms, kn) in kern.items():
+        kernels[kname] = kernels.get(kname, 0.0) + kms / steps
+    fin_ms = kern.get(("k_stream_collide", rc.j_max), (0.0, 0))[0] / steps
+    return phases, kernels, fin_ms, fin_bytes / steps
+
+
+def timed_window(s, stream, flush, steps, local):
+    """K steps, each bracketed by CUDA events on the context's stream; the L2 is
+    flushed between steps (outside the events).  Returns (ms, updates, stats, launches, clocks)."""
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    u0 = None
+    launches = 0
+    st = None
+    with ClockSampler(local) as clk:
+        for k in range(steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+            evs[k][0].record(stream)
+            st = s.step(1)
+            evs[k][1].record(stream)
+            if u0 is None:
+                u0 = st.leaf_updates - leaves_of(st)
+            launches += st.kernel_launches
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    return ms, st.leaf_updates - u0, st, launches, clk.summary()
+
+
+def regimes_run(sc, rc):
+    """The complete BASELINE run (50 000 steps) on a fresh context, chunked: device time
+    per chunk (CUDA events around back-to-back graph launches); the settled (steps
+    200..219) and developing (3000..3019) regimes are chunks of it."""
+    from paper_2103_02903_b200 import Solver, config_steps, finest_cells, initial_finest
+    n = int(config_steps(CONFIG_ID, rc))
+    s = Solver(sc, rc)
+    s.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
+    s.commit()
+    marks = [(200, 20, "settled"), (3000, 20, "developing")]
+    done, ms_tot, upd_prev, upd_tot = 0, 0.0, 0, 0
+    out = {}
+    # chunk list: run to each mark, then the marked window, then the rest
+    chunks = []
+    pos = 0
+    for at, k, name in marks:
+        while pos < at:
+            c = min(2000, at - pos)
+            chunks.append((c, None))
+            pos += c
+        chunks.append((k, name))
+        pos += k
+    while pos < n:
+        c = min(2000, n - pos)
+        chunks.append((c, None))
+        pos += c
+    t0 = time.time()
+    for c, name in chunks:
+        st = s.step(c)
+        done += c
+        ms_tot += st.ms_total
+        du = st.leaf_updates - upd_prev
+        upd_prev = st.leaf_updates
+        upd_tot += du
+        if name:
+            out[name] = {"steps": f"{done - c}..{done - 1}", "ms_per_step": st.ms_total / c,
+                         "value": du / (st.ms_total / 1e3), "leaves_last_step": leaves_of(st),
+                         "step_bytes_model": st.bytes_model,
+                         "step_frac_of_model": st.bytes_model / (st.ms_total / c / 1e3) / 1e9 / load_peaks()[0]}
+    s.close()
+    out["full_run"] = {"steps": n, "device_s": ms_tot / 1e3, "ms_per_step": ms_tot / n,
+                       "value": upd_tot / (ms_tot / 1e3), "wall_s": time.time() - t0}
+    return out
+
+
+def other_config(cid, jmax, warmup, steps, flush, peak):
+    """Secondary bench line of another 2D config (not the headline): W warm-up, K timed."""
+    import torch
+    from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
+    sc, rc = build_config(cid, jmax)
+    s = Solver(sc, rc)
+    s.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(cid, sc, rc))
+    s.commit()
+    s.step(warmup)
+    snap = snapshot(s, rc)
+    stream = torch.cuda.ExternalStream(s.stream_handle(), device=torch.device("cuda", torch.cuda.current_device()))
+    ms, upd, st, _, _ = timed_window(s, stream, flush, steps, torch.cuda.current_device())
+    s.close()
+    phases, kernels, _, _ = phase_replay(sc, rc, snap, steps, peak)
+    model = sum(p["algorithmic_bytes"] for p in phases.values())
+    step_ms = ms / steps
+    return {"workload": workload_name(cid, rc), "warmup": warmup, "steps": steps, "value": upd / (ms / 1e3),
+            "unit": UNIT, "ms_per_step": step_ms, "leaves_last_step": leaves_of(st),
+            "step_roofline": {"bytes_model_per_step": model, "achieved_gbs": model / (step_ms / 1e3) / 1e9,
+                              "frac": model / (step_ms / 1e3) / 1e9 / peak},
+            "phases": phases}
 
 
 def bench_product(args):
@@ -179,18 +341,15 @@ def bench_product(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
-    from paper_2103_02903_b200.abi import PHASES
 
+    peak, peak_kind = load_peaks()
     sc, rc = build_config(CONFIG_ID, args.jmax)
-    idx0, f0 = finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc)
     s = Solver(sc, rc)
-    s.load_leaves(rc.j_max, idx0, f0)
+    s.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(CONFIG_ID, sc, rc))
     s.commit()
     stream = torch.cuda.ExternalStream(s.stream_handle(), device=dev)
-    # warm-up (also evolves the state into the measured regime)
-    st = s.step(args.warmup)
-    # state snapshot for the e2e leg (same K steps, through host buffers)
-    snap = snapshot(s, rc)
+    s.step(args.warmup)  # warm-up: also evolves the state into the measured window
+    snap = snapshot(s, rc)  # post-warm-up state: e2e leg, phase replay, CPU sample
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def barrier():
@@ -198,88 +357,25 @@ def bench_product(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-timed region: K steps, L2 flushed between steps (outside the events)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    u0 = st.leaf_updates
+    # ---- device-timed region
     barrier()
-    launches = 0
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(k & 0xFF)
-            evs[k][0].record(stream)
-            st = s.step(1)
-            evs[k][1].record(stream)
-            launches += st.kernel_launches
+    ms, updates, st, launches, clocks = timed_window(s, stream, flush, args.steps, local)
     barrier()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
-    updates = st.leaf_updates - u0
-    clocks = clk.summary()
     ms_max, utot = reduce_replicas(ms, updates, dev, world)
     value = utot / (ms_max / 1e3)
-    state_bytes = 8 * sc.q * sum(int(st.leaves[i]) for i in range(st.levels))
-
     end_counts = {lv: s.level_count(lv) for lv in range(rc.j_min, rc.j_max + 1)}
+    s.close()
 
-    # ---- phase breakdown over the SAME K steps as the timed window: a second context
-    # restarts from the post-warm-up state (bit-identical evolution) with eager launches
-    # and CUDA events after every phase / kernel on the context's stream (~5-9 % slower
-    # than the graph, so the per-phase bandwidths below are conservative)
-    sprof = Solver(sc, rc)
-    for lv, (ix, ff) in snap.items():
-        sprof.load_leaves(lv, ix, ff)
-    sprof.commit()
-    sprof.set_profiling(True)
-    nprof = args.steps
-    phase_tot = [0.0] * len(PHASES)
-    stream_bytes_tot, model_bytes_tot, fin_bytes_tot = 0, 0, 0
-    for _ in range(nprof):
-        sp = sprof.step(1)
-        for i in range(len(PHASES)):
-            phase_tot[i] += sp.ms_phase[i]
-        stream_bytes_tot += sp.bytes_stream      # per-step algorithmic bytes
-        model_bytes_tot += sp.bytes_model
-        # finest-level table stream + collision (K7 gap 0): read f* of the level's leaves and
-        # ghosts, write the leaves (boundary-rim fallback leaves are a negligible part)
-        nl, nv = int(sp.leaves[sp.levels - 1]), int(sp.virtual_cells[sp.levels - 1])
-        fin_bytes_tot += 8 * sc.q * (2 * nl + nv)
-    kern_prof = sprof.profile_text()
-    sprof.close()
-    phase_ms = {p: phase_tot[i] / nprof for i, p in enumerate(PHASES)}
-    stream_kernels = {}
-    for (kname, lv), (kms, kn) in kern_prof.items():
-        if kname.startswith(("k_stream", "k_fb1")):
-            stream_kernels[kname] = stream_kernels.get(kname, 0.0) + kms / nprof
-    fin_ms = kern_prof.get(("k_stream_collide", rc.j_max), (0.0, 0))[0] / nprof
-    fin_bytes = fin_bytes_tot / nprof
-    dom = max(phase_ms, key=phase_ms.get)
-    peak, peak_kind = load_peaks()
-    stream_bytes = stream_bytes_tot / nprof
-    model_bytes = model_bytes_tot / nprof
-    achieved = stream_bytes / (phase_ms["stream"] / 1e3) / 1e9 if phase_ms["stream"] > 0 else 0.0
-    step_ms_prof = sum(phase_ms.values())
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "ncu_stream_traffic.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get("bytes_per_step")
-        except Exception:
-            traffic = None
+    # ---- per-phase / per-kernel breakdown of the same K steps
+    phases, kernels, fin_ms, fin_bytes = phase_replay(sc, rc, snap, args.steps, peak)
+    stream_kernels = {k: v for k, v in kernels.items() if k.startswith(("k_stream", "k_fb1"))}
+    sp = phases["stream"]
+    dom = max(phases, key=lambda p: phases[p]["ms"])
+    model_bytes = sum(p["algorithmic_bytes"] for p in phases.values())
+    step_ms = ms_max / args.steps
 
-    # ---- steady regime (context only, not the headline): after the white-noise
-    # transient the mesh settles (~0.9 M leaves); continue the run to step 200
-    steady = None
-    if args.steady and world == 1:
-        done = args.warmup + args.steps
-        if done < 200:
-            s.step(200 - done)
-        ss = s.step(20)
-        steady = {"after_steps": 200, "steps": 20, "ms_per_step": ss.ms_total / 20,
-                  "value": ss.leaf_updates and (sum(int(ss.leaves[i]) for i in range(ss.levels)) / (ss.ms_total / 20 / 1e3)),
-                  "leaves": sum(int(ss.leaves[i]) for i in range(ss.levels))}
-
-    # ---- e2e through the C-ABI with host buffers: load snapshot -> commit -> K steps -> read back.
-    # Host buffers are pinned (page-locked) as the contract asks; allocation is outside the timing.
+    # ---- e2e through the C-ABI with pinned host buffers: load the post-warm-up snapshot ->
+    # commit -> K steps -> read every level back (H2D and D2H inside the timing)
     def pinned_like(a):
         t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype).pin_memory()
         return t.numpy()
@@ -290,8 +386,6 @@ def bench_product(args):
         pi_[...] = ix
         pf_[...] = ff
         snap_p[lv] = (pi_, pf_)
-    # read-back buffers: pinned, sized by the level counts the timed run ended with (the
-    # e2e context replays the same deterministic K steps from the same state)
     out_flat = {lv: (pinned_like(np.zeros(sc.d * end_counts[lv] + 16, np.int32)),
                      pinned_like(np.zeros(sc.q * end_counts[lv] + 16)))
                 for lv in snap}
@@ -300,7 +394,8 @@ def bench_product(args):
     barrier()
     t0 = time.perf_counter()
     for lv, (ix, ff) in snap_p.items():
-        s2.load_leaves(lv, ix, ff)
+        if ix.shape[0]:
+            s2.load_leaves(lv, ix, ff)
     s2.commit()
     st2 = s2.step(args.steps)
     d2h = 0
@@ -318,54 +413,61 @@ def bench_product(args):
     e2e_val = e2e_u / e2e_smax
     s2.close()
 
-    cpu = None
+    regimes, others, cpu = None, None, None
+    if world == 1 and not args.quick:
+        regimes = regimes_run(sc, rc)
+        others = [other_config(4, 11, 5, 20, flush, peak), other_config(3, 9, 5, 10, flush, peak)]
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = run_cpu_sample()
+        cpu = run_cpu_sample(snap)
 
     if rank == 0:
-        leaves_last = [int(st.leaves[i]) for i in range(st.levels)]
-        internal_last = [int(st.internal[i]) for i in range(st.levels)]
-        virtual_last = [int(st.virtual_cells[i]) for i in range(st.levels)]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (config 5 initial datum: rest + seeded 1e-3 transverse perturbation)",
-            "config": {"workload": "config 5: D2Q9 Navier-Stokes past a cylinder, levels 2..%d (finest %dx%d), "
-                                   "eps=1e-4, Re=1200" % (rc.j_max, 8 << (rc.j_max - 2), 4 << (rc.j_max - 2)),
+            "config": {"workload": workload_name(CONFIG_ID, rc),
+                       "window": f"steps {args.warmup}..{args.warmup + args.steps - 1} from the seeded initial "
+                                 f"datum (transient: the mesh coarsens from the full grid; see regimes)",
                        "parallelism": "replicas" if world > 1 else "single-gpu",
-                       "l2": f"flushed between timed steps (256 MiB write); state {state_bytes / 1e6:.0f} MB",
-                       "leaves_per_level_last_step": leaves_last,
-                       "internal_per_level_last_step": internal_last,
-                       "virtual_per_level_last_step": virtual_last,
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "leaves_per_level_last_step": [int(st.leaves[i]) for i in range(st.levels)],
+                       "internal_per_level_last_step": [int(st.internal[i]) for i in range(st.levels)],
+                       "virtual_per_level_last_step": [int(st.virtual_cells[i]) for i in range(st.levels)],
                        "fallback_leaves_last_step": int(st.fallback_leaves)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "stream+collide phase per step (K8 k_stream_fallback, k_fb1, K7 k_stream_collide: "
-                                   "gap-1 fallback thread-per-leaf k_fb1t, finest level, coarser levels, other fallback)",
-                         "algorithmic_bytes": stream_bytes, "peak_kind": peak_kind,
+            "roofline": {"bound": "hbm", "achieved": sp.get("gbs", 0.0), "peak": peak, "unit": "GB/s",
+                         "frac": sp.get("frac", 0.0), "traffic": None,
+                         "kernel": "stream+collide phase per step (K8 k_stream_fallback, k_fb1, K7 k_stream_collide "
+                                   "variants: finest level, coarser levels, gap-1 fallback list, fallback rims)",
+                         "algorithmic_bytes": sp["algorithmic_bytes"],
+                         "bytes_rule": "8 q (2 N_S): read f* and write f of every leaf of the new tree",
+                         "peak_kind": peak_kind,
                          "timing": "CUDA events per kernel on the context stream over the same K steps as the "
                                    "timed window (eager replay from the post-warm-up state)",
+                         "traffic_note": "DRAM bytes are not measured in this run; ncu captures are in profiles/",
                          "kernels_ms_per_step": stream_kernels},
             "kernel_roofline": {"kernel": "K7 finest level (gap-0 table stream + MRT collision), per launch",
                                 "algorithmic_bytes": fin_bytes, "ms": fin_ms,
                                 "achieved_gbs": fin_bytes / (fin_ms / 1e3) / 1e9 if fin_ms > 0 else 0.0,
                                 "frac": (fin_bytes / (fin_ms / 1e3) / 1e9 / peak) if fin_ms > 0 else 0.0},
             "step_roofline": {"bytes_model_per_step": model_bytes,
-                              "achieved_gbs": model_bytes / (ms_max / args.steps / 1e3) / 1e9,
-                              "frac": model_bytes / (ms_max / args.steps / 1e3) / 1e9 / peak},
-            "phases_ms": phase_ms, "dominant_phase": dom,
+                              "achieved_gbs": model_bytes / (step_ms / 1e3) / 1e9,
+                              "frac": model_bytes / (step_ms / 1e3) / 1e9 / peak,
+                              "model": "SURVEY 8d compulsory fp64 bytes with N_G = 0, old-tree counts per step"},
+            "phases": phases, "dominant_phase": dom,
+            "kernels_ms_per_step": kernels,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps},
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if regimes is not None:
+            line["regimes"] = regimes
+        if others is not None:
+            line["other_configs"] = others
         if cpu is not None:
             line["cpu_baseline"] = cpu
-        if steady is not None:
-            line["steady_state"] = steady
         print(json.dumps(line))
-    s.close()
     if world > 1:
         torch.distributed.destroy_process_group()
 
@@ -373,12 +475,12 @@ def bench_product(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--jmax", type=int, default=0, help="override J_bar (default: config value 12)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--no-steady", dest="steady", action="store_false", help="skip the steady-regime context run")
+    ap.add_argument("--quick", action="store_true", help="skip the regimes run and the other configs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -112,6 +112,11 @@ typedef struct mrlbm_step_stats {
     int64_t bytes_model;                   /* algorithmic fp64 bytes of the last step (SURVEY 8d model) */
     int64_t bytes_stream;                  /* algorithmic bytes of the last step's stream+collide phase */
     int64_t kernel_launches;               /* CUDA kernels this call launched (graph nodes included) */
+    /* algorithmic fp64 bytes of the LAST step per phase (MRLBM_PHASE_*), SURVEY 8d model with the
+       old-tree counts taken before that step and N_G = 0 (virtual cells are not compulsory traffic):
+       project 8q(N_S,old + 2 N_I,old), details 8q(N_S,old + N_I,old), flags / compact 0 (integer),
+       transfer 8q(3 N_S,new + N_I,new), stream 8q(2 N_S,new); bytes_model = their sum */
+    int64_t bytes_phase[8];
 } mrlbm_step_stats;
 
 enum {

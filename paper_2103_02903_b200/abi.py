@@ -57,6 +57,7 @@ class StepStats(C.Structure):
         ("bytes_model", C.c_int64),
         ("bytes_stream", C.c_int64),
         ("kernel_launches", C.c_int64),
+        ("bytes_phase", C.c_int64 * 8),
     ]
 
 

@@ -18,8 +18,10 @@ NVCC_FLAGS = [
 
 def build(verbose=False):
     gen = os.path.join(HERE, "csrc", "stream_gen.cuh")
-    if not os.path.exists(gen):
-        subprocess.run([sys.executable, os.path.join(HERE, "csrc", "gen_stream.py")], check=True)
+    gen_src = [os.path.join(HERE, "csrc", "gen_stream.py"), os.path.join(HERE, "csrc", "collide_patterns.json")]
+    # regenerate the unrolled table code whenever its generator (or its input) is newer
+    if not os.path.exists(gen) or any(os.path.getmtime(p) > os.path.getmtime(gen) for p in gen_src if os.path.exists(p)):
+        subprocess.run([sys.executable, gen_src[0]], check=True)
     deps = SRC + [os.path.join(HERE, "csrc", "mrlbm_internal.h"), gen, os.path.join(ROOT, "include", "mrlbm_gpu.h")]
     if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(p) for p in deps):
         return OUT

@@ -115,6 +115,9 @@ struct Aux {
                         //     counts at fb_count[2 + seg]
     long long fbs_off[3], fbs_cap[3];
     double* frc;
+    // obstacle volume fractions alpha(m, x, y), precomputed at create over the same
+    // per-level boxes as the force terms (frc_off / 2 = cell offset); null: no obstacle
+    const double* alpha_tab;
     // near-threshold tie log (north_star): records of group metrics within
     // 1e-12 relative of eps_l or 2^{mu+d} eps_l; step_no = steps completed since commit
     mrlbm_tie_record* ties;
@@ -292,10 +295,12 @@ __device__ __forceinline__ void flag_err(int* err, int which)
     atomicAdd(&err[which], 1);
 }
 
-// warp-aggregated append: one atomicAdd per group of lanes that arrive together
-__device__ __forceinline__ int agg_inc(int* ctr)
+// warp-aggregated append: the lanes that arrive together and target the same counter
+// (same key) share one atomicAdd; lanes of one call site may append to different lists
+__device__ __forceinline__ int agg_inc(int* ctr, unsigned key)
 {
-    cg::coalesced_group grp = cg::coalesced_threads();
+    const cg::coalesced_group arrived = cg::coalesced_threads();
+    const cg::coalesced_group grp = cg::labeled_partition(arrived, key);
     int base = 0;
     if (grp.thread_rank() == 0)
         base = atomicAdd(ctr, (int)grp.size());
@@ -933,6 +938,75 @@ __global__ void k_grade_v(const __grid_constant__ Geo g, const __grid_constant__
     }
 }
 
+// The gap-1 fallback leaves without domain-leaving pairs (the bulk of the fallback
+// leaves, K7 MODE 2), listed tile by tile: one block per 16 x 16 tile of level J1-1
+// (1D: 256 cells), the tile's leaves in tile order, one atomicAdd per tile.  MODE 2
+// takes consecutive list entries, so a warp's leaves are spatial neighbours and their
+// 5 x 5 boxes and finest rings are L1 / L2 hits instead of DRAM re-reads.  (An append
+// from the classification kernel lists them in arrival order: measured 5.9 GB of DRAM
+// reads per transient step for MODE 2, L2 hit rate 19 %.)  The tiles' order in the
+// list is unspecified; every leaf's result is independent of it (bit-exact).
+template <int D>
+__global__ void __launch_bounds__(256) k_list_fb1(const __grid_constant__ Geo g, const __grid_constant__ Flags fl,
+                                                  const __grid_constant__ Aux aux)
+{
+    const int li = g.nlev - 2;
+    const int nx = g.nx[li], ny = D == 1 ? 1 : g.ny[li];
+    const int tny = D == 1 ? 1 : (ny + 15) >> 4;
+    const long long ntiles = D == 1 ? ((long long)nx + 255) / 256 : (long long)((nx + 15) >> 4) * tny;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ int woff[8];
+    __shared__ int sbase;
+    int* out = aux.fbs + aux.fbs_off[2];
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x)
+    {
+        int x, y;
+        if (D == 1)
+        {
+            x = (int)t * 256 + threadIdx.x;
+            y = 0;
+        }
+        else
+        {
+            const int tx = (int)(t / tny), ty = (int)(t - (long long)tx * tny);
+            x = tx * 16 + (threadIdx.x >> 4);
+            y = ty * 16 + (threadIdx.x & 15);
+        }
+        bool pick = false;
+        int lin = 0;
+        if (x < nx && y < ny)
+        {
+            lin = xy2lin<D>(x, y, ny);
+            pick = fl.kind[li][lin] == (K_LEAF | K_FB) && fl.fbd[li][vix<D>(x, y, ny)] == 0u;
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, pick);
+        if (lane == 0)
+            woff[wid] = __popc(b);
+        __syncthreads();
+        if (threadIdx.x == 0)
+        {
+            int tot = 0;
+            for (int w = 0; w < 8; ++w)
+            {
+                const int c = woff[w];
+                woff[w] = tot;
+                tot += c;
+            }
+            sbase = tot ? atomicAdd(aux.fb_count + 4, tot) : 0;
+        }
+        __syncthreads();
+        if (pick)
+        {
+            const int k = sbase + woff[wid] + __popc(b & ((1u << lane) - 1u));
+            if (k < aux.fbs_cap[2])
+                out[k] = lin;
+            else
+                flag_err(aux.err, 2);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- K4 kinds, fallback, ghosts, compaction
 template <int D>
 __global__ void k_kinds(const __grid_constant__ Geo g, const __grid_constant__ Flags fl, const __grid_constant__ LGrid lg_)
@@ -1226,14 +1300,14 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     fl.fbm[li][vi] = mask;
     fl.fbd[li][vi] = dmask;
     fl.kind[li][i] = K_LEAF | K_FB;
-    // segment lists (thread-per-leaf path): gap-0 fallback leaves, gap-1 leaves whose
-    // pairs leave the domain, and the other gap-1 leaves, streamed by K7 MODE 5 / k_fb1
-    // (or MODE 3) / MODE 2 from the lists, so no warp of those kernels idles on the
-    // leaves it does not take.  One atomic per coalesced group of lanes.
-    if (aux.fb1t && gap <= 1)
+    // segment lists (thread-per-leaf path): gap-0 fallback leaves and gap-1 leaves whose
+    // pairs leave the domain, streamed by K7 MODE 5 / k_fb1 (or MODE 3) from the lists;
+    // the other gap-1 leaves are listed tile by tile afterwards (k_list_fb1, MODE 2).
+    // One atomic per coalesced group of lanes.
+    if (aux.fb1t && (gap == 0 || (gap == 1 && dmask != 0)))
     {
-        const int seg = gap == 0 ? 0 : (dmask != 0 ? 1 : 2);
-        const int k = agg_inc(aux.fb_count + 2 + seg);
+        const int seg = gap == 0 ? 0 : 1;
+        const int k = agg_inc(aux.fb_count + 2 + seg, (unsigned)seg);
         if (k < aux.fbs_cap[seg])
             aux.fbs[aux.fbs_off[seg] + k] = (int)i;
         else
@@ -1242,7 +1316,7 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
     // listed: deep-gap leaves (K8, bands)
     if (gap >= 2)
     {
-        const int k = agg_inc(aux.fb_count);
+        const int k = agg_inc(aux.fb_count, 0u);
         if (k < aux.fb_cap)
         {
             aux.fb_list[k] = make_int2(m, (int)i);
@@ -2161,8 +2235,17 @@ __device__ __forceinline__ double rim_value(const Geo& g, const Tree& tn, const 
     const int kind = sc->bc_kind[face];
     if (kind == MRLBM_BC_COPY)
     {
-        // value of the leaf covering the clamped finest cell
+        // value of the leaf covering the clamped finest cell: usually the streaming leaf
+        // itself (its rim leaves the domain across the face it touches), found without a
+        // search; otherwise the covering leaf is searched level by level
         const int cx = mr_coord(x, nx, 0), cy = D == 2 ? mr_coord(y, ny, 0) : 0;
+        {
+            const int gl = lj - leaf_li;
+            int lx, ly;
+            lin2xy_l<D>((int)leaf_lin, g.ny[leaf_li], g.lny[leaf_li], lx, ly);
+            if ((cx >> gl) == lx && (D == 1 || (cy >> gl) == ly))
+                return S.f[leaf_li][(long long)h * g.cap[leaf_li] + vix<D>(lx, ly, g.ny[leaf_li])];
+        }
         for (int m = g.J1; m >= g.J0; --m)
         {
             const int li = m - g.J0;
@@ -2552,6 +2635,26 @@ __device__ __forceinline__ double obstacle_alpha(const SchemeDev* scg, int m, in
         }
     }
     return cnt > 0 ? __ddiv_rn((double)cnt, (double)(ns * ns)) : 0.0;
+}
+
+// alpha of a leaf from the table built at create (k_alpha_table: obstacle_alpha of every
+// cell of the per-level boxes around the disc), 0 outside the box: the geometry is
+// static, so the hot kernels do one load instead of 16 x 16 sub-samples per step
+__device__ __forceinline__ double obstacle_alpha_cached(const Aux& aux, int li, int x, int y)
+{
+    const int bx = x - aux.frc_x0[li], by = y - aux.frc_y0[li];
+    if (bx < 0 || by < 0 || bx >= aux.frc_nx[li] || by >= aux.frc_ny[li])
+        return 0.0;
+    return aux.alpha_tab[(aux.frc_off[li] >> 1) + (long long)bx * aux.frc_ny[li] + by];
+}
+
+__global__ void k_alpha_table(const SchemeDev* scg, int m, int x0, int y0, int nx, int ny, double* out)
+{
+    GRID_STRIDE(i, 0, (long long)nx * ny)
+    {
+        const int bx = (int)(i / ny), by = (int)(i - (long long)bx * ny);
+        out[i] = obstacle_alpha(scg, m, x0 + bx, y0 + by);
+    }
 }
 
 // obstacle force term of one leaf (oracle force_terms): the momentum the blend removes
@@ -3056,7 +3159,7 @@ __global__ void __launch_bounds__(32 * Q) k_fb1(const __grid_constant__ Geo g, c
                 {
                     int x, y;
                     lin2xy_l<D>(sLin[k], ny, g.lny[li], x, y);
-                    alpha = obstacle_alpha(scg, m, x, y);
+                    alpha = obstacle_alpha_cached(aux, li, x, y);
                     if constexpr (FRC)
                         if (alpha > 0.0)
                             force_store(aux, g, scg, m, x, y, alpha, sMo[1][k], sMo[2][k]);
@@ -3414,7 +3517,7 @@ __global__ void __launch_bounds__(256, GC == 1 ? 2 : 3)
             {
                 int x, y;
                 lin2xy_l<D>(lin, ny, g.lny[li], x, y);
-                const double alpha = obstacle_alpha(scg, m, x, y);
+                const double alpha = obstacle_alpha_cached(aux, li, x, y);
                 if (alpha > 0.0)
                 {
                     if constexpr (FRC)
@@ -3728,6 +3831,7 @@ struct mrlbm_ctx {
     int* ld_bad = nullptr;
     // obstacle force tracking (mrlbm_set_force_tracking)
     double* frc = nullptr;
+    double* alpha_tab = nullptr; // obstacle alpha per cell of the boxes (Aux::alpha_tab)
     long long frc_n = 0; // cells over all level boxes
     long long frc_off[kL]{};
     int frc_x0[kL]{}, frc_y0[kL]{}, frc_nx[kL]{}, frc_ny[kL]{};
@@ -3831,6 +3935,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.pmask = c->pmaskd;
     a.umask = c->umaskd;
     a.frc = c->frc;
+    a.alpha_tab = c->alpha_tab;
     a.ties = c->ties;
     a.tie_n = c->tie_n;
     a.tie_cap = c->tie_cap;
@@ -4050,6 +4155,12 @@ void enqueue_step(mrlbm_ctx* c)
         c->kcount++;
         k_fallback_v<<<nb, T, 0, s>>>(g, fl, lg, aux);
         kmark(c, "k_fallback_v", -1);
+    }
+    if (GEN && c->use_fb1t && c->J1 > c->J0)
+    {
+        c->kcount++;
+        k_list_fb1<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);
+        kmark(c, "k_list_fb1", -1);
     }
     { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);  kmark(c, "k_band", -1); }
     if (mv > c->J0)
@@ -4337,6 +4448,8 @@ int check_device_errors(mrlbm_ctx* ctx)
 
 extern "C" {
 
+static int init_obstacle(mrlbm_ctx* ctx);
+
 int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_ctx** out)
 {
     *out = nullptr;
@@ -4598,6 +4711,8 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
         for (auto& e : ctx->ev)
             CU(cudaEventCreate(&e));
         ctx->gen_ok = gen_constants_match(sc, ctx->nlev, idx, w);
+        if (rc->obstacle == 1 && sc->d == 2 && sc->equilibrium == MRLBM_EQ_NS_D2Q9)
+            return init_obstacle(ctx);
         return MRLBM_OK;
     }();
     if (st != MRLBM_OK)
@@ -4750,6 +4865,11 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
     if (!ctx->committed)
         return set_err(ctx, MRLBM_ERR_STATE, "step before commit");
     StepFn fn = step_fn(ctx->D, ctx->q, ctx->sc.nblocks, ctx->sc.equilibrium, ctx->use_gen);
+    // old-tree counts before the last step (per-phase byte model); one small read-back
+    // per call, only when statistics are requested
+    int old_counts[4 * kL] = {0};
+    if (stats && nsteps == 1)
+        CU(cudaMemcpy(old_counts, ctx->cnt[ctx->cur], sizeof(old_counts), cudaMemcpyDeviceToHost));
     CU(cudaMemsetAsync(ctx->err, 0, sizeof(int) * 4, ctx->stream));
     CU(cudaEventRecord(ctx->ev[14], ctx->stream));
     double phase[MRLBM_PHASE_COUNT] = {0};
@@ -4826,10 +4946,26 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
         }
         stats->fallback_leaves = fb[0] + fb[1];
         stats->kernel_launches = ctx->kernels_per_step * nsteps;
-        stats->bytes_stream = 8LL * ctx->q * (2 * nS + nG);
         stats->leaf_updates = upd;
-        // SURVEY 8d compulsory fp64 model with N_old ~ N_new (last step's counts)
-        stats->bytes_model = 8LL * ctx->q * (2 * nS + 3 * nI + 5 * nS + nI + 2 * nG);
+        // SURVEY 8d compulsory fp64 model per phase.  Old-tree counts: read before the step
+        // when the call ran one step, else approximated by the new ones.  N_G = 0: the
+        // virtual (ghost + band) cells this design materialises are not compulsory traffic.
+        (void)nG;
+        long long oS = 0, oI = 0;
+        for (int li = 0; li < ctx->nlev; ++li)
+        {
+            oS += nsteps == 1 ? old_counts[li * 4] : counts[li * 4];
+            oI += nsteps == 1 ? old_counts[li * 4 + 1] : counts[li * 4 + 1];
+        }
+        const long long b8 = 8LL * ctx->q;
+        stats->bytes_phase[MRLBM_PHASE_PROJECT] = b8 * (oS + 2 * oI);
+        stats->bytes_phase[MRLBM_PHASE_DETAILS] = b8 * (oS + oI);
+        stats->bytes_phase[MRLBM_PHASE_TRANSFER] = b8 * (3 * nS + nI);
+        stats->bytes_phase[MRLBM_PHASE_STREAM] = b8 * (2 * nS);
+        stats->bytes_stream = stats->bytes_phase[MRLBM_PHASE_STREAM];
+        stats->bytes_model = 0;
+        for (int k = 0; k < MRLBM_PHASE_COUNT; ++k)
+            stats->bytes_model += stats->bytes_phase[k];
     }
     return st;
 }
@@ -5043,25 +5179,15 @@ static void free_force(mrlbm_ctx* ctx)
     ctx->frc = nullptr;
     ctx->fhist = nullptr;
     ctx->fhn = nullptr;
-    ctx->frc_n = 0;
     ctx->fcap = 0;
 }
 
-int mrlbm_set_force_tracking(mrlbm_ctx* ctx, int capacity_steps)
+// obstacle boxes: per level, the cells whose box can meet the disc's bounding box
+// (obstacle_alpha's rejection test) plus two cells of margin, clipped to the level box;
+// their alpha values are tabulated once (k_alpha_table), bit-identical to computing
+// them per step
+static int init_obstacle(mrlbm_ctx* ctx)
 {
-    if (!ctx)
-        return MRLBM_ERR_CONFIG;
-    if (capacity_steps < 0)
-        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking: negative capacity");
-    if (capacity_steps > 0 && !(ctx->rc.obstacle == 1 && ctx->D == 2 && ctx->sc.equilibrium == MRLBM_EQ_NS_D2Q9))
-        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking needs the D2Q9 obstacle configuration (obstacle = 1)");
-    CU(cudaStreamSynchronize(ctx->stream));
-    drop_graphs(ctx);
-    free_force(ctx);
-    if (capacity_steps == 0)
-        return MRLBM_OK;
-    // per level, the cells whose box can meet the disc's bounding box (obstacle_alpha's
-    // rejection test) plus one cell of margin, clipped to the level box
     long long tot = 0;
     for (int li = 0; li < ctx->nlev; ++li)
     {
@@ -5087,6 +5213,31 @@ int mrlbm_set_force_tracking(mrlbm_ctx* ctx, int capacity_steps)
         tot += static_cast<long long>(n[0]) * n[1];
     }
     ctx->frc_n = tot;
+    CU(cudaMalloc(&ctx->alpha_tab, sizeof(double) * std::max(tot, 1LL)));
+    for (int li = 0; li < ctx->nlev; ++li)
+        if (ctx->frc_nx[li] > 0 && ctx->frc_ny[li] > 0)
+            k_alpha_table<<<grid_for(ctx, (long long)ctx->frc_nx[li] * ctx->frc_ny[li]), 256, 0, ctx->stream>>>(
+                ctx->sch, ctx->J0 + li, ctx->frc_x0[li], ctx->frc_y0[li], ctx->frc_nx[li], ctx->frc_ny[li],
+                ctx->alpha_tab + ctx->frc_off[li]);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MRLBM_OK;
+}
+
+int mrlbm_set_force_tracking(mrlbm_ctx* ctx, int capacity_steps)
+{
+    if (!ctx)
+        return MRLBM_ERR_CONFIG;
+    if (capacity_steps < 0)
+        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking: negative capacity");
+    if (capacity_steps > 0 && !(ctx->rc.obstacle == 1 && ctx->D == 2 && ctx->sc.equilibrium == MRLBM_EQ_NS_D2Q9))
+        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking needs the D2Q9 obstacle configuration (obstacle = 1)");
+    CU(cudaStreamSynchronize(ctx->stream));
+    drop_graphs(ctx);
+    free_force(ctx);
+    if (capacity_steps == 0)
+        return MRLBM_OK;
+    const long long tot = ctx->frc_n;
     CU(cudaMalloc(&ctx->frc, sizeof(double) * 2 * std::max(tot, 1LL)));
     CU(cudaMalloc(&ctx->fhist, sizeof(double) * 2 * capacity_steps));
     CU(cudaMalloc(&ctx->fhn, sizeof(int)));
@@ -5188,6 +5339,7 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
         if (gph)
             cudaGraphExecDestroy(gph);
     free_force(ctx);
+    cudaFree(ctx->alpha_tab);
     cudaFree(ctx->rdcnt);
     for (int v = 0; v < 2; ++v)
     {

@@ -1,6 +1,9 @@
-"""Warm per-kernel device times (CUDA events after every launch) for a config.
+"""Warm per-kernel device times (CUDA events after every launch) over a bench window.
 
-  python tools/kprof.py --config 5 --warmup 3 --steps 3
+  python tools/kprof.py --config 5 --warmup 5 --steps 20
+
+The graph-timed steps and the profiled (eager, event after every kernel) steps are
+the SAME window: both contexts start from the post-warm-up state.
 """
 import argparse
 import os
@@ -12,24 +15,31 @@ from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_fi
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--jmax", type=int, default=0)
-ap.add_argument("--warmup", type=int, default=3)
-ap.add_argument("--steps", type=int, default=3)
-ap.add_argument("--top", type=int, default=40)
+ap.add_argument("--warmup", type=int, default=5)
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--top", type=int, default=30)
 a = ap.parse_args()
 sc, rc = build_config(a.config, a.jmax)
 s = Solver(sc, rc)
 s.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(a.config, sc, rc))
 s.commit()
-st = s.step(a.warmup)
+s.step(a.warmup)
+snap = {lv: s.read_leaves(lv) for lv in range(rc.j_min, rc.j_max + 1)}
 g = s.step(a.steps)
-print(f"graph: {g.ms_total / a.steps:.3f} ms/step, leaves {[int(g.leaves[i]) for i in range(g.levels)]}, "
-      f"fallback {g.fallback_leaves}, virtual {sum(g.virtual_cells[i] for i in range(g.levels))}")
-s.set_profiling(True)
-p = s.step(a.steps)
-s.set_profiling(False)
-prof = s.profile_text()
+print(f"graph: {g.ms_total / a.steps:.3f} ms/step (steps {a.warmup}..{a.warmup + a.steps - 1}), last leaves "
+      f"{[int(g.leaves[i]) for i in range(g.levels)]}, fallback {g.fallback_leaves}, "
+      f"virtual {sum(g.virtual_cells[i] for i in range(g.levels))}")
+s.close()
+p = Solver(sc, rc)
+for lv, (ix, ff) in snap.items():
+    if ix.shape[0]:
+        p.load_leaves(lv, ix, ff)
+p.commit()
+p.set_profiling(True)
+st = p.step(a.steps)
+prof = p.profile_text()
 tot = sum(v[0] for v in prof.values()) / a.steps
-print(f"profiled: {p.ms_total / a.steps:.3f} ms/step (sum of kernels {tot:.3f} ms)")
+print(f"profiled: {st.ms_total / a.steps:.3f} ms/step (sum of kernels {tot:.3f} ms)")
 by_kernel = {}
 for (k, lv), (ms, n) in prof.items():
     by_kernel[k] = by_kernel.get(k, 0.0) + ms / a.steps
