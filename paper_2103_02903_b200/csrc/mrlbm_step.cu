@@ -938,6 +938,79 @@ __global__ void k_grade_v(const __grid_constant__ Geo g, const __grid_constant__
     }
 }
 
+// The deep-gap (gap >= 2) fallback leaves of levels J0..J1-2, listed tile by tile
+// (16 x 16 cells, tile order inside, one atomicAdd per tile) with their table masks:
+// K8 gives each warp 32 consecutive list entries for one population, so the warp's
+// leaves are spatial neighbours and their box / rim loads share sectors.  (Appended
+// from the classification kernel in arrival order, K8 read 3.0 GB of DRAM per
+// transient step at an L2 hit rate of 19 %.)  Multi-level launch; the order of the
+// tiles in the list is unspecified and no result depends on it.
+template <int D>
+__global__ void __launch_bounds__(256) k_list_deep(const __grid_constant__ Geo g, const __grid_constant__ Flags fl,
+                                                   const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
+{
+    LSETUP;
+    const int li = m - g.J0;
+    const int nx = g.nx[li], ny = D == 1 ? 1 : g.ny[li];
+    const int tny = D == 1 ? 1 : (ny + 15) >> 4;
+    const long long ntiles = D == 1 ? ((long long)nx + 255) / 256 : (long long)((nx + 15) >> 4) * tny;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ int woff[8];
+    __shared__ int sbase;
+    for (long long t = lvb_; t < ntiles; t += lvg_)
+    {
+        int x, y;
+        if (D == 1)
+        {
+            x = (int)t * 256 + threadIdx.x;
+            y = 0;
+        }
+        else
+        {
+            const int tx = (int)(t / tny), ty = (int)(t - (long long)tx * tny);
+            x = tx * 16 + (threadIdx.x >> 4);
+            y = ty * 16 + (threadIdx.x & 15);
+        }
+        bool pick = false;
+        int lin = 0;
+        if (x < nx && y < ny)
+        {
+            lin = xy2lin<D>(x, y, ny);
+            pick = fl.kind[li][lin] == (K_LEAF | K_FB);
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, pick);
+        if (lane == 0)
+            woff[wid] = __popc(b);
+        __syncthreads();
+        if (threadIdx.x == 0)
+        {
+            int tot = 0;
+            for (int w = 0; w < 8; ++w)
+            {
+                const int c = woff[w];
+                woff[w] = tot;
+                tot += c;
+            }
+            sbase = tot ? atomicAdd(aux.fb_count, tot) : 0;
+        }
+        __syncthreads();
+        if (pick)
+        {
+            const int k = sbase + woff[wid] + __popc(b & ((1u << lane) - 1u));
+            if (k < aux.fb_cap)
+            {
+                const int vi = vix<D>(x, y, ny);
+                aux.fb_list[k] = make_int2(m, lin);
+                aux.fb_mask[k] = fl.fbm[li][vi];
+                aux.fb_dmask[k] = fl.fbd[li][vi];
+            }
+            else
+                flag_err(aux.err, 2);
+        }
+        __syncthreads();
+    }
+}
+
 // The gap-1 fallback leaves without domain-leaving pairs (the bulk of the fallback
 // leaves, K7 MODE 2), listed tile by tile: one block per 16 x 16 tile of level J1-1
 // (1D: 256 cells), the tile's leaves in tile order, one atomicAdd per tile.  MODE 2
@@ -1100,7 +1173,11 @@ __global__ void __launch_bounds__(256) k_band(const __grid_constant__ Geo g, con
         lin2xy_l<D>(e.y, g.ny[l - g.J0], g.lny[l - g.J0], kx, ky);
         if (l == g.J1 - 1)
             continue; // gap 1: rim values are predicted on the fly from level J1-1 (rim_value)
-        for (int m = l + 1; m <= g.J1; ++m)
+        // levels l+1 .. J1-1 only: the finest-level rim cells themselves are predicted on
+        // the fly from this level-(J1-1) band by K8 (rim_value), the same operands and order
+        // as k_virtual would use; materialising them cost a 6 M-cell finest band per
+        // transient step (k_virtual, compaction) for values read once
+        for (int m = l + 1; m < g.J1; ++m)
         {
             const int li = m - g.J0;
             const int nx = g.nx[li], ny = g.ny[li];
@@ -1313,20 +1390,8 @@ __device__ __forceinline__ void fallback_cell(const Geo& g, const Flags& fl, int
         else
             flag_err(aux.err, 2);
     }
-    // listed: deep-gap leaves (K8, bands)
-    if (gap >= 2)
-    {
-        const int k = agg_inc(aux.fb_count, 0u);
-        if (k < aux.fb_cap)
-        {
-            aux.fb_list[k] = make_int2(m, (int)i);
-            aux.fb_mask[k] = mask;
-            aux.fb_dmask[k] = dmask;
-        }
-        else
-            flag_err(aux.err, 2);
-    }
-    else
+    // deep-gap leaves (K8, bands) are listed tile by tile afterwards (k_list_deep)
+    if (gap < 2)
     {
         // gap 0 / 1 fallback leaves are found by slot scans (K7 / MODE 2 or k_fb1);
         // count them for the statistics with one atomic per warp
@@ -2499,19 +2564,132 @@ __global__ void __launch_bounds__(256, 4) k_stream_fallback(const __grid_constan
 // materialised take the general rim_value path.
 constexpr int kRimB = 8;
 
+// Finest-level rim sum of a deep-gap leaf (2D), the finest rim cells reconstructed on the
+// fly: a cell in R (a finest leaf) contributes its value; any other cell inside the
+// domain contributes the zero-detail prediction from its parent's 3 x 3 stencil at level
+// J1-1 -- the value k_virtual would have materialised there (same mr_predict operands
+// and order), so the sum is bit-identical to summing a materialised finest band.  The
+// rim is at most two straight segments (a column and a row, rim_cell's order); along a
+// segment consecutive cells share their parent or move it by one, so the stencil is a
+// sliding 3 x 3 window (3 new values per parent instead of 9 per cell).  Cells outside a
+// non-periodic domain take the boundary rule (rim_value).
+struct StencilWin {
+    double v[9];
+    int px = INT_MIN, py = INT_MIN;
+};
+
 template <int D>
-__global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
-                                                           const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
-                                                           const SchemeDev* sc, const __grid_constant__ Aux aux)
+__device__ __forceinline__ void win_load(const Geo& g, const Tree& tn, const double* fp, StencilWin& w, int px, int py,
+                                         const Aux& aux)
+{
+    if (px == w.px && py == w.py)
+        return;
+    const int lp = g.nlev - 2, mp = g.J1 - 1;
+    bool ok = true;
+    // every window index is a compile-time constant (the window stays in registers)
+    auto ld = [&](int ox, int oy) -> double {
+        ok = ok && tn.kind[lp][mr_lin<D>(g, mp, px + ox, py + oy)] != 0;
+        return fp[mr_vix<D>(g, mp, px + ox, py + oy)];
+    };
+    if (px == w.px && py == w.py + 1)
+    {
+        // column slide: shift along oy, load the oy = +1 entries
+#pragma unroll
+        for (int ox = 0; ox < 3; ++ox)
+        {
+            w.v[ox * 3 + 0] = w.v[ox * 3 + 1];
+            w.v[ox * 3 + 1] = w.v[ox * 3 + 2];
+        }
+        w.v[2] = ld(-1, 1);
+        w.v[5] = ld(0, 1);
+        w.v[8] = ld(1, 1);
+    }
+    else if (py == w.py && px == w.px + 1)
+    {
+        // row slide: shift along ox, load the ox = +1 entries
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy)
+        {
+            w.v[0 * 3 + oy] = w.v[1 * 3 + oy];
+            w.v[1 * 3 + oy] = w.v[2 * 3 + oy];
+        }
+        w.v[6] = ld(1, -1);
+        w.v[7] = ld(1, 0);
+        w.v[8] = ld(1, 1);
+    }
+    else
+    {
+#pragma unroll
+        for (int o = 0; o < 9; ++o)
+            w.v[o] = ld(o / 3 - 1, o % 3 - 1);
+    }
+    if (!ok)
+        flag_err(aux.err, 0);
+    w.px = px;
+    w.py = py;
+}
+
+template <int D>
+__device__ double rim_sum_j1(const Geo& g, const Tree& tn, const Fld& F1, const SchemeDev* sc, int h, int side, int ex,
+                             int ey, int bx0, int bx1, int by0, int by1, int leaf_li, long long leaf_lin, const Aux& aux)
+{
+    const int lj = g.nlev - 1;
+    const int nxf = g.nx[lj], nyf = g.ny[lj];
+    const double* ff = F1.f[lj] + (long long)h * g.cap[lj];
+    const double* fp = F1.f[lj - 1] + (long long)h * g.cap[lj - 1];
+    int xr = 0, yr = 0;
+    const int n = rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, -1, xr, yr);
+    StencilWin w;
+    double acc = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < n; ++i)
+    {
+        int cx, cy;
+        rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, i, cx, cy);
+        const bool inside = (g.per0 || (cx >= 0 && cx < nxf)) && (g.per1 || (cy >= 0 && cy < nyf));
+        double val;
+        if (!inside)
+            val = rim_value<D>(g, tn, F1, sc, cx, cy, h, leaf_li, leaf_lin, aux);
+        else
+        {
+            const int xc = mr_coord(cx, nxf, g.per0), yc = mr_coord(cy, nyf, g.per1);
+            const int lin = xc * nyf + yc;
+            if (tn.kind[lj][lin] & K_LEAF)
+                val = ff[vix<D>(xc, yc, nyf)];
+            else
+            {
+                win_load<D>(g, tn, fp, w, xc >> 1, yc >> 1, aux);
+                val = mr_predict<D>(w.v, xc & 1, yc & 1);
+            }
+        }
+        acc = __dadd_rn(acc, val);
+    }
+    return acc;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 3) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+                                                              const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
+                                                              const SchemeDev* sc, const __grid_constant__ Aux aux)
 {
     const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
     const int q = g.q;
     const int lj = g.J1 - g.J0;
     const int nxf = g.nx[lj], nyf = g.ny[lj];
     const long long capf = g.cap[lj];
-    GRID_STRIDE(t, 0, (long long)nfb * q)
+    // task t: chunk of 32 list entries x q populations; a warp = one population of the
+    // chunk's 32 (spatially neighbouring) leaves, so the warp's lanes take the same side
+    // path together.  (Splitting the two sides over a lane pair diverged on every leaf
+    // with one table side and one rim side: measured 1.53 vs 0.88 ms per window step.)
+    const long long nchunk = ((long long)nfb + 31) / 32;
+    GRID_STRIDE(t, 0, nchunk * 32 * q)
     {
-        const int it = (int)(t / q), h = (int)(t - (long long)it * q);
+        const long long chunk = t / (32 * q);
+        const int r = (int)(t - chunk * 32 * q);
+        const int h = r >> 5;
+        const int it = (int)(chunk * 32 + (r & 31));
+        if (it >= nfb)
+            continue;
         const int2 e = aux.fb_list[it];
         const int m = e.x;
         const int gap = g.J1 - m;
@@ -2524,7 +2702,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant
         int x, y;
         lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
         const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
-        double sums[2];
+        double sum_e = 0.0, sum_a = 0.0; // scalars: an indexed array would live on the stack
 #pragma unroll 1
         for (int side = 0; side < 2; ++side)
         {
@@ -2557,6 +2735,12 @@ __global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant
                             acc = __dadd_rn(acc, v[j]);
                 }
             }
+            else if (D == 2 && (ex != 0 || ey != 0))
+            {
+                const int side_n = 1 << gap;
+                const int bx0 = x * side_n, by0 = y * side_n;
+                acc = rim_sum_j1<D>(g, tn, F1, sc, h, side, ex, ey, bx0, bx0 + side_n, by0, by0 + side_n, li, e.y, aux);
+            }
             else if (ex != 0 || ey != 0)
             {
                 const int side_n = 1 << gap;
@@ -2566,43 +2750,25 @@ __global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant
                 const int n = rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, -1, xr, yr);
                 const double* ff = F1.f[lj] + (long long)h * capf;
 #pragma unroll 1
-                for (int b0 = 0; b0 < n; b0 += kRimB)
+                for (int i = 0; i < n; ++i)
                 {
-                    double v[kRimB];
-                    uint8_t kd[kRimB];
-                    int cx[kRimB], cy[kRimB];
-#pragma unroll
-                    for (int j = 0; j < kRimB; ++j)
-                    {
-                        kd[j] = 0;
-                        v[j] = 0.0;
-                        cx[j] = cy[j] = 0;
-                        if (b0 + j < n)
-                        {
-                            rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, b0 + j, cx[j], cy[j]);
-                            const bool inside = (g.per0 || (cx[j] >= 0 && cx[j] < nxf)) &&
-                                                (D == 1 || g.per1 || (cy[j] >= 0 && cy[j] < nyf));
-                            if (inside)
-                            {
-                                kd[j] = tn.kind[lj][mr_lin<D>(g, g.J1, cx[j], cy[j])];
-                                v[j] = ff[mr_vix<D>(g, g.J1, cx[j], cy[j])];
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < kRimB; ++j)
-                        if (b0 + j < n)
-                        {
-                            const double w = kd[j] ? v[j] : rim_value<D>(g, tn, F1, sc, cx[j], cy[j], h, li, e.y, aux);
-                            acc = __dadd_rn(acc, w);
-                        }
+                    int cx, cy;
+                    rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, i, cx, cy);
+                    const bool inside = (g.per0 || (cx >= 0 && cx < nxf)) && (D == 1 || g.per1 || (cy >= 0 && cy < nyf));
+                    const uint8_t kd = inside ? tn.kind[lj][mr_lin<D>(g, g.J1, cx, cy)] : 0;
+                    const double w = kd ? ff[mr_vix<D>(g, g.J1, cx, cy)]
+                                        : rim_value<D>(g, tn, F1, sc, cx, cy, h, li, e.y, aux);
+                    acc = __dadd_rn(acc, w);
                 }
             }
-            sums[side] = acc;
+            if (side == 0)
+                sum_e = acc;
+            else
+                sum_a = acc;
         }
         const double scale = ldexp(1.0, D * (m - g.J1));
         const long long o = (long long)h * cap + vix<D>(x, y, ny);
-        F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+        F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum_e, sum_a)));
     }
 }
 
@@ -4155,6 +4321,16 @@ void enqueue_step(mrlbm_ctx* c)
         c->kcount++;
         k_fallback_v<<<nb, T, 0, s>>>(g, fl, lg, aux);
         kmark(c, "k_fallback_v", -1);
+    }
+    if (c->J1 - 2 >= c->J0)
+    {
+        LGrid ld = make_lgrid(c, c->J0, c->J1 - 2, [&](int li) {
+            const long long nt = D == 1 ? (g.nx[li] + 255) / 256 : (long long)((g.nx[li] + 15) / 16) * ((g.ny[li] + 15) / 16);
+            return static_cast<int>(std::min<long long>(std::max<long long>(nt, 1), 148 * 4));
+        }, &nb);
+        c->kcount++;
+        k_list_deep<D><<<nb, 256, 0, s>>>(g, fl, ld, aux);
+        kmark(c, "k_list_deep", -1);
     }
     if (GEN && c->use_fb1t && c->J1 > c->J0)
     {
