@@ -2578,50 +2578,47 @@ struct StencilWin {
     int px = INT_MIN, py = INT_MIN;
 };
 
+// (The window lives in local memory, indexed at run time: measured faster than a
+// register window with compile-time indices, 0.88 vs 1.66-1.96 ms per window step --
+// the register version cost 43 more registers or spilled under a bound.)
 template <int D>
 __device__ __forceinline__ void win_load(const Geo& g, const Tree& tn, const double* fp, StencilWin& w, int px, int py,
                                          const Aux& aux)
 {
-    if (px == w.px && py == w.py)
-        return;
     const int lp = g.nlev - 2, mp = g.J1 - 1;
-    bool ok = true;
-    // every window index is a compile-time constant (the window stays in registers)
-    auto ld = [&](int ox, int oy) -> double {
-        ok = ok && tn.kind[lp][mr_lin<D>(g, mp, px + ox, py + oy)] != 0;
-        return fp[mr_vix<D>(g, mp, px + ox, py + oy)];
-    };
+    int o0 = 0, o1 = 9; // stencil entries to load
+    int step = 1;
     if (px == w.px && py == w.py + 1)
     {
-        // column slide: shift along oy, load the oy = +1 entries
+        // column slide: shift oy, load the oy = +1 entries
 #pragma unroll
         for (int ox = 0; ox < 3; ++ox)
         {
             w.v[ox * 3 + 0] = w.v[ox * 3 + 1];
             w.v[ox * 3 + 1] = w.v[ox * 3 + 2];
         }
-        w.v[2] = ld(-1, 1);
-        w.v[5] = ld(0, 1);
-        w.v[8] = ld(1, 1);
+        o0 = 2;
+        step = 3;
     }
     else if (py == w.py && px == w.px + 1)
     {
-        // row slide: shift along ox, load the ox = +1 entries
+        // row slide: shift ox, load the ox = +1 entries
 #pragma unroll
         for (int oy = 0; oy < 3; ++oy)
         {
             w.v[0 * 3 + oy] = w.v[1 * 3 + oy];
             w.v[1 * 3 + oy] = w.v[2 * 3 + oy];
         }
-        w.v[6] = ld(1, -1);
-        w.v[7] = ld(1, 0);
-        w.v[8] = ld(1, 1);
+        o0 = 6;
     }
-    else
+    else if (px == w.px && py == w.py)
+        return;
+    bool ok = true;
+    for (int o = o0; o < o1; o += step)
     {
-#pragma unroll
-        for (int o = 0; o < 9; ++o)
-            w.v[o] = ld(o / 3 - 1, o % 3 - 1);
+        const int ox = o / 3 - 1, oy = o % 3 - 1;
+        ok = ok && tn.kind[lp][mr_lin<D>(g, mp, px + ox, py + oy)] != 0;
+        w.v[o] = fp[mr_vix<D>(g, mp, px + ox, py + oy)];
     }
     if (!ok)
         flag_err(aux.err, 0);
@@ -2668,7 +2665,7 @@ __device__ double rim_sum_j1(const Geo& g, const Tree& tn, const Fld& F1, const 
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 3) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+__global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
                                                               const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
                                                               const SchemeDev* sc, const __grid_constant__ Aux aux)
 {
@@ -2769,6 +2766,112 @@ __global__ void __launch_bounds__(256, 3) k_stream_fallback_t(const __grid_const
         const double scale = ldexp(1.0, D * (m - g.J1));
         const long long o = (long long)h * cap + vix<D>(x, y, ny);
         F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum_e, sum_a)));
+    }
+}
+
+// K8 variant (MRLBM_K8_BLOCK=1): the same stream, one block per chunk of 32 consecutive list entries
+// (spatial neighbours, k_list_deep) with one warp per population (blockDim = 32 q), one
+// thread per (leaf, population).  The value indices of each leaf's distinct table
+// offsets (<= 5^D box cells, with the MR clamp / wrap and the resolved-stencil check)
+// are computed once per leaf into shared memory instead of once per table entry and
+// population, so a table sum costs a shared index load, a value load and the fp ops
+// per entry.  Sums stay serial in table / rim order from 0.0 (bit-identical).
+template <int D>
+__global__ void __launch_bounds__(512) k_stream_fallback_b(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+                                                           const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
+                                                           const SchemeDev* sc, const __grid_constant__ Aux aux)
+{
+    constexpr int kU = D == 1 ? 5 : 25;
+    __shared__ int sBox[32][kU + 1];
+    __shared__ int2 sLeaf[32];
+    __shared__ unsigned sMask[32];
+    const int nfb = min(*aux.fb_count, (int)aux.fb_cap);
+    const int q = g.q;
+    const int lane = threadIdx.x & 31, h = threadIdx.x >> 5;
+    const int nchunk = (nfb + 31) / 32;
+    for (int c = blockIdx.x; c < nchunk; c += gridDim.x)
+    {
+        if (threadIdx.x < 32)
+        {
+            const int it = c * 32 + threadIdx.x;
+            sLeaf[threadIdx.x] = it < nfb ? aux.fb_list[it] : make_int2(-1, 0);
+            sMask[threadIdx.x] = it < nfb ? aux.fb_mask[it] : 0u;
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < 32 * kU; k += blockDim.x)
+        {
+            const int i = k / kU, u = k - i * kU;
+            const int2 e = sLeaf[i];
+            if (e.x < 0)
+                continue;
+            const int2 gu = aux.guidx[g.J1 - e.x];
+            if (u >= gu.y)
+                continue;
+            const int2 o = aux.guoff[gu.x + u];
+            const int li = e.x - g.J0;
+            int x, y;
+            lin2xy_l<D>(e.y, g.ny[li], g.lny[li], x, y);
+            if (!tn.kind[li][mr_lin<D>(g, e.x, x + o.x, y + o.y)])
+                flag_err(aux.err, 0);
+            sBox[i][u] = mr_vix<D>(g, e.x, x + o.x, y + o.y);
+        }
+        __syncthreads();
+        const int2 e = sLeaf[lane];
+        const int m = e.x;
+        if (m >= 0 && g.J1 - m >= 2)
+        {
+            const int gap = g.J1 - m;
+            const unsigned mask = sMask[lane];
+            const int li = m - g.J0;
+            const int ny = g.ny[li];
+            const long long cap = g.cap[li];
+            int x, y;
+            lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
+            const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
+            const double* fm = F1.f[li] + (long long)h * cap;
+            double sum_e = 0.0, sum_a = 0.0;
+#pragma unroll 1
+            for (int side = 0; side < 2; ++side)
+            {
+                double acc = 0.0;
+                if (((mask >> (2 * h + side)) & 1u) == 0)
+                {
+                    // flattened table, in table order
+                    const int2 ti = aux.tidx[(gap * q + h) * 2 + side];
+#pragma unroll 1
+                    for (int k0 = 0; k0 < ti.y; k0 += kRimB)
+                    {
+                        double v[kRimB];
+#pragma unroll
+                        for (int j = 0; j < kRimB; ++j)
+                            v[j] = k0 + j < ti.y ? __dmul_rn(aux.tw[ti.x + k0 + j], fm[sBox[lane][aux.tu[ti.x + k0 + j]]])
+                                                 : 0.0;
+#pragma unroll
+                        for (int j = 0; j < kRimB; ++j)
+                            if (k0 + j < ti.y)
+                                acc = __dadd_rn(acc, v[j]);
+                    }
+                }
+                else if (ex != 0 || ey != 0)
+                {
+                    const int side_n = 1 << gap;
+                    const int bx0 = x * side_n, bx1 = bx0 + side_n;
+                    const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
+                    if constexpr (D == 2)
+                        acc = rim_sum_j1<D>(g, tn, F1, sc, h, side, ex, ey, bx0, bx1, by0, by1, li, e.y, aux);
+                    else
+                        acc = rim_sum<D>(g, tn, F1, sc, h, side, bx0, bx1, by0, by1, li, e.y, aux);
+                }
+                if (side == 0)
+                    sum_e = acc;
+                else
+                    sum_a = acc;
+            }
+            const double scale = ldexp(1.0, D * (m - g.J1));
+            const long long o = (long long)h * cap + vix<D>(x, y, ny);
+            F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum_e, sum_a)));
+        }
+        __syncthreads();
     }
 }
 
@@ -3986,6 +4089,9 @@ struct mrlbm_ctx {
     bool fuse_pd = false;
     // K8 one warp per (leaf, population) (MRLBM_K8_WARP=1, round-1 kernel) instead of one thread
     bool k8_warp = false;
+    // K8 one block per 32-leaf chunk with shared box indices (MRLBM_K8_BLOCK=1): measured slower,
+    // 1.59 vs 1.09 ms per window step (the block waits at every chunk for its longest rim)
+    bool k8_block = false;
     bool gen_ok = false;  // the generated code's constants match this scheme
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
@@ -4375,6 +4481,8 @@ void enqueue_step(mrlbm_ctx* c)
     c->kcount++;
     if (c->k8_warp)
         k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);
+    else if (c->k8_block)
+        k_stream_fallback_b<D><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     else
         k_stream_fallback_t<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     kmark(c, "k_stream_fallback", -1);
@@ -4903,6 +5011,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     ctx->rim_tpl = std::getenv("MRLBM_RIM_TPL") != nullptr;
     ctx->fuse_pd = std::getenv("MRLBM_FUSE_PD") != nullptr;
     ctx->k8_warp = std::getenv("MRLBM_K8_WARP") != nullptr;
+    ctx->k8_block = std::getenv("MRLBM_K8_BLOCK") != nullptr;
     for (int h = 0; h < sc->q; ++h)
     {
         const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;

@@ -56,7 +56,7 @@ def test_gpu_matches_golden_fixtures():
     import os
     from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
     gdir = os.path.join(os.path.dirname(__file__), "golden")
-    names = sorted(f for f in os.listdir(gdir) if f.endswith(".npz"))
+    names = sorted(f for f in os.listdir(gdir) if f.startswith("oracle_") and f.endswith(".npz"))
     assert names
     for name in names:
         data = np.load(os.path.join(gdir, name))
@@ -87,7 +87,7 @@ def test_generic_table_path_parity(cid, J, monkeypatch):
     ora.close()
 
 
-@pytest.mark.parametrize("env", ["MRLBM_FUSE_PD", "MRLBM_NO_FB1T", "MRLBM_RIM_TPL"])
+@pytest.mark.parametrize("env", ["MRLBM_FUSE_PD", "MRLBM_NO_FB1T", "MRLBM_RIM_TPL", "MRLBM_K8_WARP", "MRLBM_K8_BLOCK"])
 @pytest.mark.parametrize("cid,J", [(3, 6), (4, 6), (5, 7)])
 def test_kernel_variant_parity(cid, J, env, monkeypatch):
     """The alternative kernel schedules stay bit-identical to the oracle: fused

@@ -144,7 +144,7 @@ def test_load_rejects_non_partition():
         o.commit()
 
 
-@pytest.mark.parametrize("name", sorted(f for f in os.listdir(GOLDEN) if f.endswith(".npz")) if os.path.isdir(GOLDEN) else [])
+@pytest.mark.parametrize("name", sorted(f for f in os.listdir(GOLDEN) if f.startswith("oracle_") and f.endswith(".npz")) if os.path.isdir(GOLDEN) else [])
 def test_golden(name):
     """Regression pin: oracle output on committed small cases (tests/golden/make_golden.py)."""
     data = np.load(os.path.join(GOLDEN, name))
