@@ -65,12 +65,14 @@ enum {
     MRLBM_EQ_EULER_D1Q3X3 = 2,     /* 3 x D1Q3: (u_i, F_i(u), lambda^2 u_i)   */
     MRLBM_EQ_ADVECTION_D2Q4 = 3,   /* (u, a u, b u, 0); eq_params = {a, b}    */
     MRLBM_EQ_EULER_D2Q4X4 = 4,     /* 4 x D2Q4: (u_i, Fx_i, Fy_i, 0)          */
-    MRLBM_EQ_NS_D2Q9 = 5           /* Lallemand-Luo; eq_params = {cs2, variant} */
+    MRLBM_EQ_NS_D2Q9 = 5,          /* Lallemand-Luo; eq_params = {cs2, variant} */
+    MRLBM_EQ_ADVECTION_D3Q6 = 6    /* (u, Vx u, Vy u, Vz u, 0, 0); eq_params = {Vx, Vy, Vz}
+                                              */
 };
 
 /* SchemeSpec */
 typedef struct mrlbm_scheme_spec {
-    int32_t d;                 /* 1 or 2 */
+    int32_t d;                 /* 1, 2 or 3 (3: the D3Q6 path) */
     int32_t q;                 /* populations, <= MRLBM_MAX_Q */
     int32_t nblocks;           /* vectorial schemes: M is block diagonal, q/nblocks per block */
     int32_t equilibrium;       /* MRLBM_EQ_* */

@@ -85,17 +85,31 @@ struct OmpErr {
 // (prediction.hpp:143-173), so the minus cross-term convention is the
 // reference's.
 // ---------------------------------------------------------------------------
+// 3^D prediction stencil, entries in lexicographic order (axis 0 slowest):
+// offset of entry o along axis a, in {-1, 0, 1}
+template <int D>
+constexpr int kStencil = (D == 1 ? 3 : (D == 2 ? 9 : 27));
+
+template <int D>
+inline int stencil_off(int o, int a)
+{
+    int div = 1;
+    for (int i = D - 1; i > a; --i)
+        div *= 3;
+    return (o / div) % 3 - 1;
+}
+
 template <int D>
 struct TableBuilder {
-    // W[delta][o] numerators (denominator 8 for D=1, 64 for D=2)
-    std::array<std::array<I64, (D == 1 ? 3 : 9)>, (1 << D)> W{};
-    static constexpr int kDen = (D == 1 ? 8 : 64);
-    static constexpr int kShift = (D == 1 ? 3 : 6);
+    // W[delta][o] numerators (denominator 8 for D=1, 64 for D=2, 512 for D=3)
+    std::array<std::array<I64, kStencil<D>>, (1 << D)> W{};
+    static constexpr int kDen = (D == 1 ? 8 : (D == 2 ? 64 : 512));
+    static constexpr int kShift = 3 * D;
 
     TableBuilder()
     {
         const auto cfg = mrlbm::PredictionConfig::make(1);
-        const int nst = (D == 1 ? 3 : 9);
+        const int nst = kStencil<D>;
         for (int s = 0; s < (1 << D); ++s)
         {
             std::array<int, D> delta{};
@@ -104,13 +118,8 @@ struct TableBuilder {
             for (int o = 0; o < nst; ++o)
             {
                 std::array<I64, 3> hot{};
-                if (D == 1)
-                    hot[0] = o - 1;
-                else
-                {
-                    hot[0] = o / 3 - 1;
-                    hot[1] = o % 3 - 1;
-                }
+                for (int a = 0; a < D; ++a)
+                    hot[a] = stencil_off<D>(o, a);
                 auto at = [&](std::array<I64, 3> off) { return (off == hot) ? 1.0 : 0.0; };
                 const double w = mrlbm::predict<D>(at, delta, cfg);
                 const double num = w * kDen;
@@ -145,20 +154,15 @@ struct TableBuilder {
                 p[i] = c[i] >> 1;
                 s = (s << 1) | static_cast<int>(c[i] - 2 * p[i]);
             }
-            const int nst = (D == 1 ? 3 : 9);
+            const int nst = kStencil<D>;
             for (int o = 0; o < nst; ++o)
             {
                 const I64 w = W[s][o];
                 if (w == 0)
                     continue;
                 std::array<I64, D> pc = p;
-                if (D == 1)
-                    pc[0] += o - 1;
-                else
-                {
-                    pc[0] += o / 3 - 1;
-                    pc[1] += o % 3 - 1;
-                }
+                for (int a = 0; a < D; ++a)
+                    pc[a] += stencil_off<D>(o, a);
                 const Form& sub = rec(dd - 1, pc, memo);
                 for (const auto& [k, v] : sub)
                     out[k] += v * w; // numerators over kDen^dd
@@ -358,6 +362,17 @@ void equilibrium(const mrlbm_scheme_spec& sc, const double* m, double* meq)
             meq[8] = qx * qy / rho;
             break;
         }
+        case MRLBM_EQ_ADVECTION_D3Q6:
+        {   // m^eq = (u, V_x u, V_y u, V_z u, 0, 0); eq_params = V
+            const double u = m[0];
+            meq[0] = u;
+            meq[1] = P[0] * u;
+            meq[2] = P[1] * u;
+            meq[3] = P[2] * u;
+            meq[4] = 0.0;
+            meq[5] = 0.0;
+            break;
+        }
         default:
             throw std::invalid_argument("unknown equilibrium");
     }
@@ -553,10 +568,16 @@ class Oracle {
         {
             s.insert_run(Idx{0}, n[0]);
         }
-        else
+        else if constexpr (D == 2)
         {
             for (I64 x = 0; x < n[0]; ++x)
                 s.insert_run(Idx{x, 0}, n[1]);
+        }
+        else
+        {
+            for (I64 x = 0; x < n[0]; ++x)
+                for (I64 y = 0; y < n[1]; ++y)
+                    s.insert_run(Idx{x, y, 0}, n[2]);
         }
         return s;
     }
@@ -709,16 +730,16 @@ class Oracle {
     bool gather_box(int m, const Idx& center, std::vector<const double*>& out, Get&& get) const
     {
         constexpr int S = 2 * W + 1;
-        out.resize(D == 1 ? S : S * S);
-        for (int o = 0; o < (D == 1 ? S : S * S); ++o)
+        constexpr int N = D == 1 ? S : (D == 2 ? S * S : S * S * S);
+        out.resize(N);
+        for (int o = 0; o < N; ++o)
         {
             Idx c = center;
-            if (D == 1)
-                c[0] += o - W;
-            else
+            int r = o;
+            for (int a = D - 1; a >= 0; --a)
             {
-                c[0] += o / S - W;
-                c[D - 1] += o % S - W;
+                c[a] += r % S - W;
+                r /= S;
             }
             out[o] = get(m, wrapclamp(m, c));
             if (!out[o])
@@ -733,10 +754,8 @@ class Oracle {
         auto at = [&](std::array<I64, 3> off) -> double
         {
             int o = 0;
-            if (D == 1)
-                o = static_cast<int>(off[0]) + 1;
-            else
-                o = (static_cast<int>(off[0]) + 1) * 3 + static_cast<int>(off[1]) + 1;
+            for (int a = 0; a < D; ++a)
+                o = o * 3 + static_cast<int>(off[a]) + 1;
             return st3[o][h];
         };
         return mrlbm::predict<D>(at, delta, pcfg);
@@ -962,17 +981,12 @@ class Oracle {
             p[a] = c[a] >> 1;
             delta[a] = static_cast<int>(c[a] - 2 * p[a]);
         }
-        std::vector<const double*> st(D == 1 ? 3 : 9);
-        for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
+        std::vector<const double*> st(kStencil<D>);
+        for (int o = 0; o < kStencil<D>; ++o)
         {
             Idx cc = p;
-            if (D == 1)
-                cc[0] += o - 1;
-            else
-            {
-                cc[0] += o / 3 - 1;
-                cc[1] += o % 3 - 1;
-            }
+            for (int a = 0; a < D; ++a)
+                cc[a] += stencil_off<D>(o, a);
             st[o] = rec(m - 1, wrapclamp(m - 1, cc), memo);
         }
         std::vector<double> v(q);
@@ -1124,17 +1138,12 @@ class Oracle {
                                             p[a] = xc[a] >> 1;
                                             delta[a] = static_cast<int>(xc[a] - 2 * p[a]);
                                         }
-                                        std::vector<const double*> st(D == 1 ? 3 : 9);
-                                        for (int o = 0; o < (D == 1 ? 3 : 9); ++o)
+                                        std::vector<const double*> st(kStencil<D>);
+                                        for (int o = 0; o < kStencil<D>; ++o)
                                         {
                                             Idx cc = p;
-                                            if (D == 1)
-                                                cc[0] += o - 1;
-                                            else
-                                            {
-                                                cc[0] += o / 3 - 1;
-                                                cc[1] += o % 3 - 1;
-                                            }
+                                            for (int a = 0; a < D; ++a)
+                                                cc[a] += stencil_off<D>(o, a);
                                             st[o] = rec(l, wrapclamp(l, cc), memo);
                                         }
                                         s += v[h] - predict_from(st, delta, h);
@@ -1271,7 +1280,7 @@ class Oracle {
             {
                 const double sx = rc.origin[0] + (static_cast<double>(k[0]) + (a + 0.5) / ns) * dx;
                 double rr = (sx - rc.obstacle_center[0]) * (sx - rc.obstacle_center[0]);
-                if (D == 2)
+                if (D >= 2)
                 {
                     const double sy = rc.origin[1] + (static_cast<double>(k[D - 1]) + (b + 0.5) / ns) * dx;
                     rr = rr + (sy - rc.obstacle_center[1]) * (sy - rc.obstacle_center[1]);
@@ -1339,6 +1348,7 @@ struct Handle {
     int d = 0;
     std::unique_ptr<Oracle<1>> o1;
     std::unique_ptr<Oracle<2>> o2;
+    std::unique_ptr<Oracle<3>> o3;
     std::string err;
 };
 
@@ -1382,8 +1392,10 @@ int oracle_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, void*
                                  h->o1 = std::make_unique<Oracle<1>>(*sc, *rc);
                              else if (sc->d == 2)
                                  h->o2 = std::make_unique<Oracle<2>>(*sc, *rc);
+                             else if (sc->d == 3)
+                                 h->o3 = std::make_unique<Oracle<3>>(*sc, *rc);
                              else
-                                 throw std::invalid_argument("d must be 1 or 2");
+                                 throw std::invalid_argument("d must be 1, 2 or 3");
                          });
     if (st != MRLBM_OK)
     {
@@ -1401,8 +1413,10 @@ int oracle_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, void*
     guard(h, [&] {                                                                                 \
         if (h->o1)                                                                                 \
             h->o1->call;                                                                           \
-        else                                                                                       \
+        else if (h->o2)                                                                            \
             h->o2->call;                                                                           \
+        else                                                                                       \
+            h->o3->call;                                                                           \
     })
 
 int oracle_load_leaves(void* p, int level, int64_t n, const int32_t* idx, const double* f)
@@ -1432,13 +1446,13 @@ int oracle_step(void* p, int nsteps)
 int oracle_level_count(void* p, int level, int64_t* n)
 {
     auto* h = static_cast<Handle*>(p);
-    return guard(h, [&] { *n = h->o1 ? h->o1->level_count(level) : h->o2->level_count(level); });
+    return guard(h, [&] { *n = h->o1 ? h->o1->level_count(level) : h->o2 ? h->o2->level_count(level) : h->o3->level_count(level); });
 }
 
 int oracle_internal_count(void* p, int level, int64_t* n)
 {
     auto* h = static_cast<Handle*>(p);
-    return guard(h, [&] { *n = h->o1 ? h->o1->internal_count(level) : h->o2->internal_count(level); });
+    return guard(h, [&] { *n = h->o1 ? h->o1->internal_count(level) : h->o2 ? h->o2->internal_count(level) : h->o3->internal_count(level); });
 }
 
 int oracle_read_leaves(void* p, int level, int32_t* idx, double* f)
@@ -1456,14 +1470,14 @@ int oracle_reconstruct_finest(void* p, double* f)
 int64_t oracle_fallback_leaves(void* p)
 {
     auto* h = static_cast<Handle*>(p);
-    return h->o1 ? h->o1->fallback_last : h->o2->fallback_last;
+    return h->o1 ? h->o1->fallback_last : h->o2 ? h->o2->fallback_last : h->o3->fallback_last;
 }
 
 int oracle_set_force_tracking(void* p, int on)
 {
     auto* h = static_cast<Handle*>(p);
     return guard(h, [&] {
-        if (h->o1)
+        if (!h->o2)
             throw std::invalid_argument("force tracking needs the 2D obstacle configuration");
         if (h->o2->rc.obstacle != 1)
             throw std::invalid_argument("force tracking needs an obstacle (run config obstacle = 1)");
@@ -1493,7 +1507,7 @@ int oracle_tie_log(void* p, mrlbm_tie_record* out, int cap, int64_t* n, int rese
 {
     auto* h = static_cast<Handle*>(p);
     return guard(h, [&] {
-        std::vector<mrlbm_tie_record>& t = h->o1 ? h->o1->ties : h->o2->ties;
+        std::vector<mrlbm_tie_record>& t = h->o1 ? h->o1->ties : h->o2 ? h->o2->ties : h->o3->ties;
         std::sort(t.begin(), t.end(), [](const mrlbm_tie_record& a, const mrlbm_tie_record& b) {
             if (a.step != b.step) return a.step < b.step;
             if (a.level != b.level) return a.level < b.level;
@@ -1543,7 +1557,7 @@ int oracle_stream_table(int d, int gap, const int32_t eta[3], int side, int cap,
             }
             *n = static_cast<int>(t.size());
         }
-        else
+        else if (d == 2)
         {
             TableBuilder<2> tb;
             auto t = tb.build(gap, eta, side);
@@ -1553,6 +1567,20 @@ int oracle_stream_table(int d, int gap, const int32_t eta[3], int side, int cap,
             {
                 offsets[2 * i] = t[i].first[0];
                 offsets[2 * i + 1] = t[i].first[1];
+                weights[i] = t[i].second;
+            }
+            *n = static_cast<int>(t.size());
+        }
+        else
+        {
+            TableBuilder<3> tb;
+            auto t = tb.build(gap, eta, side);
+            if (static_cast<int>(t.size()) > cap)
+                return MRLBM_ERR_CAPACITY;
+            for (std::size_t i = 0; i < t.size(); ++i)
+            {
+                for (int a = 0; a < 3; ++a)
+                    offsets[3 * i + a] = t[i].first[a];
                 weights[i] = t[i].second;
             }
             *n = static_cast<int>(t.size());
@@ -1587,6 +1615,12 @@ int oracle_stream_table_sets(int d, int gap, const int32_t eta[3], int side, int
         if (d == 1)
         {
             TableBuilder<1> tb;
+            tb.build(gap, eta, side);
+            return emit(tb);
+        }
+        if (d == 3)
+        {
+            TableBuilder<3> tb;
             tb.build(gap, eta, side);
             return emit(tb);
         }
@@ -1736,6 +1770,38 @@ int build_descriptors(int id, int jmax_override, double eps_override, mrlbm_sche
         rc->obstacle_center[1] = 0.5;
         rc->obstacle_radius = radius;
     }
+    else if (id == 6)
+    {   // D3Q6 advection of a sphere indicator (D.28):
+        // J 1..8, mu = 2, eps = 1e-3, lambda = 1, S = diag(0, s1, s1, s1, s2, s2), s1 = 1.4, s2 = 1,
+        // unit cube [-3/8, 5/8]^3 (2 cells per axis at level 1), V = (1/2, 1/2, 1/2), copy boundaries
+        sc->d = 3; sc->q = 6; sc->nblocks = 1; sc->equilibrium = MRLBM_EQ_ADVECTION_D3Q6; sc->lambda = 1.0;
+        const double lam = sc->lambda;
+        for (int h = 0; h < 6; ++h)
+        {   // xi^h = lambda cos(pi h) e_{h / 2}: +x, -x, +y, -y, +z, -z
+            const int ax = h / 2, sg = (h % 2 == 0) ? 1 : -1;
+            sc->eta[h][ax] = sg;
+            Mset(0, h, 1.0);
+            Mset(1 + ax, h, lam * sg);
+        }
+        // rows 4, 5: lambda^2 (1,1,-1,-1,0,0), lambda^2 (1,1,0,0,-1,-1)
+        const double r4[6] = {1, 1, -1, -1, 0, 0}, r5[6] = {1, 1, 0, 0, -1, -1};
+        for (int h = 0; h < 6; ++h)
+        {
+            Mset(4, h, lam * lam * r4[h]);
+            Mset(5, h, lam * lam * r5[h]);
+        }
+        sc->s[1] = sc->s[2] = sc->s[3] = 1.4;
+        sc->s[4] = sc->s[5] = 1.0;
+        sc->eq_params[0] = sc->eq_params[1] = sc->eq_params[2] = 0.5;
+        rc->j_min = 1; rc->j_max = 8; rc->epsilon = 1e-3; rc->mu = 2;
+        for (int a = 0; a < 3; ++a)
+        {
+            rc->base_cells[a] = 2;
+            rc->origin[a] = -0.375;
+        }
+        for (int f = 0; f < 6; ++f)
+            rc->bc_kind[f] = MRLBM_BC_COPY;
+    }
     else
         return MRLBM_ERR_CONFIG;
     if (jmax_override > 0)
@@ -1819,8 +1885,9 @@ int oracle_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_c
 {
     const int q = sc->q, d = sc->d, J = rc->j_max;
     const std::int64_t nx = rc->base_cells[0] << (J - rc->j_min);
-    const std::int64_t ny = d == 2 ? (rc->base_cells[1] << (J - rc->j_min)) : 1;
-    const std::int64_t N = nx * ny;
+    const std::int64_t ny = d >= 2 ? (rc->base_cells[1] << (J - rc->j_min)) : 1;
+    const std::int64_t nz = d == 3 ? (rc->base_cells[2] << (J - rc->j_min)) : 1;
+    const std::int64_t N = nx * ny * nz;
     const double h = std::ldexp(1.0, -J);
     mrlbm::DenseMatrix Mi(q, q);
     for (int i = 0; i < q; ++i)
@@ -1833,9 +1900,10 @@ int oracle_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_c
 #pragma omp parallel for schedule(static)
     for (std::int64_t i = 0; i < N; ++i)
     {
-        const std::int64_t ix = i / ny, iy = i % ny;
+        const std::int64_t ix = i / (ny * nz), iy = (i / nz) % ny, iz = i % nz;
         const double x = rc->origin[0] + (static_cast<double>(ix) + 0.5) * h;
         const double y = rc->origin[1] + (static_cast<double>(iy) + 0.5) * h;
+        const double z = rc->origin[2] + (static_cast<double>(iz) + 0.5) * h;
         double U[4] = {0, 0, 0, 0}; // conserved variables, one per block
         switch (id)
         {
@@ -1857,6 +1925,7 @@ int oracle_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_c
                 break;
             }
             case 5: U[0] = 1.0; U[1] = 0.0; U[2] = 1.0 * (1e-3 * unit_sm64(seed ^ static_cast<std::uint64_t>(i))); break;
+            case 6: U[0] = (x * x + y * y + z * z <= 0.15 * 0.15) ? 1.0 : 0.0; break;
             default: break;
         }
         double m[MRLBM_MAX_Q] = {}, meq[MRLBM_MAX_Q] = {}, fl[MRLBM_MAX_Q] = {};
@@ -1872,7 +1941,7 @@ int oracle_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_c
         for (int k = 0; k < q; ++k)
             f[k * N + i] = fl[k];
     }
-    return (id >= 1 && id <= 5) ? MRLBM_OK : MRLBM_ERR_CONFIG;
+    return (id >= 1 && id <= 6) ? MRLBM_OK : MRLBM_ERR_CONFIG;
 }
 
 } // extern "C"

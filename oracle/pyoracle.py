@@ -103,6 +103,11 @@ def finest_cells(sc, rc):
     if sc.d == 1:
         return np.arange(nx, dtype=np.int32).reshape(-1, 1)
     ny = int(rc.base_cells[1]) << sh
+    if sc.d == 3:
+        nz = int(rc.base_cells[2]) << sh
+        g = np.meshgrid(np.arange(nx, dtype=np.int32), np.arange(ny, dtype=np.int32),
+                        np.arange(nz, dtype=np.int32), indexing="ij")
+        return np.stack([a.ravel() for a in g], axis=1).astype(np.int32)
     xs, ys = np.meshgrid(np.arange(nx, dtype=np.int32), np.arange(ny, dtype=np.int32), indexing="ij")
     return np.stack([xs.ravel(), ys.ravel()], axis=1).astype(np.int32)
 
@@ -219,7 +224,7 @@ class Oracle:
 
 
 def stream_table(d, gap, eta, side):
-    cap = 64
+    cap = 64 if d < 3 else 256
     off = np.zeros((cap, d), dtype=np.int32)
     w = np.zeros(cap, dtype=np.float64)
     n = C.c_int(0)

@@ -75,7 +75,18 @@ def tie_tuples(recs, n):
 
 
 def level_extent(cfg: RunConfig, d: int, level: int):
+    """(nx, ny) of a level box (ny = 1 in 1D); the 3D box is level_extent3."""
     sh = level - cfg.j_min
     nx = cfg.base_cells[0] << sh
-    ny = (cfg.base_cells[1] << sh) if d == 2 else 1
+    ny = (cfg.base_cells[1] << sh) if d >= 2 else 1
     return nx, ny
+
+
+def level_extent3(cfg: RunConfig, d: int, level: int):
+    sh = level - cfg.j_min
+    return tuple((cfg.base_cells[a] << sh) if a < d else 1 for a in range(3))
+
+
+def level_cells(cfg: RunConfig, d: int, level: int) -> int:
+    nx, ny, nz = level_extent3(cfg, d, level)
+    return nx * ny * nz

@@ -212,6 +212,126 @@ int build_stream_table(int d, int g, const int32_t* eta, int side, std::vector<T
     return MRLBM_OK; // std::map order == lexicographic (x, y)
 }
 
+// 3D push builder (gamma = 1).  Prediction weights as numerators over 512
+// (prediction.hpp:160-172 with c = -1/8): centre 512; axis a at sigma e_a:
+// -64 s_a sigma; plane (a, b) at (sigma_a, sigma_b): -8 s_a s_b sigma_a sigma_b (the
+// reference's minus sign on the plane terms); corner: -s_0 s_1 s_2 sigma_0 sigma_1 sigma_2,
+// with s_a = +1 for child selector delta_a = 0, -1 for delta_a = 1.
+int build_stream_table3(int g, const int32_t* eta, int side, std::vector<TableEntry3>& out, TableSets3* sets)
+{
+    using Key = std::array<long long, 3>;
+    out.clear();
+    if (g < 0 || g > 12)
+        return MRLBM_ERR_CONFIG;
+    const long long n = 1LL << g;
+    auto inB = [&](const Key& x) {
+        for (int a = 0; a < 3; ++a)
+            if (x[a] < 0 || x[a] >= n)
+                return false;
+        return true;
+    };
+    std::map<Key, I128> cur;
+    // E = (B - eta) \ B, A = B \ (B - eta): candidates are the cells of B - eta (E) or B (A)
+    for (long long x = 0; x < n; ++x)
+        for (long long y = 0; y < n; ++y)
+            for (long long z = 0; z < n; ++z)
+            {
+                const Key b{x, y, z};
+                const Key c = side == 0 ? Key{x - eta[0], y - eta[1], z - eta[2]} : b;
+                const Key ce{c[0] + eta[0], c[1] + eta[1], c[2] + eta[2]};
+                const bool member = side == 0 ? (inB(ce) && !inB(c)) : (inB(c) && !inB(ce));
+                if (member)
+                    cur[c] = 1;
+            }
+    long long W[8][27];
+    for (int code = 0; code < 8; ++code)
+    {
+        const long long s[3] = {(code >> 2) & 1 ? -1 : 1, (code >> 1) & 1 ? -1 : 1, code & 1 ? -1 : 1};
+        for (int o = 0; o < 27; ++o)
+        {
+            const long long sg[3] = {o / 9 - 1, (o / 3) % 3 - 1, o % 3 - 1};
+            const int nz = (sg[0] != 0) + (sg[1] != 0) + (sg[2] != 0);
+            long long w = 0;
+            if (nz == 0)
+                w = 512;
+            else if (nz == 1)
+            {
+                for (int a = 0; a < 3; ++a)
+                    if (sg[a] != 0)
+                        w = -64 * s[a] * sg[a];
+            }
+            else if (nz == 2)
+            {
+                w = -8;
+                for (int a = 0; a < 3; ++a)
+                    if (sg[a] != 0)
+                        w *= s[a] * sg[a];
+            }
+            else
+                w = -(s[0] * sg[0]) * (s[1] * sg[1]) * (s[2] * sg[2]);
+            W[code][o] = w;
+        }
+    }
+    if (sets)
+    {
+        std::map<Key, int> touched, par;
+        for (const auto& kv : cur)
+            touched[kv.first] = 1;
+        for (int lvl = g; lvl > 0; --lvl)
+        {
+            std::map<Key, int> nxt;
+            for (const auto& kv : touched)
+            {
+                const Key p{kv.first[0] >> 1, kv.first[1] >> 1, kv.first[2] >> 1};
+                if (lvl == 1)
+                    par[p] = 1;
+                for (int o = 0; o < 27; ++o)
+                    nxt[Key{p[0] + o / 9 - 1, p[1] + (o / 3) % 3 - 1, p[2] + o % 3 - 1}] = 1;
+            }
+            touched.swap(nxt);
+        }
+        for (int a = 0; a < 3; ++a)
+        {
+            sets->dep_lo[a] = touched.empty() ? 0 : (1 << 30);
+            sets->dep_hi[a] = touched.empty() ? 0 : -(1 << 30);
+        }
+        for (const auto& kv : touched)
+            for (int a = 0; a < 3; ++a)
+            {
+                sets->dep_lo[a] = std::min(sets->dep_lo[a], static_cast<int>(kv.first[a]));
+                sets->dep_hi[a] = std::max(sets->dep_hi[a], static_cast<int>(kv.first[a]));
+            }
+        sets->par.clear();
+        for (const auto& kv : par)
+            sets->par.push_back({static_cast<int>(kv.first[0]), static_cast<int>(kv.first[1]), static_cast<int>(kv.first[2])});
+    }
+    for (int lvl = g; lvl > 0; --lvl)
+    {
+        std::map<Key, I128> nxt;
+        for (const auto& [c, w] : cur)
+        {
+            if (w == 0)
+                continue;
+            const Key p{c[0] >> 1, c[1] >> 1, c[2] >> 1};
+            const int code = static_cast<int>(((c[0] - 2 * p[0]) << 2) | ((c[1] - 2 * p[1]) << 1) | (c[2] - 2 * p[2]));
+            for (int o = 0; o < 27; ++o)
+                nxt[Key{p[0] + o / 9 - 1, p[1] + (o / 3) % 3 - 1, p[2] + o % 3 - 1}] += w * W[code][o];
+        }
+        cur.swap(nxt);
+    }
+    for (const auto& [c, w] : cur)
+    {
+        if (w == 0)
+            continue;
+        TableEntry3 e{};
+        for (int a = 0; a < 3; ++a)
+            e.off[a] = static_cast<int>(c[a]);
+        e.w = std::ldexp(static_cast<double>(w), -9 * g); // nearest double to the exact dyadic (D.12)
+        out.push_back(e);
+    }
+    return MRLBM_OK; // std::map order == lexicographic (x, y, z)
+}
+
 } // namespace mrlbm_b200
 
 using namespace mrlbm_b200;
@@ -249,6 +369,23 @@ extern "C" {
 
 int mrlbm_stream_table(int d, int gap, const int32_t eta[3], int side, int cap, int32_t* offsets, double* weights, int* n)
 {
+    if (d == 3)
+    {
+        std::vector<TableEntry3> t3;
+        const int st3 = build_stream_table3(gap, eta, side, t3, nullptr);
+        if (st3 != MRLBM_OK)
+            return st3;
+        if (static_cast<int>(t3.size()) > cap)
+            return MRLBM_ERR_CAPACITY;
+        for (size_t i = 0; i < t3.size(); ++i)
+        {
+            for (int a = 0; a < 3; ++a)
+                offsets[i * 3 + a] = t3[i].off[a];
+            weights[i] = t3[i].w;
+        }
+        *n = static_cast<int>(t3.size());
+        return MRLBM_OK;
+    }
     std::vector<TableEntry> t;
     const int st = build_stream_table(d, gap, eta, side, t);
     if (st != MRLBM_OK)
@@ -330,6 +467,12 @@ static void host_feq(const mrlbm_scheme_spec* sc, const double* cons, double* f)
             meq[8] = qx * qy / rho;
             break;
         }
+        case MRLBM_EQ_ADVECTION_D3Q6:
+            meq[0] = cons[0];
+            meq[1] = sc->eq_params[0] * cons[0];
+            meq[2] = sc->eq_params[1] * cons[0];
+            meq[3] = sc->eq_params[2] * cons[0];
+            break;
     }
     for (int i = 0; i < q; ++i)
     {
@@ -542,6 +685,38 @@ int mrlbm_build_config(int id, int jmax_override, double eps_override, mrlbm_sch
             rc->obstacle_radius = radius;
             break;
         }
+        case 6: // D3Q6 advection of the indicator of a sphere (D.28)
+        {
+            sc->d = 3;
+            sc->q = 6;
+            sc->equilibrium = MRLBM_EQ_ADVECTION_D3Q6;
+            sc->lambda = 1.0;
+            const double lam = sc->lambda, l2 = lam * lam;
+            const int32_t e6[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+            for (int h = 0; h < 6; ++h)
+                for (int a = 0; a < 3; ++a)
+                    sc->eta[h][a] = e6[h][a];
+            const double M[6][6] = {{1, 1, 1, 1, 1, 1},       {lam, -lam, 0, 0, 0, 0}, {0, 0, lam, -lam, 0, 0},
+                                    {0, 0, 0, 0, lam, -lam}, {l2, l2, -l2, -l2, 0, 0}, {l2, l2, 0, 0, -l2, -l2}};
+            for (int i = 0; i < 6; ++i)
+                for (int j = 0; j < 6; ++j)
+                    sc->M[i * 6 + j] = M[i][j] + 0.0;
+            const double S[6] = {0, 1.4, 1.4, 1.4, 1.0, 1.0}; // s1 = 1.4, s2 = 1
+            std::memcpy(sc->s, S, sizeof(S));
+            sc->eq_params[0] = sc->eq_params[1] = sc->eq_params[2] = 0.5; // V (D.28)
+            rc->j_min = 1;
+            rc->j_max = 8;
+            rc->epsilon = 1e-3;
+            rc->mu = 2;
+            for (int a = 0; a < 3; ++a)
+            {
+                rc->base_cells[a] = 2;     // unit cube: 2^l cells per axis at level l
+                rc->origin[a] = -0.375;    // [-3/8, 5/8]^3: the sphere stays inside until T = 0.78125
+            }
+            for (int f = 0; f < 6; ++f)
+                rc->bc_kind[f] = MRLBM_BC_COPY;
+            break;
+        }
         default:
             return MRLBM_ERR_CONFIG;
     }
@@ -583,6 +758,7 @@ int64_t mrlbm_config_steps(int id, const mrlbm_run_config* rc)
         case 3: return static_cast<int64_t>(std::ceil(1.0 * 1.0 * std::ldexp(1.0, J)));
         case 4: return static_cast<int64_t>(std::ceil(0.25 * 4.0 * std::ldexp(1.0, J)));
         case 5: return 50000;
+        case 6: return static_cast<int64_t>(std::ceil(0.78125 * 1.0 * std::ldexp(1.0, J)));
         default: return -1;
     }
 }
@@ -591,17 +767,20 @@ int mrlbm_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_co
 {
     const int J = rc->j_max;
     const int64_t nx = rc->base_cells[0] << (J - rc->j_min);
-    const int64_t ny = (sc->d == 2) ? (rc->base_cells[1] << (J - rc->j_min)) : 1;
-    const int64_t N = nx * ny;
+    const int64_t ny = (sc->d >= 2) ? (rc->base_cells[1] << (J - rc->j_min)) : 1;
+    const int64_t nz = (sc->d == 3) ? (rc->base_cells[2] << (J - rc->j_min)) : 1;
+    const int64_t N = nx * ny * nz;
     const double dx = std::ldexp(1.0, -J);
     const int q = sc->q;
     double fl[MRLBM_MAX_Q];
     for (int64_t ix = 0; ix < nx; ++ix)
-        for (int64_t iy = 0; iy < ny; ++iy)
+        for (int64_t iyz = 0; iyz < ny * nz; ++iyz)
         {
-            const int64_t i = ix * ny + iy;
+            const int64_t iy = iyz / nz, iz = iyz % nz;
+            const int64_t i = ix * ny * nz + iyz;
             const double x = rc->origin[0] + (static_cast<double>(ix) + 0.5) * dx;
             const double y = rc->origin[1] + (static_cast<double>(iy) + 0.5) * dx;
+            const double z = rc->origin[2] + (static_cast<double>(iz) + 0.5) * dx;
             double cons[4] = {0, 0, 0, 0};
             switch (id)
             {
@@ -659,6 +838,9 @@ int mrlbm_initial_finest(int id, const mrlbm_scheme_spec* sc, const mrlbm_run_co
                     cons[2] = rho * v;
                     break;
                 }
+                case 6:
+                    cons[0] = (x * x + y * y + z * z <= 0.15 * 0.15) ? 1.0 : 0.0;
+                    break;
                 default:
                     return MRLBM_ERR_CONFIG;
             }

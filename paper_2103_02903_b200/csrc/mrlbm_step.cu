@@ -4033,6 +4033,7 @@ using namespace mrlbm_b200;
 
 // ====================================================================== host context
 struct mrlbm_ctx {
+    mrlbm_b200::Engine3D* e3 = nullptr; // scheme.d == 3: the 3D engine (mrlbm_step3d.cu) owns everything
     mrlbm_scheme_spec sc{};
     mrlbm_run_config rc{};
     int D = 0, q = 0, J0 = 0, J1 = 0, nlev = 0;
@@ -4740,6 +4741,25 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     mrlbm_ctx* ctx = nullptr;
     if (!sc || !rc)
         return MRLBM_ERR_CONFIG;
+    if (sc->d == 3)
+    {
+        ctx = new mrlbm_ctx();
+        const int st3 = mrlbm_b200::e3_create(sc, rc, &ctx->e3, ctx->err_msg);
+        if (st3 != MRLBM_OK)
+        {
+            delete ctx;
+            return st3;
+        }
+        ctx->sc = *sc;
+        ctx->rc = *rc;
+        ctx->D = 3;
+        ctx->q = sc->q;
+        ctx->J0 = rc->j_min;
+        ctx->J1 = rc->j_max;
+        ctx->nlev = ctx->J1 - ctx->J0 + 1;
+        *out = ctx;
+        return MRLBM_OK;
+    }
     if (sc->d < 1 || sc->d > 2 || !step_fn(sc->d, sc->q, sc->nblocks, sc->equilibrium, false))
         return MRLBM_ERR_CONFIG;
     if (rc->j_min < 0 || rc->j_max <= rc->j_min || rc->j_max - rc->j_min + 1 > kL)
@@ -5032,6 +5052,8 @@ int mrlbm_load_leaves(mrlbm_ctx* ctx, int level, int64_t n, const int32_t* idx, 
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_load_leaves(ctx->e3, level, n, idx, f);
     if (level < ctx->J0 || level > ctx->J1 || n < 0)
         return set_err(ctx, MRLBM_ERR_CONFIG, "load: level out of range");
     const int li = level - ctx->J0;
@@ -5067,6 +5089,8 @@ int mrlbm_commit(mrlbm_ctx* ctx)
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_commit(ctx->e3);
     const Geo& g = ctx->geo;
     const int v = ctx->cur;
     Flags fl = flags_of(ctx, v);
@@ -5147,6 +5171,8 @@ int mrlbm_step(mrlbm_ctx* ctx, int nsteps, mrlbm_step_stats* stats)
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_step(ctx->e3, nsteps, stats);
     if (!ctx->committed)
         return set_err(ctx, MRLBM_ERR_STATE, "step before commit");
     StepFn fn = step_fn(ctx->D, ctx->q, ctx->sc.nblocks, ctx->sc.equilibrium, ctx->use_gen);
@@ -5259,6 +5285,8 @@ int mrlbm_level_count(mrlbm_ctx* ctx, int level, int64_t* n)
 {
     if (!ctx || level < ctx->J0 || level > ctx->J1)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_level_count(ctx->e3, level, n);
     int c = 0;
     CU(cudaMemcpyAsync(&c, ctx->cnt[ctx->cur] + (level - ctx->J0) * 4, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -5270,6 +5298,8 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f)
 {
     if (!ctx || level < ctx->J0 || level > ctx->J1)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_read_leaves(ctx->e3, level, idx, f);
     const int li = level - ctx->J0;
     for (int k = 0; k < ctx->nlev; ++k)
         if (ctx->ld_n[k])
@@ -5323,6 +5353,8 @@ int mrlbm_finest_count(const mrlbm_ctx* ctx, int64_t* n)
 {
     if (!ctx || !n)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_finest_count(ctx->e3, n);
     *n = ctx->geo.cap[ctx->nlev - 1];
     return MRLBM_OK;
 }
@@ -5369,6 +5401,8 @@ int mrlbm_reconstruct_finest(mrlbm_ctx* ctx, double* f)
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return set_err(ctx, MRLBM_ERR_CONFIG, "diagnostics are 1D/2D only");
     if (int st = recon_device(ctx); st != MRLBM_OK)
         return st;
     if (f)
@@ -5385,6 +5419,8 @@ int mrlbm_additional_error(mrlbm_ctx* ctx, mrlbm_ctx* ref, const double* row, do
 {
     if (!ctx || !ref || !row || !E)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3 || ref->e3)
+        return set_err(ctx, MRLBM_ERR_CONFIG, "diagnostics are 1D/2D only");
     const int li = ctx->nlev - 1, lr = ref->nlev - 1;
     if (ctx->D != ref->D || ctx->q != ref->q || ctx->J1 != ref->J1 || ctx->geo.nx[li] != ref->geo.nx[lr] ||
         ctx->geo.ny[li] != ref->geo.ny[lr])
@@ -5513,6 +5549,8 @@ int mrlbm_set_force_tracking(mrlbm_ctx* ctx, int capacity_steps)
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking needs the D2Q9 obstacle configuration");
     if (capacity_steps < 0)
         return set_err(ctx, MRLBM_ERR_CONFIG, "force tracking: negative capacity");
     if (capacity_steps > 0 && !(ctx->rc.obstacle == 1 && ctx->D == 2 && ctx->sc.equilibrium == MRLBM_EQ_NS_D2Q9))
@@ -5562,6 +5600,8 @@ int mrlbm_tie_log(mrlbm_ctx* ctx, mrlbm_tie_record* out, int cap, int64_t* n, in
 {
     if (!ctx || !n || cap < 0)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_tie_log(ctx->e3, out, cap, n, reset);
     int total = 0;
     CU(cudaMemcpyAsync(&total, ctx->tie_n, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -5598,6 +5638,8 @@ int mrlbm_set_graph(mrlbm_ctx* ctx, int on)
 
 void* mrlbm_stream_handle(mrlbm_ctx* ctx)
 {
+    if (ctx && ctx->e3)
+        return mrlbm_b200::e3_stream(ctx->e3);
     return ctx ? static_cast<void*>(ctx->stream) : nullptr;
 }
 
@@ -5605,12 +5647,16 @@ int mrlbm_synchronize(mrlbm_ctx* ctx)
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
+    if (ctx->e3)
+        return mrlbm_b200::e3_synchronize(ctx->e3);
     CU(cudaStreamSynchronize(ctx->stream));
     return MRLBM_OK;
 }
 
 const char* mrlbm_last_error(const mrlbm_ctx* ctx)
 {
+    if (ctx && ctx->e3 && ctx->err_msg.empty())
+        return mrlbm_b200::e3_last_error(ctx->e3);
     return ctx ? ctx->err_msg.c_str() : "null context";
 }
 
@@ -5618,6 +5664,12 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
 {
     if (!ctx)
         return;
+    if (ctx->e3)
+    {
+        mrlbm_b200::e3_destroy(ctx->e3);
+        delete ctx;
+        return;
+    }
     if (ctx->stream)
         cudaStreamSynchronize(ctx->stream);
     for (auto& gph : ctx->graph)

@@ -8,7 +8,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .abi import SchemeSpec, RunConfig, level_extent
+from .abi import SchemeSpec, RunConfig, level_cells, level_extent, level_extent3
 
 CONFIG_NAMES = {
     1: "D1Q2 Burgers",
@@ -16,6 +16,7 @@ CONFIG_NAMES = {
     3: "D2Q4 advection (periodic disc)",
     4: "D2Q4x4 Euler (4-quadrant Riemann)",
     5: "D2Q9 Navier-Stokes (cylinder, Re=1200)",
+    6: "D3Q6 advection (sphere, PAPER 7.3)",
 }
 
 
@@ -40,14 +41,17 @@ def finest_cells(sc: SchemeSpec, rc: RunConfig) -> np.ndarray:
     nx, ny = level_extent(rc, sc.d, rc.j_max)
     if sc.d == 1:
         return np.arange(nx, dtype=np.int32).reshape(-1, 1)
+    if sc.d == 3:
+        ext = level_extent3(rc, 3, rc.j_max)
+        g = np.meshgrid(*[np.arange(n, dtype=np.int32) for n in ext], indexing="ij")
+        return np.stack([a.ravel() for a in g], axis=1).astype(np.int32)
     xs, ys = np.meshgrid(np.arange(nx, dtype=np.int32), np.arange(ny, dtype=np.int32), indexing="ij")
     return np.stack([xs.ravel(), ys.ravel()], axis=1).astype(np.int32)
 
 
 def initial_finest(config_id: int, sc: SchemeSpec, rc: RunConfig, seed: int = 2103_02903) -> np.ndarray:
     """Equilibrium populations on the full finest mesh, SoA (q, N) float64."""
-    nx, ny = level_extent(rc, sc.d, rc.j_max)
-    f = np.empty((sc.q, nx * ny), dtype=np.float64)
+    f = np.empty((sc.q, level_cells(rc, sc.d, rc.j_max)), dtype=np.float64)
     st = _lib.lib().mrlbm_initial_finest(int(config_id), C.byref(sc), C.byref(rc), C.c_uint64(seed),
                                          f.ctypes.data_as(C.c_void_p))
     if st != 0:
@@ -57,7 +61,7 @@ def initial_finest(config_id: int, sc: SchemeSpec, rc: RunConfig, seed: int = 21
 
 def stream_table(d: int, gap: int, eta, side: int):
     """Flattened reconstruction table of the product (offsets (n, d), weights (n,))."""
-    cap = 64
+    cap = 64 if d < 3 else 256
     off = np.zeros((cap, d), dtype=np.int32)
     w = np.zeros(cap, dtype=np.float64)
     n = C.c_int(0)

@@ -20,7 +20,7 @@ import os
 
 import numpy as np
 
-from .abi import level_extent
+from .abi import level_cells, level_extent
 
 
 def conserved_rows(scheme):
@@ -87,13 +87,8 @@ def read_snapshot(path):
 
 def occupation_rates(rc, d, stats):
     """(MeshOR, MemOR) of the mesh after the last step."""
-    full_leaves = 1
-    for a in range(d):
-        full_leaves *= level_extent(rc, d, rc.j_max)[a]
-    full_tree = 0
-    for lv in range(rc.j_min, rc.j_max + 1):
-        nx, ny = level_extent(rc, d, lv)
-        full_tree += nx * (ny if d == 2 else 1)
+    full_leaves = level_cells(rc, d, rc.j_max)
+    full_tree = sum(level_cells(rc, d, lv) for lv in range(rc.j_min, rc.j_max + 1))
     nl = stats.levels
     leaves = sum(int(stats.leaves[i]) for i in range(nl))
     internal = sum(int(stats.internal[i]) for i in range(nl))

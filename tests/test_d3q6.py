@@ -1,0 +1,164 @@
+"""The 3D path: D3Q6 advection of a sphere indicator (PAPER.md:1462-1518,
+SPEC.md:408-416).  CPU: the 3D flattened tables (product push builder vs the oracle's pull
+recursion over the reference predict<3>), the 3D prediction known answers, the oracle's
+step properties.  GPU: step-by-step parity of the CUDA 3D engine against the oracle
+instantiated at D = 3, epsilon = 0 uniform mode, and the paper's compression result
+(MeshOR <= 0.05 at J = 8).
+"""
+import numpy as np
+import pytest
+
+from paper_2103_02903_b200 import build_config, config_steps, finest_cells, initial_finest, stream_table
+
+ETAS = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
+
+
+def test_tables_3d_product_equals_oracle_bitwise():
+    from oracle import pyoracle
+    for gap in range(0, 5):
+        for eta in ETAS:
+            for side in (0, 1):
+                po, pw = stream_table(3, gap, eta, side)
+                oo, ow = pyoracle.stream_table(3, gap, eta, side)
+                assert np.array_equal(po, oo), (gap, eta, side)
+                assert np.array_equal(pw.view(np.uint64), ow.view(np.uint64)), (gap, eta, side)
+                # a table sums f^^ over the 4^gap rim cells: exact on constants
+                assert abs(pw.sum() - 4.0 ** gap) <= 1e-12 * 4.0 ** gap
+
+
+def test_predict3_one_hot_fan():
+    """Weights of the reference predict<3> (prediction.hpp:160-172): centre 1, axis -/+1/8,
+    plane terms with the reference's minus sign, corner -/+1/512; the 8 children average
+    back to the parent (consistency, Eq. 7)."""
+    from oracle import pyoracle
+    L = pyoracle.ref_lib()
+    import ctypes as C
+    W = np.zeros((8, 27))
+    for code in range(8):
+        delta = (C.c_int * 3)((code >> 2) & 1, (code >> 1) & 1, code & 1)
+        for o in range(27):
+            st = np.zeros(27)
+            st[o] = 1.0
+            W[code, o] = L.ref_predict(3, 1, st.ctypes.data_as(C.c_void_p), delta)
+    assert np.allclose(W[:, 13], 1.0)
+    assert W[0, 13 + 9] == -0.125 and W[0, 13 - 9] == 0.125          # +x / -x for delta_x = 0
+    assert W[0, 13 + 9 + 3] == -1.0 / 64 and W[0, 13 + 9 - 3] == 1.0 / 64  # plane term: minus sign
+    assert W[0, 26] == -1.0 / 512 and W[0, 0] == 1.0 / 512
+    mean = W.mean(axis=0)
+    assert np.array_equal(mean, np.eye(27)[13])
+
+
+def test_oracle_3d_step_properties():
+    """Oracle at D = 3 (J = 5): the leaves partition the cube, the mass is conserved to
+    round-off while the support is away from the walls, the mesh compresses."""
+    from oracle import pyoracle
+    sc, rc = pyoracle.build_config(6, 5)
+    assert sc.d == 3 and sc.q == 6 and rc.j_min == 1 and rc.mu == 2
+    idx, f0 = pyoracle.finest_cells(sc, rc), pyoracle.initial_finest(6, sc, rc)
+    o = pyoracle.Oracle(sc, rc)
+    o.load_leaves(rc.j_max, idx, f0)
+    o.commit()
+    m0 = f0.sum() * 2.0 ** (-3 * rc.j_max)
+    for step in range(4):
+        o.step(1)
+        vol, mass, n = 0.0, 0.0, 0
+        for lv in range(rc.j_min, rc.j_max + 1):
+            li, lf = o.read_leaves(lv)
+            vol += li.shape[0] * 2.0 ** (-3 * lv)
+            mass += lf.sum() * 2.0 ** (-3 * lv)
+            n += li.shape[0]
+        assert vol == 1.0
+        assert abs(mass - m0) <= 1e-12 * m0
+        assert n < idx.shape[0] // 4
+    o.close()
+
+
+def test_config6_descriptor_values():
+    sc, rc = build_config(6)
+    assert [tuple(sc.eta[h][:3]) for h in range(6)] == ETAS
+    assert list(sc.s[:6]) == [0.0, 1.4, 1.4, 1.4, 1.0, 1.0]
+    assert rc.j_min == 1 and rc.j_max == 8 and rc.epsilon == 1e-3 and rc.mu == 2
+    assert config_steps(6, rc) == 200  # T = 0.78125 at dt = 2^-8
+    M = np.array(sc.M[:36]).reshape(6, 6)
+    Mi = np.array(sc.Minv[:36]).reshape(6, 6)
+    assert np.allclose(M @ Mi, np.eye(6), atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- GPU
+def _pair(J, eps=-1.0):
+    from parity_util import make_pair
+    return make_pair(6, J, eps)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("J,eps,steps", [(4, -1.0, 12), (5, -1.0, 16), (4, 0.0, 8), (6, -1.0, 6)])
+def test_gpu_3d_step_parity(J, eps, steps):
+    """CUDA 3D engine vs the oracle at D = 3, after every step: identical leaf sets,
+    fields within 1e-12 relative (north_star) -- bit-identical in practice."""
+    from parity_util import compare
+    sc, rc, gpu, ora = _pair(J, eps)
+    allbit = True
+    for k in range(steps):
+        st = gpu.step(1)
+        ora.step(1)
+        rel, bitwise, total = compare(gpu, ora, rc, f"config 6 J={J} step {k}")
+        assert rel <= 1e-12, f"config 6 J={J} step {k}: rel diff {rel}"
+        allbit = allbit and bitwise
+        assert st.fallback_leaves == ora.fallback_leaves()
+    assert allbit
+    assert gpu.tie_log() == ora.tie_log()
+    gpu.close()
+    ora.close()
+
+
+@pytest.mark.gpu
+def test_gpu_3d_reload_roundtrip():
+    """read_leaves -> load_leaves of an adapted 3D mesh into a second context continues
+    bit-identically (the snapshot contract either side of the step)."""
+    from paper_2103_02903_b200 import Solver
+    sc, rc = build_config(6, 5)
+    a = Solver(sc, rc)
+    a.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(6, sc, rc))
+    a.commit()
+    a.step(5)
+    b = Solver(sc, rc)
+    for lv in range(rc.j_min, rc.j_max + 1):
+        i, f = a.read_leaves(lv)
+        b.load_leaves(lv, i, f)
+    b.commit()
+    a.step(3)
+    b.step(3)
+    for lv in range(rc.j_min, rc.j_max + 1):
+        ai, af = a.read_leaves(lv)
+        bi, bf = b.read_leaves(lv)
+        assert np.array_equal(ai, bi) and np.array_equal(af.view(np.uint64), bf.view(np.uint64))
+    a.close()
+    b.close()
+
+
+@pytest.mark.gpu
+def test_gpu_3d_compression_J8():
+    """advection3d with J_min = 1, J = 8, mu = 2, eps = 1e-3
+    reaches a post-transient MeshOR <= 0.05 (the paper reports ~0.03); mass conserved."""
+    from paper_2103_02903_b200 import Solver
+    sc, rc = build_config(6)
+    s = Solver(sc, rc)
+    idx, f0 = finest_cells(sc, rc), initial_finest(6, sc, rc)
+    n_fine = idx.shape[0]
+    m0 = f0.sum() * 2.0 ** (-3 * rc.j_max)
+    s.load_leaves(rc.j_max, idx, f0)
+    s.commit()
+    del idx, f0
+    nsteps = config_steps(6, rc)
+    ors = []
+    for k in range(0, nsteps, 10):
+        st = s.step(10)
+        ors.append(sum(int(st.leaves[i]) for i in range(st.levels)) / n_fine)
+    assert max(ors[2:]) <= 0.05, ors
+    mass = 0.0
+    for lv in range(rc.j_min, rc.j_max + 1):
+        _, lf = s.read_leaves(lv)
+        mass += lf.sum() * 2.0 ** (-3 * lv)
+    assert abs(mass - m0) <= 1e-9 * m0
+    print("MeshOR over the run:", [round(v, 4) for v in ors])
+    s.close()

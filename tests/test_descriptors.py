@@ -14,7 +14,8 @@ from paper_2103_02903_b200 import build_config, initial_finest
 from paper_2103_02903_b200.abi import SchemeSpec, RunConfig
 
 CASES = [(1, 0, -1.0), (2, 0, -1.0), (3, 0, -1.0), (3, 0, 0.0), (4, 0, -1.0), (5, 0, -1.0),
-         (1, 7, -1.0), (2, 9, -1.0), (4, 6, -1.0), (5, 6, -1.0), (5, 9, -1.0), (5, 10, -1.0)]
+         (1, 7, -1.0), (2, 9, -1.0), (4, 6, -1.0), (5, 6, -1.0), (5, 9, -1.0), (5, 10, -1.0),
+         (6, 0, -1.0), (6, 5, -1.0), (6, 5, 0.0)]
 
 
 def oracle_config(cid, J=0, eps=-1.0):
@@ -55,7 +56,7 @@ def test_config5_values_from_the_paper():
     assert abs(feq.sum() - 1.0) < 1e-15 and np.all(np.abs(feq @ eta) < 1e-16)
 
 
-@pytest.mark.parametrize("cid,J", [(1, 8), (2, 8), (3, 6), (4, 6), (5, 6), (5, 8)])
+@pytest.mark.parametrize("cid,J", [(1, 8), (2, 8), (3, 6), (4, 6), (5, 6), (5, 8), (6, 5), (6, 6)])
 def test_initial_data_bitwise(cid, J):
     from oracle import pyoracle
     psc, prc = build_config(cid, J)
