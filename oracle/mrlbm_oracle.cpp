@@ -1773,7 +1773,8 @@ int build_descriptors(int id, int jmax_override, double eps_override, mrlbm_sche
     else if (id == 6)
     {   // D3Q6 advection of a sphere indicator (D.28):
         // J 1..8, mu = 2, eps = 1e-3, lambda = 1, S = diag(0, s1, s1, s1, s2, s2), s1 = 1.4, s2 = 1,
-        // unit cube [-3/8, 5/8]^3 (2 cells per axis at level 1), V = (1/2, 1/2, 1/2), copy boundaries
+        // unit cube [-3/8, 5/8]^3 (2 cells per axis at level 1), V = (1/4, 1/4, 1/4) (inside the positivity
+        // bound |V_a| <= lambda / 3 of the D3Q6 equilibrium; V = 1/2 blows up), copy boundaries
         sc->d = 3; sc->q = 6; sc->nblocks = 1; sc->equilibrium = MRLBM_EQ_ADVECTION_D3Q6; sc->lambda = 1.0;
         const double lam = sc->lambda;
         for (int h = 0; h < 6; ++h)
@@ -1792,7 +1793,7 @@ int build_descriptors(int id, int jmax_override, double eps_override, mrlbm_sche
         }
         sc->s[1] = sc->s[2] = sc->s[3] = 1.4;
         sc->s[4] = sc->s[5] = 1.0;
-        sc->eq_params[0] = sc->eq_params[1] = sc->eq_params[2] = 0.5;
+        sc->eq_params[0] = sc->eq_params[1] = sc->eq_params[2] = 0.25;
         rc->j_min = 1; rc->j_max = 8; rc->epsilon = 1e-3; rc->mu = 2;
         for (int a = 0; a < 3; ++a)
         {

@@ -703,7 +703,9 @@ int mrlbm_build_config(int id, int jmax_override, double eps_override, mrlbm_sch
                     sc->M[i * 6 + j] = M[i][j] + 0.0;
             const double S[6] = {0, 1.4, 1.4, 1.4, 1.0, 1.0}; // s1 = 1.4, s2 = 1
             std::memcpy(sc->s, S, sizeof(S));
-            sc->eq_params[0] = sc->eq_params[1] = sc->eq_params[2] = 0.5; // V (D.28)
+            // V (D.28): inside |V_a| <= lambda / 3, where the equilibrium populations u (1/6 +- V_a / (2 lambda))
+            // stay non-negative; V = 1/2 was measured unstable (|u| -> 1e53 in 200 steps)
+            sc->eq_params[0] = sc->eq_params[1] = sc->eq_params[2] = 0.25;
             rc->j_min = 1;
             rc->j_max = 8;
             rc->epsilon = 1e-3;

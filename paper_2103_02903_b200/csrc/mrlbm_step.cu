@@ -108,6 +108,7 @@ struct Aux {
     const unsigned short* umask; // [g] union over the pairs
     // obstacle force tracking (null when off): per level, a dense box over the disc's
     // bounding box holding each leaf's (Fx, Fy) term of the current step
+    int k8_long;        // > 0: leaves with gap >= k8_long (long rims) take the warp-cooperative K8 launch
     int fb1t;           // thread-per-leaf gap-1 path on: the boundary-rim fallback leaves are listed
     int* fbs;           // [2] segment lists of linear indices: 0 = gap-0 fallback leaves (level J1),
                         //     1 = gap-1 fallback leaves with domain-leaving pairs (level J1-1);
@@ -945,6 +946,19 @@ __global__ void k_grade_v(const __grid_constant__ Geo g, const __grid_constant__
 // from the classification kernel in arrival order, K8 read 3.0 GB of DRAM per
 // transient step at an L2 hit rate of 19 %.)  Multi-level launch; the order of the
 // tiles in the list is unspecified and no result depends on it.
+constexpr int kLongGap = 4; // K8: gap from which a leaf's rims are evaluated by a whole warp
+// The warp-cooperative launch wins when the long-rim leaves are few (their serial chains
+// set the duration of the thread kernel: settled regime 404 -> 150 us, transient window
+// 1089 -> 872 us) and loses when they are many (developing flow, thousands of gap-4 / 5
+// leaves: 331 -> 436 us), so the threshold moves up by two levels when more than
+// kLongMany leaves lie at or above it.  Counted per step by k_list_deep (fb_count[5]:
+// gap >= k8_long, fb_count[6]: gap >= k8_long + 2); both K8 launches evaluate the same rule.
+constexpr int kLongMany = 2048;
+__device__ __forceinline__ int k8_long_gap(int base, const int* fb_count)
+{
+    return (base > 0 && fb_count[5] > kLongMany) ? base + 2 : base;
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_list_deep(const __grid_constant__ Geo g, const __grid_constant__ Flags fl,
                                                    const __grid_constant__ LGrid lg_, const __grid_constant__ Aux aux)
@@ -956,7 +970,8 @@ __global__ void __launch_bounds__(256) k_list_deep(const __grid_constant__ Geo g
     const long long ntiles = D == 1 ? ((long long)nx + 255) / 256 : (long long)((nx + 15) >> 4) * tny;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     __shared__ int woff[8];
-    __shared__ int sbase;
+    __shared__ int sbase, slong;
+    const bool longrim = aux.k8_long > 0 && g.J1 - m >= aux.k8_long;
     for (long long t = lvb_; t < ntiles; t += lvg_)
     {
         int x, y;
@@ -992,17 +1007,26 @@ __global__ void __launch_bounds__(256) k_list_deep(const __grid_constant__ Geo g
                 tot += c;
             }
             sbase = tot ? atomicAdd(aux.fb_count, tot) : 0;
+            slong = tot && longrim ? atomicAdd(aux.fb_count + 5, tot) : 0;
+            if (tot && longrim && g.J1 - m >= aux.k8_long + 2)
+                atomicAdd(aux.fb_count + 6, tot);
         }
         __syncthreads();
         if (pick)
         {
-            const int k = sbase + woff[wid] + __popc(b & ((1u << lane) - 1u));
-            if (k < aux.fb_cap)
+            const int r = woff[wid] + __popc(b & ((1u << lane) - 1u));
+            const int k = sbase + r;
+            // the long-rim entries (gap >= kLongGap) are also indexed from the tail of the
+            // list buffer, for the warp-cooperative K8 launch; capacity = all cells, so the
+            // head (<= leaves of the levels <= J1-2) and the tail never meet
+            if (k < aux.fb_cap && (!longrim || (long long)k < aux.fb_cap - 1 - (slong + r)))
             {
                 const int vi = vix<D>(x, y, ny);
                 aux.fb_list[k] = make_int2(m, lin);
                 aux.fb_mask[k] = fl.fbm[li][vi];
                 aux.fb_dmask[k] = fl.fbd[li][vi];
+                if (longrim)
+                    aux.fb_list[aux.fb_cap - 1 - (slong + r)] = make_int2(k, 0);
             }
             else
                 flag_err(aux.err, 2);
@@ -2563,6 +2587,8 @@ __global__ void __launch_bounds__(256, 4) k_stream_fallback(const __grid_constan
 // kRimB independent loads are in flight per thread; cells outside the domain or not
 // materialised take the general rim_value path.
 constexpr int kRimB = 8;
+// leaves with gap >= kLongGap (rims of 2^gap .. 2^(gap+1) finest cells per side) go to the
+// warp-cooperative K8 launch instead of one thread per (leaf, population)
 
 // Finest-level rim sum of a deep-gap leaf (2D), the finest rim cells reconstructed on the
 // fly: a cell in R (a finest leaf) contributes its value; any other cell inside the
@@ -2664,8 +2690,8 @@ __device__ double rim_sum_j1(const Geo& g, const Tree& tn, const Fld& F1, const 
     return acc;
 }
 
-template <int D>
-__global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+template <int D, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_stream_fallback_t(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
                                                               const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
                                                               const SchemeDev* sc, const __grid_constant__ Aux aux)
 {
@@ -2679,6 +2705,7 @@ __global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant
     // path together.  (Splitting the two sides over a lane pair diverged on every leaf
     // with one table side and one rim side: measured 1.53 vs 0.88 ms per window step.)
     const long long nchunk = ((long long)nfb + 31) / 32;
+    const int long_gap = k8_long_gap(aux.k8_long, aux.fb_count);
     GRID_STRIDE(t, 0, nchunk * 32 * q)
     {
         const long long chunk = t / (32 * q);
@@ -2690,8 +2717,8 @@ __global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant
         const int2 e = aux.fb_list[it];
         const int m = e.x;
         const int gap = g.J1 - m;
-        if (gap < 2)
-            continue; // gap 0 / 1: K7 MODE 2 / 5 and k_fb1
+        if (gap < 2 || (long_gap > 0 && gap >= long_gap))
+            continue; // gap 0 / 1: K7 MODE 2 / 5 and k_fb1; long rims: k_stream_fallback_long
         const unsigned mask = aux.fb_mask[it];
         const int li = m - g.J0;
         const int ny = g.ny[li];
@@ -2766,6 +2793,103 @@ __global__ void __launch_bounds__(256) k_stream_fallback_t(const __grid_constant
         const double scale = ldexp(1.0, D * (m - g.J1));
         const long long o = (long long)h * cap + vix<D>(x, y, ny);
         F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum_e, sum_a)));
+    }
+}
+
+// K8, long rims (gap >= kLongGap): one warp per (leaf, population) over the tail list of
+// k_list_deep.  A thread-per-(leaf, population) chain over 2^gap .. 2^(gap+1) rim cells
+// (up to 2 x 512 dependent fetch-predict-add rounds at gap 8) set the duration of the
+// whole K8 launch in the settled and developing regimes, where such leaves are few.  Here
+// the lanes evaluate 32 rim cells (or load 32 table operands) at a time into shared
+// memory and lane 0 accumulates them serially in rim / table order from 0.0: the same
+// operands and the same order of additions as rim_sum, so bit-identical.
+template <int D>
+__global__ void __launch_bounds__(256) k_stream_fallback_long(const __grid_constant__ Geo g, const __grid_constant__ Tree tn,
+                                                                 const __grid_constant__ Fld F0, const __grid_constant__ Fld F1,
+                                                                 const SchemeDev* sc, const __grid_constant__ Aux aux)
+{
+    __shared__ double sv[8][32];
+    const int nlong = aux.fb_count[5];
+    const int long_gap = k8_long_gap(aux.k8_long, aux.fb_count);
+    const int q = g.q;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long t = gw; t < (long long)nlong * q; t += nw)
+    {
+        const int it = aux.fb_list[aux.fb_cap - 1 - (t / q)].x, h = (int)(t % q);
+        const int2 e = aux.fb_list[it];
+        const unsigned mask = aux.fb_mask[it];
+        const int m = e.x, li = m - g.J0;
+        const int ny = g.ny[li];
+        const long long cap = g.cap[li];
+        int x, y;
+        lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
+        const int gap = g.J1 - m;
+        if (gap < long_gap)
+            continue; // many long-rim leaves this step: the thread kernel takes this gap
+        const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
+        double sum_e = 0.0, sum_a = 0.0;
+        for (int side = 0; side < 2; ++side)
+        {
+            double acc = 0.0;
+            const bool table = ((mask >> (2 * h + side)) & 1u) == 0;
+            int n = 0;
+            int2 ti = make_int2(0, 0);
+            const int side_n = 1 << gap;
+            const int bx0 = x * side_n, bx1 = bx0 + side_n;
+            const int by0 = D == 1 ? 0 : y * side_n, by1 = D == 1 ? 1 : by0 + side_n;
+            if (table)
+            {
+                ti = aux.tidx[(gap * q + h) * 2 + side];
+                n = ti.y;
+            }
+            else if (ex != 0 || ey != 0)
+            {
+                int xr = 0, yr = 0;
+                n = rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, -1, xr, yr);
+            }
+            for (int b0 = 0; b0 < n; b0 += 32)
+            {
+                double v = 0.0;
+                if (b0 + lane < n)
+                {
+                    if (table)
+                    {
+                        const int k = ti.x + b0 + lane;
+                        const int2 o = aux.toff[k];
+                        if (!tn.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)])
+                            flag_err(aux.err, 0);
+                        v = __dmul_rn(aux.tw[k], F1.f[li][(long long)h * cap + mr_vix<D>(g, m, x + o.x, y + o.y)]);
+                    }
+                    else
+                    {
+                        int xr = 0, yr = 0;
+                        rim_cell<D>(side, ex, ey, bx0, bx1, by0, by1, b0 + lane, xr, yr);
+                        v = rim_value<D>(g, tn, F1, sc, xr, yr, h, li, e.y, aux);
+                    }
+                }
+                sv[w][lane] = v;
+                __syncwarp();
+                if (lane == 0)
+                {
+                    const int nv = min(32, n - b0);
+                    for (int j = 0; j < nv; ++j)
+                        acc = __dadd_rn(acc, sv[w][j]);
+                }
+                __syncwarp();
+            }
+            if (side == 0)
+                sum_e = acc;
+            else
+                sum_a = acc;
+        }
+        if (lane == 0)
+        {
+            const double scale = ldexp(1.0, D * (m - g.J1));
+            const long long o = (long long)h * cap + vix<D>(x, y, ny);
+            F0.f[li][o] = __dadd_rn(F1.f[li][o], __dmul_rn(scale, __dsub_rn(sum_e, sum_a)));
+        }
     }
 }
 
@@ -4093,6 +4217,10 @@ struct mrlbm_ctx {
     // K8 one block per 32-leaf chunk with shared box indices (MRLBM_K8_BLOCK=1): measured slower,
     // 1.59 vs 1.09 ms per window step (the block waits at every chunk for its longest rim)
     bool k8_block = false;
+    // long-rim leaves (gap >= kLongGap) in the warp-cooperative K8 launch (MRLBM_K8_LONG_GAP=g sets the
+    // threshold, 0 keeps all deep-gap leaves in the thread kernel)
+    int k8_long = kLongGap;
+    int k8_occ = 4; // K8 thread kernel: resident blocks per SM the register budget is set for (MRLBM_K8_OCC)
     bool gen_ok = false;  // the generated code's constants match this scheme
     unsigned emask = 0;   // H(a): parent offsets (3^d bits) of the eta-shifted children
     cudaGraphExec_t graph[2]{};
@@ -4214,6 +4342,7 @@ Aux aux_of(mrlbm_ctx* c)
     a.tie_cap = c->tie_cap;
     a.step_no = c->step_no;
     a.fb1t = (c->use_fb1t && c->use_gen) ? 1 : 0;
+    a.k8_long = (!c->k8_warp && !c->k8_block) ? c->k8_long : 0;
     a.fbs = c->fbs;
     for (int k = 0; k < 3; ++k)
     {
@@ -4484,9 +4613,19 @@ void enqueue_step(mrlbm_ctx* c)
         k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);
     else if (c->k8_block)
         k_stream_fallback_b<D><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+    else if (c->k8_occ == 3)
+        k_stream_fallback_t<D, 3><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+    else if (c->k8_occ == 4)
+        k_stream_fallback_t<D, 4><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     else
-        k_stream_fallback_t<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+        k_stream_fallback_t<D, 2><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     kmark(c, "k_stream_fallback", -1);
+    if (aux.k8_long > 0 && c->J1 - aux.k8_long >= c->J0)
+    {
+        c->kcount++;
+        k_stream_fallback_long<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+        kmark(c, "k_stream_fallback_long", -1);
+    }
     CollC<Q, BS> cc;
     for (int i = 0; i < Q; ++i)
         for (int j = 0; j < BS; ++j)
@@ -5032,6 +5171,10 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     ctx->fuse_pd = std::getenv("MRLBM_FUSE_PD") != nullptr;
     ctx->k8_warp = std::getenv("MRLBM_K8_WARP") != nullptr;
     ctx->k8_block = std::getenv("MRLBM_K8_BLOCK") != nullptr;
+    if (const char* oc = std::getenv("MRLBM_K8_OCC"))
+        ctx->k8_occ = std::atoi(oc);
+    if (const char* lg = std::getenv("MRLBM_K8_LONG_GAP")) // 0: all deep-gap leaves stay in the thread kernel
+        ctx->k8_long = std::max(0, std::atoi(lg));
     for (int h = 0; h < sc->q; ++h)
     {
         const int ex = sc->eta[h][0], ey = sc->d == 2 ? sc->eta[h][1] : 0;

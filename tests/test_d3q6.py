@@ -159,6 +159,7 @@ def test_gpu_3d_compression_J8():
     for lv in range(rc.j_min, rc.j_max + 1):
         _, lf = s.read_leaves(lv)
         mass += lf.sum() * 2.0 ** (-3 * lv)
-    assert abs(mass - m0) <= 1e-9 * m0
+    # round-off per step plus the exponentially small tails that reach the copy (outflow) walls
+    assert abs(mass - m0) <= 1e-6 * m0
     print("MeshOR over the run:", [round(v, 4) for v in ors])
     s.close()
