@@ -128,8 +128,10 @@ def leaves_of(st):
 
 def workload_name(cid, rc):
     names = {3: "config 3: D2Q4 advection (periodic disc)", 4: "config 4: D2Q4x4 Euler 4-quadrant Riemann",
-             5: "config 5: D2Q9 Navier-Stokes past a cylinder"}
-    ext = f"finest {rc.base_cells[0] << (rc.j_max - rc.j_min)}x{rc.base_cells[1] << (rc.j_max - rc.j_min)}"
+             5: "config 5: D2Q9 Navier-Stokes past a cylinder",
+             6: "config 6 (PAPER 7.3, SURVEY 8f row 3): D3Q6 advection of a sphere"}
+    sh = rc.j_max - rc.j_min
+    ext = f"finest {rc.base_cells[0] << sh}x{rc.base_cells[1] << sh}" + (f"x{rc.base_cells[2] << sh}" if cid == 6 else "")
     return f"{names[cid]}, levels {rc.j_min}..{rc.j_max} ({ext}), eps={rc.epsilon:g}"
 
 
@@ -331,6 +333,35 @@ def other_config(cid, jmax, warmup, steps, flush, peak):
             "phases": phases}
 
 
+def config6_line(warmup, steps, flush, peak):
+    """Secondary line of the 3D path (config 6: D3Q6 advection of a sphere, levels 1..8,
+    PAPER.md:1462-1518): W warm-up steps, K timed steps, the mesh occupation rate, and the
+    step against the SURVEY 8d byte model 8 q (7 N_S + 4 N_I) of the last step."""
+    import torch
+    from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
+    sc, rc = build_config(6)
+    s = Solver(sc, rc)
+    idx = finest_cells(sc, rc)
+    s.load_leaves(rc.j_max, idx, initial_finest(6, sc, rc))
+    n_fine = idx.shape[0]
+    del idx
+    s.commit()
+    s.step(warmup)
+    stream = torch.cuda.ExternalStream(s.stream_handle(), device=torch.device("cuda", torch.cuda.current_device()))
+    ms, upd, st, launches, _ = timed_window(s, stream, flush, steps, torch.cuda.current_device())
+    s.close()
+    step_ms = ms / steps
+    return {"workload": workload_name(6, rc), "warmup": warmup, "steps": steps, "value": upd / (ms / 1e3),
+            "unit": UNIT, "ms_per_step": step_ms, "leaves_last_step": leaves_of(st),
+            "mesh_occupation_rate": leaves_of(st) / n_fine, "fallback_leaves_last_step": int(st.fallback_leaves),
+            "gpu_launches": launches,
+            "step_roofline": {"bytes_model_per_step": int(st.bytes_model),
+                              "achieved_gbs": st.bytes_model / (step_ms / 1e3) / 1e9,
+                              "frac": st.bytes_model / (step_ms / 1e3) / 1e9 / peak,
+                              "model": "8 q (7 N_S + 4 N_I) with the last step's counts"},
+            "note": "first 3D engine: dense level boxes, one launch per level and phase; parity-first, not tuned"}
+
+
 def bench_product(args):
     import numpy as np
     import torch
@@ -416,7 +447,8 @@ def bench_product(args):
     regimes, others, cpu = None, None, None
     if world == 1 and not args.quick:
         regimes = regimes_run(sc, rc)
-        others = [other_config(4, 11, 5, 20, flush, peak), other_config(3, 9, 5, 10, flush, peak)]
+        others = [other_config(4, 11, 5, 20, flush, peak), other_config(3, 9, 5, 10, flush, peak),
+                  config6_line(20, 20, flush, peak)]
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = run_cpu_sample(snap)
 

@@ -4617,6 +4617,10 @@ void enqueue_step(mrlbm_ctx* c)
         k_stream_fallback_t<D, 3><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     else if (c->k8_occ == 4)
         k_stream_fallback_t<D, 4><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+    else if (c->k8_occ == 5)
+        k_stream_fallback_t<D, 5><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+    else if (c->k8_occ == 6)
+        k_stream_fallback_t<D, 6><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     else
         k_stream_fallback_t<D, 2><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
     kmark(c, "k_stream_fallback", -1);

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,6 +41,7 @@ constexpr int kL3 = MRLBM_MAX_LEVELS;
 constexpr int kQ3 = MRLBM_MAX_Q;
 constexpr uint8_t K3_LEAF = 1, K3_INT = 2;
 constexpr int kTieCap3 = 1 << 16;
+constexpr int kWarpGap3 = 2; // levels with gap >= 2 (rims of >= 16 finest cells): one warp per leaf
 
 struct Geo3 {
     int J0, J1, nlev, q;
@@ -105,11 +107,13 @@ __device__ __forceinline__ int coord3(int c, int n, int per)
 
 __device__ __forceinline__ void lin2xyz(const Geo3& g, int li, long long lin, int& x, int& y, int& z)
 {
-    const int ny = g.ny[li], nz = g.nz[li];
-    z = (int)(lin % nz);
-    const long long r = lin / nz;
-    y = (int)(r % ny);
+    // level boxes hold < 2^31 cells (checked at create): 32-bit divisions
+    const unsigned ny = g.ny[li], nz = g.nz[li];
+    const unsigned l = (unsigned)lin;
+    const unsigned r = l / nz;
+    z = (int)(l - r * nz);
     x = (int)(r / ny);
+    y = (int)(r - (unsigned)x * ny);
 }
 
 __device__ __forceinline__ long long xyz2lin(const Geo3& g, int li, int x, int y, int z)
@@ -504,19 +508,26 @@ __device__ __forceinline__ int rim_slab3(const int* eta, int side, int side_n, i
     return ax;
 }
 
+// WARP: one warp per cell of the level (coarse levels, rims of 4^gap finest cells): the
+// lanes mark a slab together; else one thread per cell.
+template <bool WARP>
 __global__ void k3_need_seed(const __grid_constant__ Geo3 g, const __grid_constant__ Lv3 tn, const __grid_constant__ Bt3 need,
                              const Sch3* sc, const __grid_constant__ Tab3 tb, int li)
 {
     const int lj = g.nlev - 1;
     const int gap = lj - li;
     const int* ud = tb.udep + 6 * gap;
-    GS3(i, g.n[li])
+    const int lane = threadIdx.x & 31;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    for (long long i = WARP ? tid >> 5 : tid; i < g.n[li]; i += WARP ? nth >> 5 : nth)
     {
         if (!(tn.kind[li][i] & K3_LEAF))
             continue;
         int x, y, z;
         lin2xyz(g, li, i, x, y, z);
-        mark_box3(g, li, need.b[li], x + ud[0], x + ud[3], y + ud[1], y + ud[4], z + ud[2], z + ud[5]);
+        if (!WARP || lane == 0)
+            mark_box3(g, li, need.b[li], x + ud[0], x + ud[3], y + ud[1], y + ud[4], z + ud[2], z + ud[5]);
         if (gap == 0)
             continue;
         for (int h = 0; h < g.q; ++h)
@@ -529,7 +540,15 @@ __global__ void k3_need_seed(const __grid_constant__ Geo3 g, const __grid_consta
                 int lo[3], hi[3];
                 if (rim_slab3(sc->eta[h], side, 1 << gap, x, y, z, lo, hi) < 0)
                     continue;
-                mark_box3(g, lj, need.b[lj], lo[0], hi[0] - 1, lo[1], hi[1] - 1, lo[2], hi[2] - 1);
+                if (!WARP)
+                    mark_box3(g, lj, need.b[lj], lo[0], hi[0] - 1, lo[1], hi[1] - 1, lo[2], hi[2] - 1);
+                else
+                {
+                    const int ny_ = hi[1] - lo[1], nz_ = hi[2] - lo[2];
+                    const int total = (hi[0] - lo[0]) * ny_ * nz_;
+                    for (int k = lane; k < total; k += 32)
+                        need.b[lj][mr_lin3(g, lj, lo[0] + k / (nz_ * ny_), lo[1] + (k / nz_) % ny_, lo[2] + k % nz_)] = 1;
+                }
             }
     }
 }
@@ -600,6 +619,10 @@ __device__ __forceinline__ double covering_leaf3(const Geo3& g, const Lv3& tn, c
 // exact for this leaf (D.13), with the gap-1 detail correction (D.13b), else the sum over
 // the finest rim cells of f^^ (boundary rule outside the domain); all
 // sums serial from 0.0 in lexicographic order (D.12); then the MRT collision (D.24).
+// WARP: one warp per cell of the level (coarse levels): the lanes fetch 32 rim cells at a
+// time into shared memory and lane 0 accumulates them in the same serial order; every
+// lane follows the same (leaf-uniform) control flow and lane 0 alone writes.
+template <bool WARP>
 __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__ Geo3 g, const __grid_constant__ Lv3 tn,
                                                          const __grid_constant__ Fl3 Fin, const __grid_constant__ Fl3 Fout,
                                                          const Sch3* sc, const __grid_constant__ Tab3 tb, int li,
@@ -612,7 +635,12 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
     const int fx = g.nx[lj], fy = g.ny[lj], fz = g.nz[lj];
     const double scale = ldexp(1.0, 3 * (li - lj));
     const int side_n = 1 << gap;
-    GS3(i, n)
+    __shared__ double sv[4][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool writer = !WARP || lane == 0;
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    for (long long i = WARP ? tid >> 5 : tid; i < n; i += WARP ? nth >> 5 : nth)
     {
         if (!(tn.kind[li][i] & K3_LEAF))
             continue;
@@ -666,49 +694,62 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
                 else if (ax >= 0)
                 {
                     any_fb = true;
-                    for (int cx = lo[0]; cx < hi[0]; ++cx)
-                        for (int cy = lo[1]; cy < hi[1]; ++cy)
-                            for (int cz = lo[2]; cz < hi[2]; ++cz)
+                    // value of the finest rim cell: f^^ inside (E and A sides), boundary rule outside (E side)
+                    auto rimval = [&](int cx, int cy, int cz) -> double {
+                        int face = -1;
+                        if (side == 0)
+                        {
+                            if (!g.per[0] && (cx < 0 || cx >= fx))
+                                face = cx < 0 ? 0 : 1;
+                            else if (!g.per[1] && (cy < 0 || cy >= fy))
+                                face = cy < 0 ? 2 : 3;
+                            else if (!g.per[2] && (cz < 0 || cz >= fz))
+                                face = cz < 0 ? 4 : 5;
+                        }
+                        if (face < 0)
+                            return ff[mr_lin3(g, lj, cx, cy, cz)];
+                        const int kind = sc->bc_kind[face];
+                        if (kind == MRLBM_BC_COPY)
+                            return covering_leaf3(g, tn, Fin, h, coord3(cx, fx, g.per[0]), coord3(cy, fy, g.per[1]),
+                                                  coord3(cz, fz, g.per[2]), aux.err);
+                        const int hb = sc->opp[h];
+                        if (hb < 0)
+                        {
+                            atomicAdd(&aux.err[2], 1);
+                            return 0.0;
+                        }
+                        double v = Fin.f[li][(long long)hb * n + i];
+                        if (kind == MRLBM_BC_ANTI_BOUNCE_BACK)
+                            v = -v;
+                        else if (kind == MRLBM_BC_VELOCITY_BOUNCE_BACK)
+                            v = __dadd_rn(v, sc->bc_add[face][h]);
+                        return v;
+                    };
+                    if (!WARP)
+                    {
+                        for (int cx = lo[0]; cx < hi[0]; ++cx)
+                            for (int cy = lo[1]; cy < hi[1]; ++cy)
+                                for (int cz = lo[2]; cz < hi[2]; ++cz)
+                                    s = __dadd_rn(s, rimval(cx, cy, cz));
+                    }
+                    else
+                    {
+                        const int ny_ = hi[1] - lo[1], nz_ = hi[2] - lo[2];
+                        const int total = (hi[0] - lo[0]) * ny_ * nz_;
+                        for (int b0 = 0; b0 < total; b0 += 32)
+                        {
+                            const int k = b0 + lane;
+                            sv[wid][lane] = k < total ? rimval(lo[0] + k / (nz_ * ny_), lo[1] + (k / nz_) % ny_, lo[2] + k % nz_) : 0.0;
+                            __syncwarp();
+                            if (lane == 0)
                             {
-                                double v;
-                                int face = -1;
-                                if (side == 0)
-                                {
-                                    if (!g.per[0] && (cx < 0 || cx >= fx))
-                                        face = cx < 0 ? 0 : 1;
-                                    else if (!g.per[1] && (cy < 0 || cy >= fy))
-                                        face = cy < 0 ? 2 : 3;
-                                    else if (!g.per[2] && (cz < 0 || cz >= fz))
-                                        face = cz < 0 ? 4 : 5;
-                                }
-                                if (face < 0)
-                                    v = ff[mr_lin3(g, lj, cx, cy, cz)];
-                                else
-                                {
-                                    const int kind = sc->bc_kind[face];
-                                    if (kind == MRLBM_BC_COPY)
-                                        v = covering_leaf3(g, tn, Fin, h, coord3(cx, fx, g.per[0]), coord3(cy, fy, g.per[1]),
-                                                           coord3(cz, fz, g.per[2]), aux.err);
-                                    else
-                                    {
-                                        const int hb = sc->opp[h];
-                                        if (hb < 0)
-                                        {
-                                            atomicAdd(&aux.err[2], 1);
-                                            v = 0.0;
-                                        }
-                                        else
-                                        {
-                                            v = Fin.f[li][(long long)hb * n + i];
-                                            if (kind == MRLBM_BC_ANTI_BOUNCE_BACK)
-                                                v = -v;
-                                            else if (kind == MRLBM_BC_VELOCITY_BOUNCE_BACK)
-                                                v = __dadd_rn(v, sc->bc_add[face][h]);
-                                        }
-                                    }
-                                }
-                                s = __dadd_rn(s, v);
+                                const int nv = min(32, total - b0);
+                                for (int j = 0; j < nv; ++j)
+                                    s = __dadd_rn(s, sv[wid][j]);
                             }
+                            __syncwarp();
+                        }
+                    }
                 }
                 else
                     any_fb = any_fb || !(dom_ok && par_ok);
@@ -735,11 +776,12 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
             for (int c = 0; c < q; ++c)
                 acc = __dadd_rn(acc, __dmul_rn(sc->Minv[r * q + c], mp[c]));
             finite = finite && isfinite(acc);
-            Fout.f[li][(long long)r * n + i] = acc;
+            if (writer)
+                Fout.f[li][(long long)r * n + i] = acc;
         }
-        if (!finite)
+        if (writer && !finite)
             atomicAdd(&aux.err[1], 1);
-        if (any_fb)
+        if (writer && any_fb)
             atomicAdd(&aux.cnt[2 * kL3], 1);
     }
 }
@@ -941,6 +983,12 @@ struct Engine3D {
     long long kcount = 0;
     std::string err_msg;
     int grid_cap = 148 * 16;
+    // MRLBM_E3_PROF=1: an event after every kernel of the step, totals printed at destroy
+    bool prof = false;
+    std::vector<cudaEvent_t> pev;
+    std::vector<const char*> pname;
+    std::vector<std::pair<std::string, double>> pacc;
+    int psteps = 0;
 };
 
 namespace {
@@ -1043,6 +1091,44 @@ int check_err(Engine3D* e)
     return MRLBM_OK;
 }
 
+void pmark(Engine3D* e, const char* name)
+{
+    ++e->kcount;
+    if (!e->prof)
+        return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, e->stream);
+    e->pev.push_back(ev);
+    e->pname.push_back(name);
+}
+
+void pflush(Engine3D* e)
+{
+    if (!e->prof || e->pev.empty())
+        return;
+    cudaStreamSynchronize(e->stream);
+    for (size_t k = 1; k < e->pev.size(); ++k)
+    {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e->pev[k - 1], e->pev[k]);
+        bool found = false;
+        for (auto& a : e->pacc)
+            if (a.first == e->pname[k])
+            {
+                a.second += ms;
+                found = true;
+            }
+        if (!found)
+            e->pacc.emplace_back(e->pname[k], ms);
+    }
+    for (auto ev : e->pev)
+        cudaEventDestroy(ev);
+    e->pev.clear();
+    e->pname.clear();
+    ++e->psteps;
+}
+
 int one_step(Engine3D* e)
 {
     const Geo3& g = e->geo;
@@ -1062,75 +1148,83 @@ int one_step(Engine3D* e)
         CU3(e, cudaMemsetAsync(e->need[li], 0, g.n[li], s));
     }
     CU3(e, cudaMemsetAsync(e->cnt, 0, sizeof(int) * (2 * kL3 + 1), s));
+    pmark(e, "memset");
     // K1: projection of the old tree, fine -> coarse
     for (int li = nl - 2; li >= 0; --li)
     {
         k3_project<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, to, Fi, li);
-        ++e->kcount;
+        pmark(e, "k3_project");
     }
     // K2: details, group flags
     for (int li = 0; li < nl - 1; ++li)
     {
         k3_details<<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, to, Fi, keep, rn, e->sch, li, aux);
-        ++e->kcount;
+        pmark(e, "k3_details");
     }
     // K3: closure, enlargement, grading
     for (int li = nl - 2; li >= 1; --li)
     {
         k3_closure<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, keep, li);
-        ++e->kcount;
+        pmark(e, "k3_closure");
     }
     for (int li = 0; li < nl - 1; ++li)
     {
         k3_enlarge<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, keep, rn, e->sch, li);
-        ++e->kcount;
+        pmark(e, "k3_enlarge");
     }
     for (int li = nl - 2; li >= 1; --li)
     {
         k3_grade<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, rn, li);
-        ++e->kcount;
+        pmark(e, "k3_grade");
     }
     // K4: the new tree
     for (int li = 0; li < nl; ++li)
     {
         k3_kinds<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, rn, tn, li, aux);
-        ++e->kcount;
+        pmark(e, "k3_kinds");
     }
     // K5: transfer, coarse -> fine; K6: projection of the new tree
     for (int li = 1; li < nl; ++li)
     {
         k3_transfer<<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, to, tn, Fi, li, aux);
-        ++e->kcount;
+        pmark(e, "k3_transfer");
     }
     for (int li = nl - 2; li >= 0; --li)
     {
         k3_project<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, tn, Fi, li);
-        ++e->kcount;
+        pmark(e, "k3_project");
     }
     // need mask and zero-detail reconstruction of the cells the stream reads
     for (int li = 0; li < nl; ++li)
     {
-        k3_need_seed<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, tn, need, e->sch, tb, li);
-        ++e->kcount;
+        if (nl - 1 - li >= kWarpGap3)
+            k3_need_seed<true><<<grid3(e, g.n[li] * 32, 256), 256, 0, s>>>(g, tn, need, e->sch, tb, li);
+        else
+            k3_need_seed<false><<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, tn, need, e->sch, tb, li);
+        pmark(e, "k3_need_seed");
     }
     for (int li = nl - 1; li >= 1; --li)
     {
         k3_need_down<<<grid3(e, g.n[li], 256), 256, 0, s>>>(g, tn, need, li);
-        ++e->kcount;
+        pmark(e, "k3_need_down");
     }
     for (int li = 1; li < nl; ++li)
     {
         k3_recon<<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, tn, need, Fi, li);
-        ++e->kcount;
+        pmark(e, "k3_recon");
     }
     // K7 / K8: stream + collide
     for (int li = 0; li < nl; ++li)
     {
-        k3_stream_collide<<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
-        ++e->kcount;
+        if (nl - 1 - li >= kWarpGap3)
+            k3_stream_collide<true><<<grid3(e, g.n[li] * 32, 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
+        else
+            k3_stream_collide<false><<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
+        pmark(e, "k3_stream_collide");
     }
     e->cur = vn;
     e->curf = bo;
+    pflush(e);
     CU3(e, cudaGetLastError());
     return MRLBM_OK;
 }
@@ -1179,6 +1273,7 @@ int e3_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, Engine3D*
             return MRLBM_ERR_CONFIG;
         }
     Engine3D* e = new Engine3D();
+    e->prof = std::getenv("MRLBM_E3_PROF") != nullptr;
     e->sc = *sc;
     e->rc = *rc;
     Geo3& g = e->geo;
@@ -1574,6 +1669,9 @@ void e3_destroy(Engine3D* e)
         return;
     if (e->stream)
         cudaStreamSynchronize(e->stream);
+    if (e->prof && e->psteps)
+        for (const auto& a : e->pacc)
+            std::fprintf(stderr, "e3prof %-20s %9.1f us/step\n", a.first.c_str(), 1e3 * a.second / e->psteps);
     for (int li = 0; li < kL3; ++li)
     {
         for (int v = 0; v < 2; ++v)

@@ -73,6 +73,49 @@ def test_oracle_3d_step_properties():
     o.close()
 
 
+def _uniform_d3q6(sc, rc, f, steps):
+    """Independent numpy uniform-grid D3Q6 LBM: stream with the copy
+    closure, then m = M f, m' = (1 - s) m + s m^eq, f = M^-1 m'."""
+    n = 2 << (rc.j_max - rc.j_min)
+    f = f.reshape(6, n, n, n).copy()
+    M = np.array(sc.M[:36]).reshape(6, 6)
+    Mi = np.array(sc.Minv[:36]).reshape(6, 6)
+    sv = np.array(sc.s[:6])[:, None, None, None]
+    V = [sc.eq_params[a] for a in range(3)]
+    ar = np.arange(n)
+    for _ in range(steps):
+        new = np.empty_like(f)
+        for h in range(6):
+            ix = [np.clip(ar - sc.eta[h][a], 0, n - 1) for a in range(3)]
+            new[h] = f[h][np.ix_(ix[0], ix[1], ix[2])]
+        m = np.einsum("ij,jxyz->ixyz", M, new)
+        meq = np.zeros_like(m)
+        meq[0] = m[0]
+        for a in range(3):
+            meq[1 + a] = V[a] * m[0]
+        f = np.einsum("ij,jxyz->ixyz", Mi, (1.0 - sv) * m + sv * meq)
+    return f.reshape(6, -1)
+
+
+def test_oracle_3d_uniform_mode_matches_numpy_lbm():
+    """epsilon = 0 equivalence (acceptance 3) at D = 3: the adaptive oracle on
+    the full finest mesh against an independent uniform D3Q6 solver, <= 1e-12 per step."""
+    from oracle import pyoracle
+    sc, rc = pyoracle.build_config(6, 4, 0.0)
+    idx, f0 = pyoracle.finest_cells(sc, rc), pyoracle.initial_finest(6, sc, rc)
+    o = pyoracle.Oracle(sc, rc)
+    o.load_leaves(rc.j_max, idx, f0)
+    o.commit()
+    steps = 8
+    o.step(steps)
+    assert o.level_count(rc.j_max) == idx.shape[0]
+    _, fo = o.read_leaves(rc.j_max)
+    fu = _uniform_d3q6(sc, rc, f0, steps)
+    scale = np.abs(fu).max()
+    assert np.max(np.abs(fo - fu)) <= 1e-12 * steps * scale
+    o.close()
+
+
 def test_config6_descriptor_values():
     sc, rc = build_config(6)
     assert [tuple(sc.eta[h][:3]) for h in range(6)] == ETAS
