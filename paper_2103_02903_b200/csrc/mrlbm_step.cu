@@ -950,13 +950,17 @@ constexpr int kLongGap = 4; // K8: gap from which a leaf's rims are evaluated by
 // The warp-cooperative launch wins when the long-rim leaves are few (their serial chains
 // set the duration of the thread kernel: settled regime 404 -> 150 us, transient window
 // 1089 -> 872 us) and loses when they are many (developing flow, thousands of gap-4 / 5
-// leaves: 331 -> 436 us), so the threshold moves up by two levels when more than
-// kLongMany leaves lie at or above it.  Counted per step by k_list_deep (fb_count[5]:
-// gap >= k8_long, fb_count[6]: gap >= k8_long + 2); both K8 launches evaluate the same rule.
+// leaves: 331 -> 436 us serialised), so the threshold moves up by kLongStep levels when more
+// than kLongMany leaves lie at or above it.  (With the two launches on forked streams a
+// step of 1 -- gap >= 5 in the warp launch, 229 us, beside gap 2..4 in the thread launch,
+// 168 us -- still lost to a step of 2 at step 3000: 1.345 vs 1.297 ms per step.)  Counted
+// per step by k_list_deep (fb_count[5]: gap >= k8_long, fb_count[6]: gap >= k8_long +
+// kLongStep); both K8 launches evaluate the same rule.
 constexpr int kLongMany = 2048;
+constexpr int kLongStep = 2;
 __device__ __forceinline__ int k8_long_gap(int base, const int* fb_count)
 {
-    return (base > 0 && fb_count[5] > kLongMany) ? base + 2 : base;
+    return (base > 0 && fb_count[5] > kLongMany) ? base + kLongStep : base;
 }
 
 template <int D>
@@ -1008,7 +1012,7 @@ __global__ void __launch_bounds__(256) k_list_deep(const __grid_constant__ Geo g
             }
             sbase = tot ? atomicAdd(aux.fb_count, tot) : 0;
             slong = tot && longrim ? atomicAdd(aux.fb_count + 5, tot) : 0;
-            if (tot && longrim && g.J1 - m >= aux.k8_long + 2)
+            if (tot && longrim && g.J1 - m >= aux.k8_long + kLongStep)
                 atomicAdd(aux.fb_count + 6, tot);
         }
         __syncthreads();
@@ -1026,7 +1030,7 @@ __global__ void __launch_bounds__(256) k_list_deep(const __grid_constant__ Geo g
                 aux.fb_mask[k] = fl.fbm[li][vi];
                 aux.fb_dmask[k] = fl.fbd[li][vi];
                 if (longrim)
-                    aux.fb_list[aux.fb_cap - 1 - (slong + r)] = make_int2(k, 0);
+                    aux.fb_list[aux.fb_cap - 1 - (slong + r)] = make_int2(k, m);
             }
             else
                 flag_err(aux.err, 2);
@@ -2748,8 +2752,9 @@ __global__ void __launch_bounds__(256, MINB) k_stream_fallback_t(const __grid_co
                         {
                             const int k = ti.x + k0 + j;
                             const int2 o = aux.toff[k];
-                            if (!tn.kind[li][mr_lin<D>(g, m, x + o.x, y + o.y)])
-                                flag_err(aux.err, 0);
+                            // (no kind check: the table offsets stay inside the 5^D box, which the ghost
+                            // layer materialises around every R cell, ghost_dist = 2 below the finest
+                            // level; K7's table path does not check either)
                             v[j] = __dmul_rn(aux.tw[k], fm[mr_vix<D>(g, m, x + o.x, y + o.y)]);
                         }
                     }
@@ -2815,9 +2820,14 @@ __global__ void __launch_bounds__(256) k_stream_fallback_long(const __grid_const
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    if (long_gap > aux.k8_long && aux.fb_count[6] == 0)
+        return; // many long-rim leaves, none at the raised threshold: all of them are the thread kernel's
     for (long long t = gw; t < (long long)nlong * q; t += nw)
     {
-        const int it = aux.fb_list[aux.fb_cap - 1 - (t / q)].x, h = (int)(t % q);
+        const int2 te = aux.fb_list[aux.fb_cap - 1 - (t / q)]; // (index into the list, level)
+        if (g.J1 - te.y < long_gap)
+            continue; // many long-rim leaves this step: the thread kernel takes this gap
+        const int it = te.x, h = (int)(t % q);
         const int2 e = aux.fb_list[it];
         const unsigned mask = aux.fb_mask[it];
         const int m = e.x, li = m - g.J0;
@@ -2826,8 +2836,6 @@ __global__ void __launch_bounds__(256) k_stream_fallback_long(const __grid_const
         int x, y;
         lin2xy_l<D>(e.y, ny, g.lny[li], x, y);
         const int gap = g.J1 - m;
-        if (gap < long_gap)
-            continue; // many long-rim leaves this step: the thread kernel takes this gap
         const int ex = sc->eta[h][0], ey = D == 1 ? 0 : sc->eta[h][1];
         double sum_e = 0.0, sum_a = 0.0;
         for (int side = 0; side < 2; ++side)
@@ -4217,6 +4225,12 @@ struct mrlbm_ctx {
     // K8 one block per 32-leaf chunk with shared box indices (MRLBM_K8_BLOCK=1): measured slower,
     // 1.59 vs 1.09 ms per window step (the block waits at every chunk for its longest rim)
     bool k8_block = false;
+    // the stream + collide launches are independent of one another (disjoint leaves, all read the
+    // transferred state) except K8 -> MODE 1; they fork onto side streams inside the step graph so
+    // that the small latency-bound ones overlap (MRLBM_SERIAL_STREAM=1: one stream)
+    bool fork_stream = true;
+    cudaStream_t side[5]{};
+    cudaEvent_t ev_fork = nullptr, ev_join[5]{};
     // long-rim leaves (gap >= kLongGap) in the warp-cooperative K8 launch (MRLBM_K8_LONG_GAP=g sets the
     // threshold, 0 keeps all deep-gap leaves in the thread kernel)
     int k8_long = kLongGap;
@@ -4607,7 +4621,22 @@ void enqueue_step(mrlbm_ctx* c)
     for (int m = c->J0 + 1; m <= c->J1; ++m)
         { c->kcount++; k_virtual<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, tn, Sf, m, aux);  kmark(c, "k_virtual", m); }
     phase_mark(c, 5);
-    // K7/K8 stream + collide (+ obstacle) on every new leaf
+    // K7/K8 stream + collide (+ obstacle) on every new leaf.  Fork: every launch below reads the
+    // transferred state (Sf) and writes its own leaves of Tf; only MODE 1 (collision of the deep-gap
+    // fallback leaves) reads what K8 wrote.  Not in profiling mode (the per-kernel events assume one stream).
+    const bool forked = c->fork_stream && !c->profiling;
+    cudaStream_t sK8L = s, sRim = s, sFb1t = s, sL12 = s, sCoarse = s;
+    if (forked)
+    {
+        cudaEventRecord(c->ev_fork, s);
+        for (int i = 0; i < 5; ++i)
+            cudaStreamWaitEvent(c->side[i], c->ev_fork, 0);
+        sK8L = c->side[0];
+        sRim = c->side[1];
+        sFb1t = c->side[2];
+        sL12 = c->side[3];
+        sCoarse = c->side[4];
+    }
     c->kcount++;
     if (c->k8_warp)
         k_stream_fallback<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux);
@@ -4627,7 +4656,7 @@ void enqueue_step(mrlbm_ctx* c)
     if (aux.k8_long > 0 && c->J1 - aux.k8_long >= c->J0)
     {
         c->kcount++;
-        k_stream_fallback_long<D><<<c->grid_cap, 256, 0, s>>>(g, tn, Tf, Sf, c->sch, aux);
+        k_stream_fallback_long<D><<<c->grid_cap, 256, 0, sK8L>>>(g, tn, Tf, Sf, c->sch, aux);
         kmark(c, "k_stream_fallback_long", -1);
     }
     CollC<Q, BS> cc;
@@ -4652,9 +4681,9 @@ void enqueue_step(mrlbm_ctx* c)
         {
             c->kcount++;
             if (frc)
-                k_fb1<D, Q, BS, EQ, GEN, kObs><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+                k_fb1<D, Q, BS, EQ, GEN, kObs><<<c->grid_cap, 32 * Q, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
             else
-                k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+                k_fb1<D, Q, BS, EQ, GEN><<<c->grid_cap, 32 * Q, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
             kmark(c, "k_fb1", -1);
         }
         else if (!c->rim_tpl)
@@ -4662,9 +4691,9 @@ void enqueue_step(mrlbm_ctx* c)
             // the listed boundary-rim gap-1 leaves: Q warps per batch, compact generic loops
             c->kcount++;
             if (frc)
-                k_fb1<D, Q, BS, EQ, false, kObs><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+                k_fb1<D, Q, BS, EQ, false, kObs><<<c->grid_cap, 32 * Q, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
             else
-                k_fb1<D, Q, BS, EQ, false><<<c->grid_cap, 32 * Q, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
+                k_fb1<D, Q, BS, EQ, false><<<c->grid_cap, 32 * Q, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, aux, cc);
             kmark(c, "k_fb1_rim", -1);
         }
         if constexpr (GEN)
@@ -4673,17 +4702,17 @@ void enqueue_step(mrlbm_ctx* c)
             LGrid l2 = make_lgrid(c, c->J1 - 1, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
             c->kcount += 2;
             if (frc)
-                k_stream_collide<D, Q, BS, EQ, GEN, 2, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 2, 1, kObs><<<nb, 256, 0, sFb1t>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
             else
-                k_stream_collide<D, Q, BS, EQ, GEN, 2, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 2, 1><<<nb, 256, 0, sFb1t>>>(g, tn, Tf, Sf, fl, c->sch, l2, aux, cc);
             kmark(c, "k_fb1t", -1);
             if (c->rim_tpl)
             {
                 LGrid l3 = make_lgrid(c, c->J1 - 1, c->J1 - 1, [&](int) { return 148; }, &nb);
                 if (frc)
-                    k_stream_collide<D, Q, BS, EQ, GEN, 3, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l3, aux, cc);
+                    k_stream_collide<D, Q, BS, EQ, GEN, 3, 1, kObs><<<nb, 256, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, l3, aux, cc);
                 else
-                    k_stream_collide<D, Q, BS, EQ, GEN, 3, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l3, aux, cc);
+                    k_stream_collide<D, Q, BS, EQ, GEN, 3, 1><<<nb, 256, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, l3, aux, cc);
                 kmark(c, "k_fb1_rim", -1);
             }
             else
@@ -4699,27 +4728,27 @@ void enqueue_step(mrlbm_ctx* c)
             // then every coarser level (gap classes 1 and >= 2)
             LGrid l0 = make_lgrid(c, c->J1, c->J1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
             if (frc)
-                k_stream_collide<D, Q, BS, EQ, GEN, 0, 0, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, 0, kObs><<<nb, 256, 0, sL12>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
             else
-                k_stream_collide<D, Q, BS, EQ, GEN, 0, 0><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, 0><<<nb, 256, 0, sL12>>>(g, tn, Tf, Sf, fl, c->sch, l0, aux, cc);
             kmark(c, "k_stream_collide", c->J1);
             if (c->J1 > c->J0)
             {
                 LGrid l1 = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], 256); }, &nb);
                 c->kcount++;
                 if (frc)
-                    k_stream_collide<D, Q, BS, EQ, GEN, 0, 1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
+                    k_stream_collide<D, Q, BS, EQ, GEN, 0, 1, kObs><<<nb, 256, 0, sCoarse>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
                 else
-                    k_stream_collide<D, Q, BS, EQ, GEN, 0, 1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
+                    k_stream_collide<D, Q, BS, EQ, GEN, 0, 1><<<nb, 256, 0, sCoarse>>>(g, tn, Tf, Sf, fl, c->sch, l1, aux, cc);
                 kmark(c, "k_stream_collide", -1);
             }
         }
         else
         {
             if (frc)
-                k_stream_collide<D, Q, BS, EQ, GEN, 0, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, -1, kObs><<<nb, 256, 0, sL12>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
             else
-                k_stream_collide<D, Q, BS, EQ, GEN, 0, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 0, -1><<<nb, 256, 0, sL12>>>(g, tn, Tf, Sf, fl, c->sch, lg, aux, cc);
             kmark(c, "k_stream_collide", -1);
         }
         // MODE 1: deep-gap fallback leaves (collide K8's output) by slot scan, and with
@@ -4729,6 +4758,12 @@ void enqueue_step(mrlbm_ctx* c)
         {
             LGrid lf = make_lgrid(c, c->J0, mtop, [&](int li) { return grid_for(c, g.cap[li] / 8, 256); }, &nb);
             c->kcount++;
+            if (forked)
+            {
+                // K8's long-rim launch ran on its own stream: its leaves are collided here
+                cudaEventRecord(c->ev_join[0], sK8L);
+                cudaStreamWaitEvent(s, c->ev_join[0], 0);
+            }
             if (frc)
                 k_stream_collide<D, Q, BS, EQ, GEN, 1, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, lf, aux, cc);
             else
@@ -4741,12 +4776,18 @@ void enqueue_step(mrlbm_ctx* c)
             LGrid l5 = make_lgrid(c, c->J1, c->J1, [&](int) { return 148; }, &nb);
             c->kcount++;
             if (frc)
-                k_stream_collide<D, Q, BS, EQ, GEN, 5, -1, kObs><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l5, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 5, -1, kObs><<<nb, 256, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, l5, aux, cc);
             else
-                k_stream_collide<D, Q, BS, EQ, GEN, 5, -1><<<nb, 256, 0, s>>>(g, tn, Tf, Sf, fl, c->sch, l5, aux, cc);
+                k_stream_collide<D, Q, BS, EQ, GEN, 5, -1><<<nb, 256, 0, sRim>>>(g, tn, Tf, Sf, fl, c->sch, l5, aux, cc);
             kmark(c, "k_stream_collide_fb0", -1);
         }
     }
+    if (forked)
+        for (int i = 0; i < 5; ++i)
+        {
+            cudaEventRecord(c->ev_join[i], c->side[i]);
+            cudaStreamWaitEvent(s, c->ev_join[i], 0);
+        }
     { c->kcount++; k_count_updates<<<1, 32, 0, s>>>(c->cnt[n], c->nlev, c->upd, c->step_no);  kmark(c, "k_count_updates", -1); }
     if (c->frc)
         { c->kcount++; k_force_sum<<<1, 1024, 0, s>>>(c->frc, c->frc_n, c->fhist, c->fhn, c->fcap);  kmark(c, "k_force_sum", -1); }
@@ -4962,6 +5003,12 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     int st = [&]() -> int
     {
         CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        for (int i = 0; i < 5; ++i)
+        {
+            CU(cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming));
+        }
         for (int v = 0; v < 2; ++v)
         {
             CU(cudaMalloc(&ctx->cnt[v], sizeof(int) * 4 * kL));
@@ -5175,6 +5222,7 @@ int mrlbm_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, mrlbm_
     ctx->fuse_pd = std::getenv("MRLBM_FUSE_PD") != nullptr;
     ctx->k8_warp = std::getenv("MRLBM_K8_WARP") != nullptr;
     ctx->k8_block = std::getenv("MRLBM_K8_BLOCK") != nullptr;
+    ctx->fork_stream = std::getenv("MRLBM_SERIAL_STREAM") == nullptr;
     if (const char* oc = std::getenv("MRLBM_K8_OCC"))
         ctx->k8_occ = std::atoi(oc);
     if (const char* lg = std::getenv("MRLBM_K8_LONG_GAP")) // 0: all deep-gap leaves stay in the thread kernel
@@ -5874,6 +5922,15 @@ void mrlbm_destroy(mrlbm_ctx* ctx)
     cudaFree(ctx->etad);
     cudaFree(ctx->pmaskd);
     cudaFree(ctx->umaskd);
+    for (int i = 0; i < 5; ++i)
+    {
+        if (ctx->side[i])
+            cudaStreamDestroy(ctx->side[i]);
+        if (ctx->ev_join[i])
+            cudaEventDestroy(ctx->ev_join[i]);
+    }
+    if (ctx->ev_fork)
+        cudaEventDestroy(ctx->ev_fork);
     for (auto& e : ctx->ev)
         if (e)
             cudaEventDestroy(e);
