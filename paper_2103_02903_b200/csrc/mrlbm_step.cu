@@ -4468,7 +4468,16 @@ void enqueue_step(mrlbm_ctx* c)
     {
         LGrid lz = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 16 + 1, T); }, &nb);
         c->kcount++;
-        k_zero_flags<<<nb, T, 0, s>>>(g, fl, lz, c->fbc);
+        // the per-step flags are first touched by the details: zeroing runs beside the K1 projections
+        const bool fz = c->fork_stream && !c->profiling && !c->fuse_pd;
+        if (fz)
+        {
+            cudaEventRecord(c->ev_fork, s);
+            cudaStreamWaitEvent(c->side[0], c->ev_fork, 0);
+        }
+        k_zero_flags<<<nb, T, 0, fz ? c->side[0] : s>>>(g, fl, lz, c->fbc);
+        if (fz)
+            cudaEventRecord(c->ev_join[0], c->side[0]);
         kmark(c, "k_zero_flags", -1);
     }
     phase_mark(c, 0);
@@ -4489,6 +4498,8 @@ void enqueue_step(mrlbm_ctx* c)
         for (int m = c->J1 - 1; m >= c->J0; --m)
             { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
         phase_mark(c, 1);
+        if (c->fork_stream && !c->profiling)
+            cudaStreamWaitEvent(s, c->ev_join[0], 0); // k_zero_flags
         // K2 details + flags
         LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
         c->kcount++;
@@ -4582,10 +4593,22 @@ void enqueue_step(mrlbm_ctx* c)
         k_list_deep<D><<<nb, 256, 0, s>>>(g, fl, ld, aux);
         kmark(c, "k_list_deep", -1);
     }
+    // the gap-1 list reads leaf kinds and fallback masks only (band and ghost marking never change a
+    // leaf byte's value): it runs beside k_list_deep / k_band / the ghost passes
+    const bool fl1 = c->fork_stream && !c->profiling;
+    bool fl1_used = false;
     if (GEN && c->use_fb1t && c->J1 > c->J0)
     {
         c->kcount++;
-        k_list_fb1<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);
+        if (fl1)
+        {
+            cudaEventRecord(c->ev_fork, s);
+            cudaStreamWaitEvent(c->side[1], c->ev_fork, 0);
+            fl1_used = true;
+        }
+        k_list_fb1<D><<<c->grid_cap, 256, 0, fl1 ? c->side[1] : s>>>(g, fl, aux);
+        if (fl1)
+            cudaEventRecord(c->ev_join[1], c->side[1]);
         kmark(c, "k_list_fb1", -1);
     }
     { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);  kmark(c, "k_band", -1); }
@@ -4612,6 +4635,8 @@ void enqueue_step(mrlbm_ctx* c)
         kmark(c, "k_ghost_v", -1);
     }
     launch_compaction_all(c, g, fl, tn);
+    if (fl1_used)
+        cudaStreamWaitEvent(s, c->ev_join[1], 0); // k_list_fb1
     phase_mark(c, 4);
     // K5 transfer (top-down), K6 projection of the new tree, virtual values (top-down)
     for (int m = c->J0; m <= c->J1; ++m)
