@@ -4569,6 +4569,35 @@ void enqueue_step(mrlbm_ctx* c)
         k_kinds_v<<<nb, T, 0, s>>>(g, fl, lg);
         kmark(c, "k_kinds_v", -1);
     }
+    // Pass 1 of the ghost dilation reads R membership only (fixed by the kinds kernels; the fallback
+    // bit and the band marks never touch the leaf / internal bits) and writes its own scratch (keep,
+    // free after K3): it runs beside the fallback classification, the lists and the band marking.
+    // Pass 2 rewrites whole 16-byte chunks of the kinds, so it stays after the band marking.
+    const bool fgr = c->fork_stream && !c->profiling && D == 2;
+    cudaStream_t sGr = fgr ? c->side[2] : s;
+    auto ghost_rows = [&]() {
+        if (mv > c->J0 && D == 2)
+        {
+            LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
+            c->kcount++;
+            k_ghost_rows<D><<<nb, T, 0, sGr>>>(g, fl, lg);
+            kmark(c, "k_ghost_rows", -1);
+        }
+        if (mv <= c->J1)
+        {
+            LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
+            c->kcount++;
+            k_ghost_rows_v<<<nb, T, 0, sGr>>>(g, fl, lg);
+            kmark(c, "k_ghost_rows_v", -1);
+        }
+    };
+    if (fgr)
+    {
+        cudaEventRecord(c->ev_fork, s);
+        cudaStreamWaitEvent(sGr, c->ev_fork, 0);
+        ghost_rows();
+        cudaEventRecord(c->ev_join[2], sGr);
+    }
     if (mv > c->J0)
     {
         LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
@@ -4612,15 +4641,13 @@ void enqueue_step(mrlbm_ctx* c)
         kmark(c, "k_list_fb1", -1);
     }
     { c->kcount++; k_band<D><<<c->grid_cap, 256, 0, s>>>(g, fl, aux);  kmark(c, "k_band", -1); }
+    if (fgr)
+        cudaStreamWaitEvent(s, c->ev_join[2], 0);
+    else
+        ghost_rows();
     if (mv > c->J0)
     {
         LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
-        if (D == 2)
-        {
-            c->kcount++;
-            k_ghost_rows<D><<<nb, T, 0, s>>>(g, fl, lg);
-            kmark(c, "k_ghost_rows", -1);
-        }
         c->kcount++;
         k_ghost<D><<<nb, T, 0, s>>>(g, fl, lg);
         kmark(c, "k_ghost", -1);
@@ -4628,9 +4655,7 @@ void enqueue_step(mrlbm_ctx* c)
     if (mv <= c->J1)
     {
         LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
-        c->kcount += 2;
-        k_ghost_rows_v<<<nb, T, 0, s>>>(g, fl, lg);
-        kmark(c, "k_ghost_rows_v", -1);
+        c->kcount++;
         k_ghost_v<<<nb, T, 0, s>>>(g, fl, lg);
         kmark(c, "k_ghost_v", -1);
     }
