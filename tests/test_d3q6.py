@@ -134,7 +134,7 @@ def _pair(J, eps=-1.0):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("J,eps,steps", [(4, -1.0, 12), (5, -1.0, 16), (4, 0.0, 8), (6, -1.0, 6)])
+@pytest.mark.parametrize("J,eps,steps", [(4, -1.0, 12), (5, -1.0, 16), (4, 0.0, 8), (6, -1.0, 6), (7, -1.0, 4)])
 def test_gpu_3d_step_parity(J, eps, steps):
     """CUDA 3D engine vs the oracle at D = 3, after every step: identical leaf sets,
     fields within 1e-12 relative (north_star) -- bit-identical in practice."""
@@ -177,6 +177,47 @@ def test_gpu_3d_reload_roundtrip():
         assert np.array_equal(ai, bi) and np.array_equal(af.view(np.uint64), bf.view(np.uint64))
     a.close()
     b.close()
+
+
+@pytest.mark.gpu
+def test_gpu_3d_restart_window_J8():
+    """Parity at the paper's size (levels 1..8, 256^3 finest): the GPU state after 60 steps is
+    read back through the ABI and loaded into the oracle and into a second GPU context; three
+    more steps on each, compared bit for bit on every level after every step (gaps up to 5:
+    the long-rim recursive path of the coarse leaves)."""
+    from oracle import pyoracle
+    from paper_2103_02903_b200 import Solver
+    from parity_util import compare
+    sc, rc = build_config(6)
+    a = Solver(sc, rc)
+    idx = finest_cells(sc, rc)
+    a.load_leaves(rc.j_max, idx, initial_finest(6, sc, rc))
+    del idx
+    a.commit()
+    a.step(60)
+    b = Solver(sc, rc)
+    o = pyoracle.Oracle(sc, rc)
+    total = 0
+    for lv in range(rc.j_min, rc.j_max + 1):
+        i, f = a.read_leaves(lv)
+        total += i.shape[0]
+        if i.shape[0]:
+            b.load_leaves(lv, i, f)
+            o.load_leaves(lv, i, f)
+    b.commit()
+    o.commit()
+    assert 200_000 < total < 600_000
+    for k in range(3):
+        sa = a.step(1)
+        b.step(1)
+        o.step(1)
+        rel, bitwise, n = compare(b, o, rc, f"config 6 J=8 window step {60 + k}")
+        assert bitwise, rel
+        rel2, bitwise2, _ = compare(a, o, rc, f"config 6 J=8 continued run step {60 + k}")
+        assert bitwise2, rel2
+        assert sa.fallback_leaves == o.fallback_leaves()
+    for s_ in (a, b, o):
+        s_.close()
 
 
 @pytest.mark.gpu
