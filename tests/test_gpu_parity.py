@@ -88,14 +88,15 @@ def test_generic_table_path_parity(cid, J, monkeypatch):
 
 
 @pytest.mark.parametrize("env", ["MRLBM_FUSE_PD", "MRLBM_NO_FB1T", "MRLBM_RIM_TPL", "MRLBM_K8_WARP", "MRLBM_K8_BLOCK",
-                                 "MRLBM_K8_LONG_GAP=0", "MRLBM_K8_LONG_GAP=2", "MRLBM_K8_OCC=2"])
+                                 "MRLBM_K8_LONG_GAP=0", "MRLBM_K8_LONG_GAP=2", "MRLBM_K8_OCC=2", "MRLBM_SERIAL_STREAM"])
 @pytest.mark.parametrize("cid,J", [(3, 6), (4, 6), (5, 7)])
 def test_kernel_variant_parity(cid, J, env, monkeypatch):
     """The alternative kernel schedules stay bit-identical to the oracle: fused
     projection + details; all gap-1 fallback leaves in the block kernel k_fb1 (slot
     scan, no segment lists); boundary-rim gap-1 leaves thread per leaf (K7 MODE 3); the K8
     variants (one warp / one block per chunk, every deep-gap leaf
-    in the thread kernel or in the warp-cooperative one, another register budget)."""
+    in the thread kernel or in the warp-cooperative one, another register budget); the step graph
+    without forked streams."""
     name, _, val = env.partition("=")
     monkeypatch.setenv(name, val or "1")
     sc, rc, gpu, ora = make_pair(cid, J)
