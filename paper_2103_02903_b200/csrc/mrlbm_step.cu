@@ -1608,16 +1608,14 @@ __global__ void k_ghost_v(const __grid_constant__ Geo g, const __grid_constant__
             acc.v.z |= t.z;
             acc.v.w |= t.w;
         }
-        bool chg = false;
+        // byte stores of the marked cells only: the classification (fallback bit on leaf bytes) and
+        // the band marking (0 -> K_VIRT) run beside this kernel, and a whole-chunk store of the
+        // snapshot would undo theirs
+        uint8_t* kb = fl.kind[li] + c * 16;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
             if (k.b[j] == 0 && acc.b[j])
-            {
-                k.b[j] = K_VIRT;
-                chg = true;
-            }
-        if (chg)
-            reinterpret_cast<uint4*>(fl.kind[li])[c] = k.v;
+                kb[j] = K_VIRT;
     }
 }
 
@@ -4572,8 +4570,10 @@ void enqueue_step(mrlbm_ctx* c)
     // Pass 1 of the ghost dilation reads R membership only (fixed by the kinds kernels; the fallback
     // bit and the band marks never touch the leaf / internal bits) and writes its own scratch (keep,
     // free after K3): it runs beside the fallback classification, the lists and the band marking.
-    // Pass 2 rewrites whole 16-byte chunks of the kinds, so it stays after the band marking.
-    const bool fgr = c->fork_stream && !c->profiling && D == 2;
+    // Pass 2 marks 0 -> K_VIRT with byte stores, like the band marking: both only ever write
+    // K_VIRT into bytes without a leaf / internal bit, so they commute.  The whole ghost
+    // dilation runs beside classification, lists and bands; the compaction waits for both.
+    const bool fgr = c->fork_stream && !c->profiling;
     cudaStream_t sGr = fgr ? c->side[2] : s;
     auto ghost_rows = [&]() {
         if (mv > c->J0 && D == 2)
@@ -4591,11 +4591,28 @@ void enqueue_step(mrlbm_ctx* c)
             kmark(c, "k_ghost_rows_v", -1);
         }
     };
+    auto ghost_marks = [&]() {
+        if (mv > c->J0)
+        {
+            LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
+            c->kcount++;
+            k_ghost<D><<<nb, T, 0, sGr>>>(g, fl, lg);
+            kmark(c, "k_ghost", -1);
+        }
+        if (mv <= c->J1)
+        {
+            LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
+            c->kcount++;
+            k_ghost_v<<<nb, T, 0, sGr>>>(g, fl, lg);
+            kmark(c, "k_ghost_v", -1);
+        }
+    };
     if (fgr)
     {
         cudaEventRecord(c->ev_fork, s);
         cudaStreamWaitEvent(sGr, c->ev_fork, 0);
         ghost_rows();
+        ghost_marks();
         cudaEventRecord(c->ev_join[2], sGr);
     }
     if (mv > c->J0)
@@ -4644,20 +4661,9 @@ void enqueue_step(mrlbm_ctx* c)
     if (fgr)
         cudaStreamWaitEvent(s, c->ev_join[2], 0);
     else
+    {
         ghost_rows();
-    if (mv > c->J0)
-    {
-        LGrid lg = make_lgrid(c, c->J0, mv - 1, blocks_s, &nb);
-        c->kcount++;
-        k_ghost<D><<<nb, T, 0, s>>>(g, fl, lg);
-        kmark(c, "k_ghost", -1);
-    }
-    if (mv <= c->J1)
-    {
-        LGrid lg = make_lgrid(c, mv, c->J1, blocks_v, &nb);
-        c->kcount++;
-        k_ghost_v<<<nb, T, 0, s>>>(g, fl, lg);
-        kmark(c, "k_ghost_v", -1);
+        ghost_marks();
     }
     launch_compaction_all(c, g, fl, tn);
     if (fl1_used)
