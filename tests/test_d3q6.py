@@ -275,3 +275,68 @@ def test_gpu_3d_compression_J8():
     assert abs(mass - m0) <= 1e-6 * m0
     print("MeshOR over the run:", [round(v, 4) for v in ors])
     s.close()
+
+
+# ----------------------------------------------------------------------------- ties in 3D
+TIE_CELL = (5, 9, 6)
+
+
+def _crafted3(delta, eps=7.0, J=4):
+    """All populations 0 except population 0 of one finest cell = delta: the projected parent is
+    delta / 8, its neighbours 0, so the group metric is exactly 7 delta / 8; with delta = 8 and
+    eps = 7 it equals eps_l = 2^{3(l-J)} eps at every level (the 3D form of tests/test_ties.py)."""
+    sc, rc = build_config(6, J, eps)
+    idx = finest_cells(sc, rc)
+    f = np.zeros((sc.q, idx.shape[0]))
+    n = 2 << (J - rc.j_min)
+    f[0, (TIE_CELL[0] * n + TIE_CELL[1]) * n + TIE_CELL[2]] = delta
+    return sc, rc, idx, f
+
+
+def _expected_ties3(rc, eps=7.0):
+    out = []
+    # (not l = J_min + 1: the level-1 box is 2^3 cells, so the parent's clamped stencil holds the
+    # parent itself and the metric there is not 7/8 of the value)
+    for l in range(rc.j_min + 2, rc.j_max + 1):
+        sh = rc.j_max - l + 1
+        thr = float(np.ldexp(eps, 3 * (l - rc.j_max)))
+        out.append((1, l, TIE_CELL[0] >> sh, TIE_CELL[1] >> sh, TIE_CELL[2] >> sh, 0, thr, thr))
+    return out
+
+
+def test_oracle_3d_exact_ties_logged_and_kept():
+    from oracle import pyoracle
+    sc, rc, idx, f = _crafted3(8.0)
+    o = pyoracle.Oracle(sc, rc)
+    o.load_leaves(rc.j_max, idx, f)
+    o.commit()
+    o.step(1)
+    assert o.tie_log() == _expected_ties3(rc)
+    li, _ = o.read_leaves(rc.j_max)
+    sib = {tuple(2 * (TIE_CELL[a] // 2) + b[a] for a in range(3)) for b in np.ndindex(2, 2, 2)}
+    assert sib <= {tuple(r) for r in li}  # inclusive threshold: the group is kept
+    o.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("delta", [8.0, 8.0 * (1 + 5e-13), 8.0 * (1 - 5e-13), 8.0 * (1 + 1e-11)])
+def test_gpu_3d_tie_log_matches_oracle(delta):
+    from oracle import pyoracle
+    from paper_2103_02903_b200 import Solver
+    from parity_util import compare
+    sc, rc, idx, f = _crafted3(delta)
+    g = Solver(sc, rc)
+    o = pyoracle.Oracle(sc, rc)
+    for s_ in (g, o):
+        s_.load_leaves(rc.j_max, idx, f)
+        s_.commit()
+        s_.step(1)
+    assert g.tie_log() == o.tie_log()
+    if delta == 8.0:
+        assert g.tie_log() == _expected_ties3(rc)
+    if delta == 8.0 * (1 + 1e-11):
+        assert [t for t in g.tie_log() if t[1] == rc.j_max] == []
+    rel, bitwise, _ = compare(g, o, rc, f"3D ties delta={delta}")
+    assert bitwise
+    g.close()
+    o.close()
