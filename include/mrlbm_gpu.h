@@ -160,6 +160,10 @@ int mrlbm_read_leaves(mrlbm_ctx* ctx, int level, int32_t* idx, double* f);
    when more records were logged than the device buffer holds (65536).  reset != 0
    clears the log.  The oracle logs the same records (tests/test_ties.py). */
 int mrlbm_tie_log(mrlbm_ctx* ctx, mrlbm_tie_record* out, int cap, int64_t* n, int reset);
+/* Profiling of the following mrlbm_step calls (eager launches instead of the step graph):
+   on = 1: a CUDA event after every kernel, everything on one stream (mrlbm_profile_text,
+           ms_phase); on = 2: phase events only, the step's independent launches forked onto
+           side streams as in the graph (ms_phase adds up to the step); 0: off. */
 int mrlbm_set_profiling(mrlbm_ctx* ctx, int on);
 int mrlbm_set_graph(mrlbm_ctx* ctx, int on);
 /* per-kernel device times accumulated over profiled steps: lines "kernel level ms launches" */

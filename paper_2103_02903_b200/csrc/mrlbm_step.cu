@@ -4209,7 +4209,7 @@ struct mrlbm_ctx {
     int cur = 0;
     int curf = 0; // F[curf] holds the state f* (dense, indexed by the linear cell index)
     bool committed = false;
-    bool profiling = false;
+    int profiling = 0; // 1: an event after every kernel, one stream; 2: phase events only, forks active
     bool use_graph = true;
     bool use_gen = false; // generated stream / collision path (built-in velocity sets)
     bool use_fb1t = true; // gap-1 fallback leaves thread per leaf (K7 MODE 2) instead of k_fb1; MRLBM_NO_FB1T=1 turns it off
@@ -4387,7 +4387,7 @@ void kmark(mrlbm_ctx* c, const char* name, int level);
 
 void kmark(mrlbm_ctx* c, const char* name, int level)
 {
-    if (!c->profiling)
+    if (c->profiling != 1)
         return;
     if (c->kn >= static_cast<int>(c->kev.size()))
     {
@@ -4467,7 +4467,7 @@ void enqueue_step(mrlbm_ctx* c)
         LGrid lz = make_lgrid(c, c->J0, c->J1, [&](int li) { return grid_for(c, g.cap[li] / 16 + 1, T); }, &nb);
         c->kcount++;
         // the per-step flags are first touched by the details: zeroing runs beside the K1 projections
-        const bool fz = c->fork_stream && !c->profiling && !c->fuse_pd;
+        const bool fz = c->fork_stream && c->profiling != 1 && !c->fuse_pd;
         if (fz)
         {
             cudaEventRecord(c->ev_fork, s);
@@ -4496,7 +4496,7 @@ void enqueue_step(mrlbm_ctx* c)
         for (int m = c->J1 - 1; m >= c->J0; --m)
             { c->kcount++; k_project<D, Q><<<grid_for(c, g.cap[m - c->J0], T), T, 0, s>>>(g, to, Sf, m, aux);  kmark(c, "k_project", m); }
         phase_mark(c, 1);
-        if (c->fork_stream && !c->profiling)
+        if (c->fork_stream && c->profiling != 1)
             cudaStreamWaitEvent(s, c->ev_join[0], 0); // k_zero_flags
         // K2 details + flags
         LGrid lg = make_lgrid(c, c->J0, c->J1 - 1, [&](int li) { return grid_for(c, g.cap[li], T); }, &nb);
@@ -4573,7 +4573,7 @@ void enqueue_step(mrlbm_ctx* c)
     // Pass 2 marks 0 -> K_VIRT with byte stores, like the band marking: both only ever write
     // K_VIRT into bytes without a leaf / internal bit, so they commute.  The whole ghost
     // dilation runs beside classification, lists and bands; the compaction waits for both.
-    const bool fgr = c->fork_stream && !c->profiling;
+    const bool fgr = c->fork_stream && c->profiling != 1;
     cudaStream_t sGr = fgr ? c->side[2] : s;
     auto ghost_rows = [&]() {
         if (mv > c->J0 && D == 2)
@@ -4641,7 +4641,7 @@ void enqueue_step(mrlbm_ctx* c)
     }
     // the gap-1 list reads leaf kinds and fallback masks only (band and ghost marking never change a
     // leaf byte's value): it runs beside k_list_deep / k_band / the ghost passes
-    const bool fl1 = c->fork_stream && !c->profiling;
+    const bool fl1 = c->fork_stream && c->profiling != 1;
     bool fl1_used = false;
     if (GEN && c->use_fb1t && c->J1 > c->J0)
     {
@@ -4680,7 +4680,7 @@ void enqueue_step(mrlbm_ctx* c)
     // K7/K8 stream + collide (+ obstacle) on every new leaf.  Fork: every launch below reads the
     // transferred state (Sf) and writes its own leaves of Tf; only MODE 1 (collision of the deep-gap
     // fallback leaves) reads what K8 wrote.  Not in profiling mode (the per-kernel events assume one stream).
-    const bool forked = c->fork_stream && !c->profiling;
+    const bool forked = c->fork_stream && c->profiling != 1;
     cudaStream_t sK8L = s, sRim = s, sFb1t = s, sL12 = s, sCoarse = s;
     if (forked)
     {
@@ -5713,7 +5713,7 @@ int mrlbm_set_profiling(mrlbm_ctx* ctx, int on)
 {
     if (!ctx)
         return MRLBM_ERR_CONFIG;
-    ctx->profiling = on != 0;
+    ctx->profiling = on < 0 ? 0 : (on > 2 ? 2 : on);
     return MRLBM_OK;
 }
 

@@ -155,7 +155,9 @@ class Solver:
         return fx, fy
 
     def set_profiling(self, on=True):
-        self._check(self.L.mrlbm_set_profiling(self.h, int(bool(on))))
+        """True / 1: an event after every kernel (one stream); 2: phase events only with the
+        step's forks active; False / 0: off."""
+        self._check(self.L.mrlbm_set_profiling(self.h, int(on)))
 
     def profile_text(self, reset=True):
         """Per-kernel device times of the profiled steps: {(kernel, level): (ms, launches)}."""
