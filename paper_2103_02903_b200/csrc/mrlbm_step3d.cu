@@ -41,7 +41,9 @@ constexpr int kL3 = MRLBM_MAX_LEVELS;
 constexpr int kQ3 = MRLBM_MAX_Q;
 constexpr uint8_t K3_LEAF = 1, K3_INT = 2;
 constexpr int kTieCap3 = 1 << 16;
-constexpr int kWarpGap3 = 2; // levels with gap >= 2 (rims of >= 16 finest cells): one warp per leaf
+constexpr int kWarpGap3 = 2;  // levels with gap >= 2 (rims of >= 16 finest cells): one warp per leaf
+constexpr int kBlockGap3 = 5; // levels with gap >= 5 (rims of >= 1024 cells): one block of 2 q warps per leaf
+                              // (measured at J = 8: stream + collide 2233 us without, 2280 / 1990 / 1857 us from gap 3 / 4 / 5)
 
 struct Geo3 {
     int J0, J1, nlev, q;
@@ -194,6 +196,29 @@ __device__ __forceinline__ bool load_stencil3(const Geo3& g, int li, const doubl
     return ok;
 }
 
+// the 27 linear indices of the stencil around (px, py, pz), MR rule, computed once per cell and
+// reused for every population; ok = every stencil cell has kind != 0 when kind is given
+__device__ __forceinline__ bool stencil_idx3(const Geo3& g, int li, const uint8_t* kind, int px, int py, int pz, int* lin)
+{
+    int xs[3], ys[3], zs[3];
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+    {
+        xs[o] = coord3(px + o - 1, g.nx[li], g.per[0]) * g.ny[li];
+        ys[o] = coord3(py + o - 1, g.ny[li], g.per[1]);
+        zs[o] = coord3(pz + o - 1, g.nz[li], g.per[2]);
+    }
+    bool ok = true;
+#pragma unroll
+    for (int o = 0; o < 27; ++o)
+    {
+        lin[o] = (xs[o / 9] + ys[(o / 3) % 3]) * g.nz[li] + zs[o % 3]; // < 2^31 cells per level box
+        if (kind)
+            ok = ok && kind[lin[o]] != 0;
+    }
+    return ok;
+}
+
 // ------------------------------------------------------------------ K1 / K6 projection
 // internal node = mean of its 8 children in children order (prediction.hpp:51-60)
 __global__ void __launch_bounds__(256) k3_project(const __grid_constant__ Geo3 g, const __grid_constant__ Lv3 t,
@@ -263,11 +288,15 @@ __global__ void __launch_bounds__(128) k3_details(const __grid_constant__ Geo3 g
         lin2xyz(g, li, i, x, y, z);
         const long long c0 = ((long long)(2 * x) * ny1 + 2 * y) * nz1 + 2 * z;
         double metric = 0.0;
-        bool ok = true;
+        int lin[27];
+        const bool ok = stencil_idx3(g, li, t.kind[li], x, y, z, lin);
         for (int h = 0; h < g.q; ++h)
         {
             double st[27];
-            ok = load_stencil3(g, li, F.f[li] + (long long)h * n, t.kind[li], x, y, z, st) && ok;
+            const double* fp = F.f[li] + (long long)h * n;
+#pragma unroll
+            for (int o = 0; o < 27; ++o)
+                st[o] = fp[lin[o]];
             const double* src = F.f[li + 1] + (long long)h * n1;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
@@ -434,11 +463,15 @@ __global__ void __launch_bounds__(128) k3_transfer(const __grid_constant__ Geo3 
             continue;
         int x, y, z;
         lin2xyz(g, li, i, x, y, z);
-        bool ok = true;
+        int lin[27];
+        const bool ok = stencil_idx3(g, li - 1, tn.kind[li - 1], x >> 1, y >> 1, z >> 1, lin);
         for (int h = 0; h < g.q; ++h)
         {
             double st[27];
-            ok = load_stencil3(g, li - 1, F.f[li - 1] + (long long)h * np, tn.kind[li - 1], x >> 1, y >> 1, z >> 1, st) && ok;
+            const double* fp = F.f[li - 1] + (long long)h * np;
+#pragma unroll
+            for (int o = 0; o < 27; ++o)
+                st[o] = fp[lin[o]];
             F.f[li][(long long)h * n + i] = predict3(st, x & 1, y & 1, z & 1);
         }
         if (!ok)
@@ -578,10 +611,15 @@ __global__ void __launch_bounds__(128) k3_recon(const __grid_constant__ Geo3 g, 
             continue;
         int x, y, z;
         lin2xyz(g, li, i, x, y, z);
+        int lin[27];
+        stencil_idx3(g, li - 1, nullptr, x >> 1, y >> 1, z >> 1, lin);
         for (int h = 0; h < g.q; ++h)
         {
             double st[27];
-            load_stencil3(g, li - 1, F.f[li - 1] + (long long)h * np, nullptr, x >> 1, y >> 1, z >> 1, st);
+            const double* fp = F.f[li - 1] + (long long)h * np;
+#pragma unroll
+            for (int o = 0; o < 27; ++o)
+                st[o] = fp[lin[o]];
             F.f[li][(long long)h * n + i] = predict3(st, x & 1, y & 1, z & 1);
         }
     }
@@ -619,11 +657,16 @@ __device__ __forceinline__ double covering_leaf3(const Geo3& g, const Lv3& tn, c
 // exact for this leaf (D.13), with the gap-1 detail correction (D.13b), else the sum over
 // the finest rim cells of f^^ (boundary rule outside the domain); all
 // sums serial from 0.0 in lexicographic order (D.12); then the MRT collision (D.24).
-// WARP: one warp per cell of the level (coarse levels): the lanes fetch 32 rim cells at a
+// MODE 1: one warp per cell of the level (coarse levels): the lanes fetch 32 rim cells at a
 // time into shared memory and lane 0 accumulates them in the same serial order; every
 // lane follows the same (leaf-uniform) control flow and lane 0 alone writes.
-template <bool WARP>
-__global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__ Geo3 g, const __grid_constant__ Lv3 tn,
+// MODE 2: one block of 2 q warps per cell (the coarsest levels, rims of >= 1024 cells): warp w
+// takes the pair (population w / 2, side w % 2) the same way, thread 0 then assembles the
+// populations from the 2 q sums and collides.  (With one warp per leaf the 12 pairs of a
+// gap-5 leaf, 2 x 6 x 32 batches, were one dependent chain that set the duration of the
+// level's launch.)
+template <int MODE>
+__global__ void __launch_bounds__(MODE == 2 ? 512 : 128) k3_stream_collide(const __grid_constant__ Geo3 g, const __grid_constant__ Lv3 tn,
                                                          const __grid_constant__ Fl3 Fin, const __grid_constant__ Fl3 Fout,
                                                          const Sch3* sc, const __grid_constant__ Tab3 tb, int li,
                                                          const __grid_constant__ Aux3 aux)
@@ -635,27 +678,43 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
     const int fx = g.nx[lj], fy = g.ny[lj], fz = g.nz[lj];
     const double scale = ldexp(1.0, 3 * (li - lj));
     const int side_n = 1 << gap;
-    __shared__ double sv[4][32];
+    __shared__ double sv[MODE == 2 ? 16 : 4][32];
+    __shared__ double ssum[32];
+    __shared__ int sfb;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const bool writer = !WARP || lane == 0;
+    const bool writer = MODE == 0 || (MODE == 1 && lane == 0) || (MODE == 2 && threadIdx.x == 0);
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nth = (long long)gridDim.x * blockDim.x;
-    for (long long i = WARP ? tid >> 5 : tid; i < n; i += WARP ? nth >> 5 : nth)
+    const long long i0 = MODE == 0 ? tid : (MODE == 1 ? tid >> 5 : blockIdx.x);
+    const long long di = MODE == 0 ? nth : (MODE == 1 ? nth >> 5 : gridDim.x);
+    for (long long i = i0; i < n; i += di)
     {
         if (!(tn.kind[li][i] & K3_LEAF))
-            continue;
+            continue; // (block-uniform in MODE 2)
         int x, y, z;
         lin2xyz(g, li, i, x, y, z);
         double f[kQ3];
+        for (int h = 0; h < kQ3; ++h)
+            f[h] = 0.0;
         bool any_fb = false;
+        if (MODE == 2)
+        {
+            if (threadIdx.x == 0)
+                sfb = 0;
+            __syncthreads();
+        }
         for (int h = 0; h < q; ++h)
         {
+            if (MODE == 2 && h != (wid >> 1))
+                continue;
             const double* fl = Fin.f[li] + (long long)h * n;
             const double* ff = Fin.f[lj] + (long long)h * nf;
             const double fstar = fl[i];
             double sums[2] = {0.0, 0.0};
             for (int side = 0; side < 2; ++side)
             {
+                if (MODE == 2 && side != (wid & 1))
+                    continue;
                 const int ti = (gap * q + h) * 2 + side;
                 const int2 tr = tb.tidx[ti];
                 bool dom_ok, par_ok;
@@ -725,7 +784,7 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
                             v = __dadd_rn(v, sc->bc_add[face][h]);
                         return v;
                     };
-                    if (!WARP)
+                    if (MODE == 0)
                     {
                         for (int cx = lo[0]; cx < hi[0]; ++cx)
                             for (int cy = lo[1]; cy < hi[1]; ++cy)
@@ -754,8 +813,24 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
                 else
                     any_fb = any_fb || !(dom_ok && par_ok);
                 sums[side] = s;
+                if (MODE == 2 && lane == 0)
+                    ssum[wid] = s;
             }
-            f[h] = __dadd_rn(fstar, __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+            if (MODE != 2)
+                f[h] = __dadd_rn(fstar, __dmul_rn(scale, __dsub_rn(sums[0], sums[1])));
+        }
+        if (MODE == 2)
+        {
+            if (lane == 0 && any_fb)
+                atomicOr(&sfb, 1);
+            __syncthreads();
+            if (threadIdx.x == 0)
+            {
+                for (int h = 0; h < q; ++h)
+                    f[h] = __dadd_rn(Fin.f[li][(long long)h * n + i],
+                                     __dmul_rn(scale, __dsub_rn(ssum[2 * h], ssum[2 * h + 1])));
+                any_fb = sfb != 0;
+            }
         }
         // collision: m = M f, m' = (1 - s) m + s m^eq, f* = M^-1 m' (DenseMatrix::multiply order)
         double m[kQ3], meq[kQ3], mp[kQ3];
@@ -783,6 +858,8 @@ __global__ void __launch_bounds__(128) k3_stream_collide(const __grid_constant__
             atomicAdd(&aux.err[1], 1);
         if (writer && any_fb)
             atomicAdd(&aux.cnt[2 * kL3], 1);
+        if (MODE == 2)
+            __syncthreads(); // ssum / sfb are reused by the block's next leaf
     }
 }
 
@@ -983,6 +1060,7 @@ struct Engine3D {
     long long kcount = 0;
     std::string err_msg;
     int grid_cap = 148 * 16;
+    int block_gap = kBlockGap3; // MRLBM_E3_BLOCK_GAP
     // MRLBM_E3_PROF=1: an event after every kernel of the step, totals printed at destroy
     bool prof = false;
     std::vector<cudaEvent_t> pev;
@@ -1216,10 +1294,12 @@ int one_step(Engine3D* e)
     // K7 / K8: stream + collide
     for (int li = 0; li < nl; ++li)
     {
-        if (nl - 1 - li >= kWarpGap3)
-            k3_stream_collide<true><<<grid3(e, g.n[li] * 32, 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
+        if (nl - 1 - li >= e->block_gap)
+            k3_stream_collide<2><<<(int)std::min<long long>(g.n[li], e->grid_cap), 64 * g.q, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
+        else if (nl - 1 - li >= kWarpGap3)
+            k3_stream_collide<1><<<grid3(e, g.n[li] * 32, 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
         else
-            k3_stream_collide<false><<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
+            k3_stream_collide<0><<<grid3(e, g.n[li], 128), 128, 0, s>>>(g, tn, Fi, Fo, e->sch, tb, li, aux);
         pmark(e, "k3_stream_collide");
     }
     e->cur = vn;
@@ -1274,6 +1354,8 @@ int e3_create(const mrlbm_scheme_spec* sc, const mrlbm_run_config* rc, Engine3D*
         }
     Engine3D* e = new Engine3D();
     e->prof = std::getenv("MRLBM_E3_PROF") != nullptr;
+    if (const char* bg = std::getenv("MRLBM_E3_BLOCK_GAP"))
+        e->block_gap = std::max(2, std::atoi(bg));
     e->sc = *sc;
     e->rc = *rc;
     Geo3& g = e->geo;
