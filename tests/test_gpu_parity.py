@@ -107,3 +107,29 @@ def test_kernel_variant_parity(cid, J, env, monkeypatch):
         assert rel <= 1e-12
     gpu.close()
     ora.close()
+
+
+@pytest.mark.parametrize("cid,J", [(5, 7), (3, 6), (1, 8)])
+def test_profiling_modes_do_not_change_the_state(cid, J):
+    """mrlbm_set_profiling 0 (step graph), 1 (an event after every kernel, one stream) and 2
+    (phase events, the graph's forks active) evolve the state bit-identically; mode 2's phase
+    times add up to the step."""
+    from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
+    sc, rc = build_config(cid, J)
+    outs = []
+    for mode in (0, 1, 2):
+        s = Solver(sc, rc)
+        s.load_leaves(rc.j_max, finest_cells(sc, rc), initial_finest(cid, sc, rc))
+        s.commit()
+        s.set_profiling(mode)
+        st = s.step(15)
+        outs.append([s.read_leaves(lv) for lv in range(rc.j_min, rc.j_max + 1)])
+        phases = sum(st.ms_phase[i] for i in range(6))
+        if mode == 0:
+            assert phases == 0.0
+        else:
+            assert 0.5 * st.ms_total <= phases <= 1.05 * st.ms_total
+        s.close()
+    for other in outs[1:]:
+        for (ai, af), (bi, bf) in zip(outs[0], other):
+            assert np.array_equal(ai, bi) and np.array_equal(af.view(np.uint64), bf.view(np.uint64))
