@@ -66,3 +66,35 @@ def test_parity_full_size_config5():
     print(f"config 5 J=12: 2 steps bit-exact, {total} leaves")
     gpu.close()
     ora.close()
+
+
+@pytest.mark.gpu
+def test_uniform_mode_config3_baseline_size_vs_numpy():
+    """BASELINE config 3 "plus a uniform-mesh run (epsilon=0) at level 9": the GPU step in
+    uniform mode on the full 512 x 512 mesh against the independent numpy uniform LBM
+    (tests/uniform_ref.py), per step <= 1e-12 (north_star: "The same check runs in uniform-mesh
+    mode (epsilon=0)").  Both start each step from the same state, so the growth
+    of the (a, b) = (1, 1) instability does not enter."""
+    import numpy as np
+    from paper_2103_02903_b200 import Solver, build_config, finest_cells, initial_finest
+    from uniform_ref import UniformLBM
+    sc, rc = build_config(3, 9, 0.0)
+    f0 = initial_finest(3, sc, rc)
+    g = Solver(sc, rc)
+    g.load_leaves(rc.j_max, finest_cells(sc, rc), f0)
+    g.commit()
+    ref = UniformLBM(sc, rc, f0)
+    worst = 0.0
+    for k in range(24):
+        ref.f = g.read_leaves(rc.j_max)[1].reshape(ref.f.shape).copy()
+        g.step(1)
+        ref.step()
+        for lv in range(rc.j_min, rc.j_max):
+            assert g.level_count(lv) == 0, "epsilon = 0 must keep the full finest mesh"
+        _, f = g.read_leaves(rc.j_max)
+        scale = max(1.0, float(np.abs(ref.soa()).max()))
+        err = float(np.abs(f - ref.soa()).max()) / scale
+        assert err <= 1e-12, f"step {k}: {err}"
+        worst = max(worst, err)
+    g.close()
+    print(f"config 3 uniform mode at J=9: worst per-step difference {worst:.2e}")
